@@ -1,0 +1,779 @@
+/* qvts_oracle.c — TEST INFRASTRUCTURE ONLY (see qvts_oracle.h).
+ *
+ * Plain fp64 C, scalar loops, recursive depth-first tree.  Every function cites the passage
+ * of PAPER.md (arXiv 1810.00204) or the SURVEY.md reading it follows.  Nothing here is
+ * blocked, fused or reordered beyond what the cited definition states.
+ */
+#include "qvts_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define OR_NZ_GRID 16
+#define OR_ZERO_LIK 1e-300      /* SPEC.md:55, 96 (reading R25) */
+#define OR_FLAG_GAP 1e-6        /* SURVEY A.6 / north star "CDF gap under 1e-6" (R11) */
+
+struct or_model {
+    int nx, na, nz;
+    double gamma;
+    /* sparse clamped T rows: row (x,a) = entries [t_start[x*na+a], t_start[x*na+a+1]) */
+    int *t_start, *t_y;
+    double *t_p;
+    double *O;          /* [nx][nz] */
+    double *R;          /* [nx][na] */
+    /* grid-only data (is_grid = 1) */
+    int is_grid, H, W, goal;
+    int action_id[9];
+    uint8_t *occ;       /* [nx] */
+    int *sig;           /* [nx] */
+    double *Tp;         /* pre-clamp T'(x,a,k): [nx][na][9] */
+};
+
+/* ------------------------------------------------------------------------------------------ */
+/* Grid geometry ("N_4(x) = x").                        */
+static int stencil_dr(int k) { return k / 3 - 1; }
+static int stencil_dc(int k) { return k % 3 - 1; }
+
+/* occ(y) = 1 if y is off-map or m(y) = 1 (reading R4). Returns the neighbour cell or -1. */
+static int grid_neighbour(const or_model *m, int x, int k, int *occupied) {
+    int r = x / m->W + stencil_dr(k), c = x % m->W + stencil_dc(k);
+    if (r < 0 || r >= m->H || c < 0 || c >= m->W) { *occupied = 1; return -1; }
+    int y = r * m->W + c;
+    *occupied = m->occ[y] ? 1 : 0;
+    return y;
+}
+
+/* Ring of the 8 moving actions, clockwise from up-left (reading R3). */
+static const int RING[8] = {0, 1, 2, 5, 8, 7, 6, 3};
+
+/* Pre-clamp T'(x,a,.) over stencil offsets k (Fig. 2 unreadable -> reading R1/R2). */
+static void grid_tprime(int a_id, double p_int, double p_stay, double p_lat, double w[9]) {
+    for (int k = 0; k < 9; ++k) w[k] = 0.0;
+    if (a_id == 4) { w[4] = 1.0; return; }           /* stay is deterministic (R2) */
+    int i = 0;
+    while (RING[i] != a_id) ++i;
+    w[a_id] += p_int;
+    w[4] += p_stay;
+    w[RING[(i + 7) % 8]] += p_lat;
+    w[RING[(i + 1) % 8]] += p_lat;
+}
+
+static void model_free_arrays(or_model *m) {
+    free(m->t_start); free(m->t_y); free(m->t_p); free(m->O); free(m->R);
+    free(m->occ); free(m->sig); free(m->Tp);
+}
+
+void or_model_free(or_model *m) {
+    if (!m) return;
+    model_free_arrays(m);
+    free(m);
+}
+
+or_model *or_grid_model_create(int H, int W, const uint8_t *occ, int goal, unsigned action_mask,
+                               double p_int, double p_stay, double p_lat, double acc,
+                               double gamma, int *status) {
+    *status = OR_ERR_INVALID_MODEL;
+    if (H <= 0 || W <= 0 || !occ) return NULL;
+    if (goal < 0 || goal >= H * W || occ[goal]) return NULL;
+    if (p_int < 0 || p_stay < 0 || p_lat < 0 || fabs(p_int + p_stay + 2 * p_lat - 1.0) > 1e-9)
+        return NULL;
+    if (!(acc > 0.5 && acc <= 1.0)) return NULL;
+    if (!(gamma > 0.0 && gamma < 1.0)) return NULL;
+    action_mask &= 0x1FF;
+    if (!action_mask) return NULL;
+
+    or_model *m = (or_model *)calloc(1, sizeof(or_model));
+    m->is_grid = 1; m->H = H; m->W = W; m->goal = goal; m->gamma = gamma;
+    m->nx = H * W; m->nz = OR_NZ_GRID;
+    for (int k = 0; k < 9; ++k) if (action_mask & (1u << k)) m->action_id[m->na++] = k;
+    int nx = m->nx, na = m->na;
+    m->occ = (uint8_t *)malloc(nx);
+    for (int x = 0; x < nx; ++x) m->occ[x] = occ[x] ? 1 : 0;
+
+    /* Signature: bit k <-> sensor N_{2k+1} (reading R6; PAPER.md:336 sensors N1,N3,N5,N7). */
+    m->sig = (int *)malloc(sizeof(int) * nx);
+    for (int x = 0; x < nx; ++x) {
+        int s = 0, o;
+        for (int k = 0; k < 4; ++k) { grid_neighbour(m, x, 2 * k + 1, &o); s |= o << k; }
+        m->sig[x] = s;
+    }
+    /* O(x,z) = prod over 4 independent sensors, each correct w.p. acc (R7);
+     * occupied x: uniform (reading R5). */
+    m->O = (double *)malloc(sizeof(double) * nx * m->nz);
+    for (int x = 0; x < nx; ++x)
+        for (int z = 0; z < m->nz; ++z) {
+            double o = 1.0;
+            if (m->occ[x]) o = 1.0 / 16.0;
+            else
+                for (int k = 0; k < 4; ++k)
+                    o *= (((z >> k) & 1) == ((m->sig[x] >> k) & 1)) ? acc : (1.0 - acc);
+            m->O[x * m->nz + z] = o;
+        }
+    /* T' and clamped T (mass on occupied y is accumulated to x). */
+    m->Tp = (double *)calloc((size_t)nx * na * 9, sizeof(double));
+    m->t_start = (int *)malloc(sizeof(int) * (nx * na + 1));
+    m->t_y = (int *)malloc(sizeof(int) * nx * na * 9);
+    m->t_p = (double *)malloc(sizeof(double) * nx * na * 9);
+    int ne = 0;
+    for (int x = 0; x < nx; ++x)
+        for (int a = 0; a < na; ++a) {
+            double w[9];
+            grid_tprime(m->action_id[a], p_int, p_stay, p_lat, w);
+            memcpy(&m->Tp[((size_t)x * na + a) * 9], w, sizeof(w));
+            m->t_start[x * na + a] = ne;
+            if (m->occ[x]) {                       /* absorbing occupied rows (R5) */
+                m->t_y[ne] = x; m->t_p[ne] = 1.0; ++ne;
+                continue;
+            }
+            int row0 = ne;
+            for (int k = 0; k < 9; ++k) {
+                if (w[k] == 0.0) continue;
+                int o, y = grid_neighbour(m, x, k, &o);
+                if (k == 4) { y = x; o = 0; }
+                if (o) y = x;                       /* clamp */
+                int found = -1;
+                for (int e = row0; e < ne; ++e) if (m->t_y[e] == y) found = e;
+                if (found >= 0) m->t_p[found] += w[k];
+                else { m->t_y[ne] = y; m->t_p[ne] = w[k]; ++ne; }
+            }
+        }
+    m->t_start[nx * na] = ne;
+    /* Reward: r(y) in {-2,-1,0}; R(x,4) = -2 off-goal; otherwise
+     * R(x,a) = sum_y r(y) T'(x,a,y) with the PRE-clamp T', off-map y counted as occupied (R22). */
+    m->R = (double *)malloc(sizeof(double) * nx * na);
+    for (int x = 0; x < nx; ++x)
+        for (int a = 0; a < na; ++a) {
+            double v = 0.0;
+            if (m->occ[x]) v = 0.0;                 /* unused (R5) */
+            else if (m->action_id[a] == 4 && x != goal) v = -2.0;
+            else {
+                const double *w = &m->Tp[((size_t)x * na + a) * 9];
+                for (int k = 0; k < 9; ++k) {
+                    if (w[k] == 0.0) continue;
+                    int o, y = grid_neighbour(m, x, k, &o);
+                    if (k == 4) { y = x; o = 0; }
+                    double r = o ? -2.0 : (y == goal ? 0.0 : -1.0);
+                    v += r * w[k];
+                }
+            }
+            m->R[x * na + a] = v;
+        }
+    *status = OR_OK;
+    return m;
+}
+
+or_model *or_dense_model_create(int nx, int na, int nz, const double *T, const double *O,
+                                const double *R, double gamma, int *status) {
+    *status = OR_ERR_INVALID_MODEL;
+    if (nx <= 0 || na <= 0 || nz <= 0 || !(gamma > 0 && gamma < 1)) return NULL;
+    or_model *m = (or_model *)calloc(1, sizeof(or_model));
+    m->nx = nx; m->na = na; m->nz = nz; m->gamma = gamma;
+    for (int a = 0; a < na && a < 9; ++a) m->action_id[a] = a;
+    m->t_start = (int *)malloc(sizeof(int) * (nx * na + 1));
+    m->t_y = (int *)malloc(sizeof(int) * (size_t)nx * na * nx);
+    m->t_p = (double *)malloc(sizeof(double) * (size_t)nx * na * nx);
+    int ne = 0;
+    for (int x = 0; x < nx; ++x)
+        for (int a = 0; a < na; ++a) {
+            m->t_start[x * na + a] = ne;
+            double s = 0;
+            for (int y = 0; y < nx; ++y) {
+                double p = T[((size_t)x * na + a) * nx + y];
+                if (p < 0) { or_model_free(m); return NULL; }
+                s += p;
+                if (p > 0) { m->t_y[ne] = y; m->t_p[ne] = p; ++ne; }
+            }
+            if (fabs(s - 1.0) > 1e-9) { or_model_free(m); return NULL; }
+        }
+    m->t_start[nx * na] = ne;
+    m->O = (double *)malloc(sizeof(double) * nx * nz);
+    memcpy(m->O, O, sizeof(double) * nx * nz);
+    m->R = (double *)malloc(sizeof(double) * nx * na);
+    memcpy(m->R, R, sizeof(double) * nx * na);
+    *status = OR_OK;
+    return m;
+}
+
+int or_num_states(const or_model *m) { return m->nx; }
+int or_num_actions(const or_model *m) { return m->na; }
+int or_num_obs(const or_model *m) { return m->nz; }
+int or_action_id(const or_model *m, int a) { return m->action_id[a]; }
+double or_O(const or_model *m, int x, int z) { return m->O[x * m->nz + z]; }
+double or_R(const or_model *m, int x, int a) { return m->R[x * m->na + a]; }
+int or_sig(const or_model *m, int x) { return m->is_grid ? m->sig[x] : 0; }
+int or_occ(const or_model *m, int x) { return m->is_grid ? m->occ[x] : 0; }
+double or_T(const or_model *m, int x, int a, int y) {
+    double p = 0.0;
+    for (int e = m->t_start[x * m->na + a]; e < m->t_start[x * m->na + a + 1]; ++e)
+        if (m->t_y[e] == y) p += m->t_p[e];
+    return p;
+}
+double or_Tprime(const or_model *m, int x, int a, int k) {
+    return m->is_grid ? m->Tp[((size_t)x * m->na + a) * 9 + k] : 0.0;
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* Philox4x32-10 (Salmon et al. 2011).                                   */
+void or_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+    uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3];
+    uint32_t k0 = key[0], k1 = key[1];
+    for (int round = 0; round < 10; ++round) {
+        if (round > 0) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+        uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+        uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+        uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        uint32_t n0 = hi1 ^ c1 ^ k0, n1 = lo1, n2 = hi0 ^ c3 ^ k1, n3 = lo0;
+        c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* A.4: u = ((w >> 8) + 0.5) * 2^-24 */
+double or_uniform(uint32_t w) { return ((double)(w >> 8) + 0.5) * (1.0 / 16777216.0); }
+
+/* A.5: C_k = sum_{i<=k} p_i ascending in fp64; result = min{k : u*C_{K-1} < C_k}.
+ * A.6: flag when min_{k<K-1} |u*C_{K-1} - C_k| < 1e-6. */
+int or_inverse_cdf(const double *p, int K, double u, int *flag) {
+    double *C = (double *)malloc(sizeof(double) * K);
+    double s = 0.0;
+    for (int k = 0; k < K; ++k) { s += p[k]; C[k] = s; }
+    double t = u * C[K - 1];
+    int res = K - 1;
+    for (int k = 0; k < K; ++k) if (t < C[k]) { res = k; break; }
+    if (flag) {
+        *flag = 0;
+        for (int k = 0; k < K - 1; ++k) if (fabs(t - C[k]) < OR_FLAG_GAP) *flag = 1;
+    }
+    free(C);
+    return res;
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* Eq. 3 inner sum, scatter form: bbar(y) = sum_x T(x,a,y) b(x).          */
+void or_predict(const or_model *m, const double *b, int a, double *bbar) {
+    for (int y = 0; y < m->nx; ++y) bbar[y] = 0.0;
+    for (int x = 0; x < m->nx; ++x) {
+        if (b[x] == 0.0) continue;
+        for (int e = m->t_start[x * m->na + a]; e < m->t_start[x * m->na + a + 1]; ++e)
+            bbar[m->t_y[e]] += m->t_p[e] * b[x];
+    }
+}
+
+/* Normaliser of Eq. 3: P(z|b,a) = sum_y O(y,z) bbar(y). */
+void or_marginal(const or_model *m, const double *bbar, double *P) {
+    for (int z = 0; z < m->nz; ++z) {
+        double s = 0.0;
+        for (int y = 0; y < m->nx; ++y) s += m->O[y * m->nz + z] * bbar[y];
+        P[z] = s;
+    }
+}
+
+/* R(b,a) = sum_x R(x,a) b(x). */
+double or_belief_reward(const or_model *m, const double *b, int a) {
+    double s = 0.0;
+    for (int x = 0; x < m->nx; ++x) s += m->R[x * m->na + a] * b[x];
+    return s;
+}
+
+/* Eq. 3: Phi(b,a,z)(x') = O(x',z) sum_x T(x,a,x') b(x) / P(z|b,a). */
+int or_belief_update(const or_model *m, const double *b, int a, int z, double *out, double *p_obs) {
+    if (a < 0 || a >= m->na || z < 0 || z >= m->nz) return OR_ERR_INVALID_ARG;
+    double *bbar = (double *)malloc(sizeof(double) * m->nx);
+    double *P = (double *)malloc(sizeof(double) * m->nz);
+    or_predict(m, b, a, bbar);
+    or_marginal(m, bbar, P);
+    double pz = P[z];
+    if (p_obs) *p_obs = pz;
+    int st = OR_OK;
+    if (pz <= OR_ZERO_LIK) st = OR_ERR_ZERO_LIKELIHOOD;
+    else
+        for (int y = 0; y < m->nx; ++y) out[y] = m->O[y * m->nz + z] * bbar[y] / pz;
+    free(bbar); free(P);
+    return st;
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* MDP value iteration ("self-implemented value iteration"; reading R24):
+ * synchronous Jacobi from V0 = 0, Q_k(x,a) = R(x,a) + gamma sum_y T(x,a,y) V_k(y),
+ * V_{k+1} = max_a Q_k, stop when max|V_{k+1} - V_k| < eps; then Q = R + gamma T V.
+ * Occupied grid cells: V = Q = 0 (reading R5). */
+static double bellman_q(const or_model *m, const double *V, int x, int a) {
+    double s = 0.0;
+    for (int e = m->t_start[x * m->na + a]; e < m->t_start[x * m->na + a + 1]; ++e)
+        s += m->t_p[e] * V[m->t_y[e]];
+    return m->R[x * m->na + a] + m->gamma * s;
+}
+
+int or_value_iteration(const or_model *m, double eps, int max_sweeps, double *V, double *Q,
+                       int *sweeps, double *resid) {
+    int nx = m->nx, na = m->na;
+    double *Vn = (double *)malloc(sizeof(double) * nx);
+    for (int x = 0; x < nx; ++x) V[x] = 0.0;
+    int k = 0, st = OR_ERR_NOT_CONVERGED;
+    double res = INFINITY;
+    while (k < max_sweeps) {
+        res = 0.0;
+        for (int x = 0; x < nx; ++x) {
+            if (m->is_grid && m->occ[x]) { Vn[x] = 0.0; continue; }
+            double best = -INFINITY;
+            for (int a = 0; a < na; ++a) {
+                double q = bellman_q(m, V, x, a);
+                if (q > best) best = q;
+            }
+            Vn[x] = best;
+            double d = fabs(best - V[x]);
+            if (d > res) res = d;
+        }
+        memcpy(V, Vn, sizeof(double) * nx);
+        ++k;
+        if (res < eps) { st = OR_OK; break; }
+    }
+    for (int a = 0; a < na; ++a)
+        for (int x = 0; x < nx; ++x)
+            Q[(size_t)a * nx + x] = (m->is_grid && m->occ[x]) ? 0.0 : bellman_q(m, V, x, a);
+    if (sweeps) *sweeps = k;
+    if (resid) *resid = res;
+    free(Vn);
+    return st;
+}
+
+/* Eq. 4 with one alpha-vector per action, alpha_a = Q(.,a) (north star Q_MDP leaf; R14). */
+double or_qmdp_value(const or_model *m, const double *Q, const double *b, int *argmax) {
+    double best = -INFINITY;
+    int arg = 0;
+    for (int a = 0; a < m->na; ++a) {
+        double s = 0.0;
+        for (int x = 0; x < m->nx; ++x) s += b[x] * Q[(size_t)a * m->nx + x];
+        if (s > best) { best = s; arg = a; }            /* ties -> lowest index (R16) */
+    }
+    if (argmax) *argmax = arg;
+    return best;
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* Trace storage.                                                                             */
+typedef struct { uint64_t path; int32_t level, action; double R, Q; double P[16]; uint16_t cnt[16]; } qrec_t;
+typedef struct { uint64_t path; int32_t level, z, f; double V; int64_t bidx; } vrec_t;
+
+struct or_trace {
+    int capture, n;
+    int64_t nq, capq, nv, capv, nb, capb, nx;
+    qrec_t *q; vrec_t *v;
+    uint8_t *z, *flag;           /* [capq][n] */
+    double *bel;                 /* [capb][nx] */
+};
+
+or_trace *or_trace_new(int capture_beliefs) {
+    or_trace *t = (or_trace *)calloc(1, sizeof(or_trace));
+    t->capture = capture_beliefs;
+    return t;
+}
+void or_trace_free(or_trace *t) {
+    if (!t) return;
+    free(t->q); free(t->v); free(t->z); free(t->flag); free(t->bel); free(t);
+}
+int64_t or_trace_nq(const or_trace *t) { return t->nq; }
+int64_t or_trace_nv(const or_trace *t) { return t->nv; }
+int32_t or_trace_nsamples(const or_trace *t) { return t->n; }
+
+static int64_t trace_add_q(or_trace *t, int n) {
+    if (t->nq == t->capq) {
+        t->capq = t->capq ? 2 * t->capq : 64;
+        t->q = (qrec_t *)realloc(t->q, sizeof(qrec_t) * t->capq);
+        t->z = (uint8_t *)realloc(t->z, (size_t)t->capq * (n > 0 ? n : 1));
+        t->flag = (uint8_t *)realloc(t->flag, (size_t)t->capq * (n > 0 ? n : 1));
+    }
+    return t->nq++;
+}
+static int64_t trace_add_v(or_trace *t) {
+    if (t->nv == t->capv) {
+        t->capv = t->capv ? 2 * t->capv : 64;
+        t->v = (vrec_t *)realloc(t->v, sizeof(vrec_t) * t->capv);
+    }
+    return t->nv++;
+}
+static int64_t trace_add_belief(or_trace *t, const double *b) {
+    if (t->nb == t->capb) {
+        t->capb = t->capb ? 2 * t->capb : 16;
+        t->bel = (double *)realloc(t->bel, sizeof(double) * t->capb * t->nx);
+    }
+    memcpy(&t->bel[t->nb * t->nx], b, sizeof(double) * t->nx);
+    return t->nb++;
+}
+
+void or_trace_export_q(const or_trace *t, uint64_t *path, int32_t *level, int32_t *action,
+                       double *R, double *P, uint16_t *cnt, double *Q, uint8_t *z, uint8_t *flag) {
+    for (int64_t i = 0; i < t->nq; ++i) {
+        path[i] = t->q[i].path; level[i] = t->q[i].level; action[i] = t->q[i].action;
+        R[i] = t->q[i].R; Q[i] = t->q[i].Q;
+        for (int k = 0; k < 16; ++k) { P[i * 16 + k] = t->q[i].P[k]; cnt[i * 16 + k] = t->q[i].cnt[k]; }
+    }
+    if (t->n > 0) {
+        memcpy(z, t->z, (size_t)t->nq * t->n);
+        memcpy(flag, t->flag, (size_t)t->nq * t->n);
+    }
+}
+void or_trace_export_v(const or_trace *t, uint64_t *path, int32_t *level, double *V, int32_t *zobs,
+                       int32_t *f, int64_t *belief_idx) {
+    for (int64_t i = 0; i < t->nv; ++i) {
+        path[i] = t->v[i].path; level[i] = t->v[i].level; V[i] = t->v[i].V;
+        zobs[i] = t->v[i].z; f[i] = t->v[i].f; belief_idx[i] = t->v[i].bidx;
+    }
+}
+void or_trace_belief(const or_trace *t, int64_t bi, double *out) {
+    memcpy(out, &t->bel[bi * t->nx], sizeof(double) * t->nx);
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* Plan step: SURVEY §8(c) O6.  Alg. 2 creates all |A| Q-nodes of a V-node;
+ * Alg. 3 draws n observations (Alg. 4 distribution, reading R9, keyed by
+ * tree path per Appendix A), keeps the unique ones with their frequency as weight
+ * (R12), builds one child per unique z with Eq. 3, and updates q
+ * (Alg. 6 with gamma, reading R13); Alg. 7 takes V = max_a Q.  Leaves use Q_MDP (R14).     */
+typedef struct {
+    const or_model *m;
+    const double *Q;
+    const or_plan_cfg *cfg;
+    or_trace *tr;
+} plan_ctx;
+
+static uint64_t qpath_of(uint64_t vpath, int level, int a_id) {
+    return vpath | ((uint64_t)(a_id + 1) << (8 * level));
+}
+static uint64_t vpath_of(uint64_t qpath, int level, int z) {
+    return qpath | ((uint64_t)z << (8 * level + 4));
+}
+
+static int replay_lookup(const or_plan_cfg *cfg, uint64_t qpath, int j, int *z) {
+    for (int i = 0; i < cfg->n_replay; ++i)
+        if (cfg->replay_path[i] == qpath && cfg->replay_j[i] == j) { *z = cfg->replay_z[i]; return 1; }
+    return 0;
+}
+
+/* Draws of one Q-node (Appendix A.2-A.6); returns the draws, flags and counts. */
+static void qnode_draws(const or_plan_cfg *cfg, int nz, const double *P, uint64_t qpath,
+                        uint8_t *zs, uint8_t *flags, uint16_t *cnt) {
+    double C[16];
+    double s = 0.0;
+    for (int k = 0; k < nz; ++k) { s += P[k]; C[k] = s; cnt[k] = 0; }
+    for (int j = 0; j < cfg->n_samples; ++j) {
+        uint32_t ctr[4] = {(uint32_t)j, (uint32_t)qpath, (uint32_t)(qpath >> 32), cfg->step};
+        uint32_t key[2] = {cfg->seed, cfg->episode}, w[4];
+        or_philox4x32_10(ctr, key, w);
+        double u = or_uniform(w[0]);
+        int flag;
+        int z = or_inverse_cdf(P, nz, u, &flag);
+        int zr;
+        if (flag && cfg->n_replay > 0 && replay_lookup(cfg, qpath, j, &zr) && zr != z) {
+            /* accept the replayed category only if it borders a near boundary (c.5 step 3) */
+            double t = u * C[nz - 1];
+            for (int k = 0; k < nz - 1; ++k) {
+                if (fabs(t - C[k]) >= OR_FLAG_GAP) continue;
+                int lo = nz - 1, hi = nz - 1;
+                for (int i = 0; i < nz; ++i) if (C[i] >= C[k]) { lo = i; break; }
+                for (int i = 0; i < nz; ++i) if (C[i] > C[k]) { hi = i; break; }
+                if (zr == lo || zr == hi) { z = zr; break; }
+            }
+        }
+        zs[j] = (uint8_t)z;
+        flags[j] = (uint8_t)flag;
+        cnt[z]++;
+    }
+}
+
+static double vnode_rec(plan_ctx *c, const double *b, uint64_t vpath, int level, double *qvals);
+
+/* Q-node at `level` (its parent V-node is at `level`), with levels_left = depth - level. */
+static double qnode_rec(plan_ctx *c, const double *b, int a, uint64_t qpath, int level) {
+    const or_model *m = c->m;
+    const or_plan_cfg *cfg = c->cfg;
+    int nx = m->nx, nz = m->nz, n = cfg->n_samples;
+    double *bbar = (double *)malloc(sizeof(double) * nx);
+    double *child = (double *)malloc(sizeof(double) * nx);
+    double P[16];
+    uint16_t cnt[16];
+    uint8_t *zs = (uint8_t *)calloc(n > 0 ? n : 1, 1), *flags = (uint8_t *)calloc(n > 0 ? n : 1, 1);
+    or_predict(m, b, a, bbar);                            /* Eq. 3 inner sum */
+    or_marginal(m, bbar, P);                              /* P(z|b,a)       */
+    double R = or_belief_reward(m, b, a);                 /* R(b,a)         */
+    if (cfg->mode == OR_MODE_BRUTE) { for (int z = 0; z < nz; ++z) cnt[z] = 0; }
+    else qnode_draws(cfg, nz, P, qpath, zs, flags, cnt);  /* Alg. 3 l.4-5   */
+    double acc = 0.0;
+    for (int z = 0; z < nz; ++z) {                        /* unique z ascending (R17) */
+        int take = (cfg->mode == OR_MODE_BRUTE) ? (P[z] > OR_ZERO_LIK) : (cnt[z] > 0);
+        if (!take) continue;
+        double w = (cfg->mode == OR_MODE_FREQ) ? (double)cnt[z] / (double)n : P[z];
+        for (int y = 0; y < nx; ++y) child[y] = m->O[y * nz + z] * bbar[y] / P[z];  /* Eq. 3 */
+        uint64_t vpath = vpath_of(qpath, level, z);
+        double V;
+        int64_t bidx = -1;
+        if (c->tr && c->tr->capture && level + 1 < cfg->depth) bidx = trace_add_belief(c->tr, child);
+        if (level + 1 == cfg->depth) V = or_qmdp_value(m, c->Q, child, NULL);       /* leaf */
+        else V = vnode_rec(c, child, vpath, level + 1, NULL);
+        if (c->tr) {
+            int64_t i = trace_add_v(c->tr);
+            vrec_t *r = &c->tr->v[i];
+            r->path = vpath; r->level = level + 1; r->z = z; r->f = cnt[z]; r->V = V; r->bidx = bidx;
+        }
+        acc += w * V;
+    }
+    double Qv = R + m->gamma * acc;                      /* Alg. 6 with gamma (R13) */
+    if (c->tr) {
+        int64_t i = trace_add_q(c->tr, n);
+        qrec_t *r = &c->tr->q[i];
+        r->path = qpath; r->level = level; r->action = m->action_id[a]; r->R = R; r->Q = Qv;
+        for (int k = 0; k < 16; ++k) { r->P[k] = k < nz ? P[k] : 0.0; r->cnt[k] = k < nz ? cnt[k] : 0; }
+        if (n > 0) {
+            memcpy(&c->tr->z[i * n], zs, n);
+            memcpy(&c->tr->flag[i * n], flags, n);
+        }
+    }
+    free(bbar); free(child); free(zs); free(flags);
+    return Qv;
+}
+
+/* V-node: Alg. 2 expansion over all actions, Alg. 7 V = max_a Q (ties -> lowest, R16). */
+static double vnode_rec(plan_ctx *c, const double *b, uint64_t vpath, int level, double *qvals) {
+    const or_model *m = c->m;
+    double best = -INFINITY;
+    for (int a = 0; a < m->na; ++a) {
+        double q = qnode_rec(c, b, a, qpath_of(vpath, level, m->action_id[a]), level);
+        if (qvals) qvals[a] = q;
+        if (q > best) best = q;
+    }
+    return best;
+}
+
+double or_vnode_value(const or_model *m, const double *Q, const double *b, uint64_t vpath, int level,
+                      const or_plan_cfg *cfg, double *qvals) {
+    plan_ctx c = {m, Q, cfg, NULL};
+    if (level >= cfg->depth) return or_qmdp_value(m, Q, b, NULL);
+    return vnode_rec(&c, b, vpath, level, qvals);
+}
+
+int or_plan(const or_model *m, const double *Q, const double *b0, const or_plan_cfg *cfg,
+            int *action, double *qroot, or_trace *trace) {
+    if (!m->is_grid || cfg->depth < 0 || cfg->depth > 8 || cfg->n_samples < 0 ||
+        (cfg->mode != OR_MODE_BRUTE && cfg->n_samples < 1) || cfg->n_samples > 65535)
+        return OR_ERR_INVALID_ARG;
+    int na = m->na;
+    if (cfg->depth == 0) {                                /* plain Q_MDP on the root (R15) */
+        for (int a = 0; a < na; ++a) {
+            double s = 0.0;
+            for (int x = 0; x < m->nx; ++x) s += b0[x] * Q[(size_t)a * m->nx + x];
+            qroot[a] = s;
+        }
+    } else if (trace) {
+        trace->nx = m->nx;
+        trace->n = cfg->n_samples;
+        plan_ctx c = {m, Q, cfg, trace};
+        vnode_rec(&c, b0, 0, 0, qroot);
+    } else {
+#ifdef _OPENMP
+        int th = cfg->threads > 0 ? cfg->threads : omp_get_max_threads();
+#pragma omp parallel for schedule(dynamic, 1) num_threads(th)
+#endif
+        for (int a = 0; a < na; ++a) {
+            plan_ctx c = {m, Q, cfg, NULL};
+            qroot[a] = qnode_rec(&c, b0, a, qpath_of(0, 0, m->action_id[a]), 0);
+        }
+    }
+    int arg = 0;
+    for (int a = 1; a < na; ++a) if (qroot[a] > qroot[arg]) arg = a;
+    *action = m->action_id[arg];
+    return OR_OK;
+}
+
+int or_qnode_sample(const or_model *m, const double *b, int a, uint64_t qpath, const or_plan_cfg *cfg,
+                    double *P, double *R, uint8_t *z, uint8_t *flag, uint16_t *cnt) {
+    double *bbar = (double *)malloc(sizeof(double) * m->nx);
+    or_predict(m, b, a, bbar);
+    or_marginal(m, bbar, P);
+    *R = or_belief_reward(m, b, a);
+    qnode_draws(cfg, m->nz, P, qpath, z, flag, cnt);
+    free(bbar);
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* Baselines: belief mode, MDP table lookup, A* on the mode.                   */
+int or_belief_mode(const or_model *m, const double *b) {
+    int arg = 0;
+    for (int x = 1; x < m->nx; ++x) if (b[x] > b[arg]) arg = x;   /* ties -> lowest (R30) */
+    return arg;
+}
+
+static int has_diagonal(const or_model *m) {
+    for (int a = 0; a < m->na; ++a) {
+        int k = m->action_id[a];
+        if (k != 4 && stencil_dr(k) != 0 && stencil_dc(k) != 0) return 1;
+    }
+    return 0;
+}
+
+static int astar_run(const or_model *m, int start, int *first_k) {
+    /* Unit-cost A* over free cells with the model's moving actions (reading R29); heuristic
+     * Chebyshev when diagonals are allowed (admissible for unit diagonal cost), else Manhattan.
+     * Priority (f, cell) lexicographic; neighbours expanded in ascending stencil id. */
+    int nx = m->nx, W = m->W;
+    int diag = has_diagonal(m);
+    int gr = m->goal / W, gc = m->goal % W;
+    int *g = (int *)malloc(sizeof(int) * nx), *par = (int *)malloc(sizeof(int) * nx);
+    char *closed = (char *)calloc(nx, 1);
+    int64_t *heap = (int64_t *)malloc(sizeof(int64_t) * (size_t)nx * 9 + 16);
+    int hn = 0;
+    for (int x = 0; x < nx; ++x) { g[x] = -1; par[x] = -1; }
+#define HKEY(f, x) (((int64_t)(f) << 32) | (int64_t)(x))
+#define HEUR(x) (diag ? (abs((x) / W - gr) > abs((x) % W - gc) ? abs((x) / W - gr) : abs((x) % W - gc)) \
+                      : abs((x) / W - gr) + abs((x) % W - gc))
+    g[start] = 0;
+    heap[hn++] = HKEY(HEUR(start), start);
+    int found = 0;
+    while (hn > 0) {
+        int64_t top = heap[0];
+        heap[0] = heap[--hn];
+        for (int i = 0;;) {                                /* sift down */
+            int l = 2 * i + 1, r = l + 1, s = i;
+            if (l < hn && heap[l] < heap[s]) s = l;
+            if (r < hn && heap[r] < heap[s]) s = r;
+            if (s == i) break;
+            int64_t tmp = heap[i]; heap[i] = heap[s]; heap[s] = tmp; i = s;
+        }
+        int x = (int)(top & 0xFFFFFFFF);
+        if (closed[x]) continue;
+        closed[x] = 1;
+        if (x == m->goal) { found = 1; break; }
+        for (int a = 0; a < m->na; ++a) {
+            int k = m->action_id[a];
+            if (k == 4) continue;
+            int o, y = grid_neighbour(m, x, k, &o);
+            if (o || closed[y]) continue;
+            if (g[y] < 0 || g[x] + 1 < g[y]) {
+                g[y] = g[x] + 1; par[y] = x;
+                int i = hn++;
+                heap[i] = HKEY(g[y] + HEUR(y), y);
+                while (i > 0 && heap[(i - 1) / 2] > heap[i]) {   /* sift up */
+                    int p = (i - 1) / 2;
+                    int64_t tmp = heap[i]; heap[i] = heap[p]; heap[p] = tmp; i = p;
+                }
+            }
+        }
+    }
+#undef HKEY
+#undef HEUR
+    int len = -1;
+    if (found) {
+        len = g[m->goal];
+        int y = m->goal;
+        if (y != start) {
+            while (par[y] != start) y = par[y];
+            int dr = y / W - start / W, dc = y % W - start % W;
+            *first_k = 3 * (dr + 1) + (dc + 1);
+        } else *first_k = 4;
+    }
+    free(g); free(par); free(closed); free(heap);
+    return len;
+}
+
+int or_astar_length(const or_model *m, int start) {
+    int k;
+    return astar_run(m, start, &k);
+}
+
+int or_astar_action(const or_model *m, int start) {
+    int k = 4;
+    if (astar_run(m, start, &k) < 0) k = 4;
+    for (int a = 0; a < m->na; ++a) if (m->action_id[a] == k) return k;
+    return m->action_id[0];
+}
+
+/* Alg. 4 literal: x ~ b, x' ~ P(x'|x,a) (clamped T), z ~ P(z|x'),
+ * using Philox words 1..3 of one call. */
+int or_ancestral_sample(const or_model *m, const double *b, int a, const uint32_t ctr[4],
+                        const uint32_t key[2]) {
+    uint32_t w[4];
+    or_philox4x32_10(ctr, key, w);
+    int x = or_inverse_cdf(b, m->nx, or_uniform(w[1]), NULL);
+    int e0 = m->t_start[x * m->na + a], e1 = m->t_start[x * m->na + a + 1];
+    double *p = (double *)malloc(sizeof(double) * (e1 - e0));
+    for (int e = e0; e < e1; ++e) p[e - e0] = m->t_p[e];
+    int xp = m->t_y[e0 + or_inverse_cdf(p, e1 - e0, or_uniform(w[2]), NULL)];
+    free(p);
+    return or_inverse_cdf(&m->O[xp * m->nz], m->nz, or_uniform(w[3]), NULL);
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* Closed-loop episodes (Alg. 1 outer loop PAPER.md:149-165; Eq. 1 return PAPER.md:36-42;
+ * termination/collision readings R26/R27; environment draws per Appendix A.2). */
+int or_run_episode(const or_model *m, const double *Q, const double *b0, const or_episode_cfg *cfg,
+                   or_episode_record *rec, int32_t *log_a, int32_t *log_z, int32_t *log_x) {
+    if (!m->is_grid) return OR_ERR_INVALID_ARG;
+    int nx = m->nx, na = m->na;
+    double *b = (double *)malloc(sizeof(double) * nx), *bn = (double *)malloc(sizeof(double) * nx);
+    double *qroot = (double *)malloc(sizeof(double) * na);
+    memcpy(b, b0, sizeof(double) * nx);
+    uint32_t key[2] = {cfg->seed, cfg->episode}, w[4];
+    uint32_t ctr0[4] = {0, 0, 0, 0};
+    or_philox4x32_10(ctr0, key, w);
+    int x = or_inverse_cdf(b0, nx, or_uniform(w[2]), NULL);      /* x0 ~ b0 */
+    memset(rec, 0, sizeof(*rec));
+    rec->x0 = x;
+    rec->outcome = 2;
+    double disc = 1.0;
+    int streak = 0, s;
+    for (s = 0; s < cfg->max_steps; ++s) {
+        int a_id;
+        if (cfg->planner == OR_PLANNER_QVTS) {
+            or_plan_cfg pc;
+            memset(&pc, 0, sizeof(pc));
+            pc.depth = cfg->depth; pc.n_samples = cfg->n_samples; pc.mode = OR_MODE_FREQ;
+            pc.seed = cfg->seed; pc.step = (uint32_t)s; pc.episode = cfg->episode; pc.threads = 1;
+            or_plan(m, Q, b, &pc, &a_id, qroot, NULL);
+        } else if (cfg->planner == OR_PLANNER_MDP) {
+            int xm = or_belief_mode(m, b), arg = 0;
+            for (int a = 1; a < na; ++a)
+                if (Q[(size_t)a * nx + xm] > Q[(size_t)arg * nx + xm]) arg = a;
+            a_id = m->action_id[arg];
+        } else {
+            a_id = or_astar_action(m, or_belief_mode(m, b));
+        }
+        int a = 0;
+        while (m->action_id[a] != a_id) ++a;
+        uint32_t ctr[4] = {0, 0, 0, (uint32_t)s};
+        or_philox4x32_10(ctr, key, w);
+        /* true motion y ~ T'(x,a,.) in stencil order; blocked -> collision, stay */
+        int k = or_inverse_cdf(&m->Tp[((size_t)x * na + a) * 9], 9, or_uniform(w[0]), NULL);
+        int xn = x;
+        if (k != 4) {
+            int o, y = grid_neighbour(m, x, k, &o);
+            if (o) rec->collisions++;
+            else xn = y;
+        }
+        int z = or_inverse_cdf(&m->O[xn * m->nz], m->nz, or_uniform(w[1]), NULL);
+        rec->disc_return += disc * m->R[x * na + a];
+        disc *= m->gamma;
+        double pz;
+        int st = or_belief_update(m, b, a, z, bn, &pz);
+        if (log_a) log_a[s] = a_id;
+        if (log_z) log_z[s] = z;
+        if (log_x) log_x[s] = xn;
+        x = xn;
+        if (st != OR_OK) { rec->outcome = 3; ++s; break; }
+        memcpy(b, bn, sizeof(double) * nx);
+        streak = (a_id == 4) ? streak + 1 : 0;
+        if (cfg->stop_patience > 0 && streak >= cfg->stop_patience) {
+            rec->outcome = (x == m->goal) ? 0 : 1;
+            ++s;
+            break;
+        }
+    }
+    rec->steps = s;
+    rec->x_final = x;
+    free(b); free(bn); free(qroot);
+    return OR_OK;
+}

@@ -1,0 +1,411 @@
+"""Pins of the fp64 CPU oracle against values and properties the paper and mathematics fix
+(SURVEY.md §8(c) c.4).  CPU only."""
+import json
+import os
+from collections import deque
+
+import numpy as np
+import pytest
+
+import oracle as O
+import workloads as W
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "pins.json")))
+
+
+def open3x3(goal=0, blocked=()):
+    occ = np.zeros(9, np.uint8)
+    for b in blocked:
+        occ[b] = 1
+    return W.GridMap(3, 3, occ, goal)
+
+
+def dense_T(m):
+    T = np.zeros((m.nx, m.na, m.nx))
+    for x in range(m.nx):
+        for a in range(m.na):
+            for y in range(m.nx):
+                T[x, a, y] = m.T(x, a, y)
+    return T
+
+
+# ---- P1 RNG ------------------------------------------------------------------------------
+def test_philox_known_answers():
+    for v in GOLD["philox_kat"]["vectors"]:
+        ctr = [int(h, 16) for h in v["ctr"]]
+        key = [int(h, 16) for h in v["key"]]
+        out = O.philox(ctr, key)
+        assert [f"{w:08x}" for w in out] == v["out"]
+
+
+def test_uniform_and_inverse_cdf():
+    assert O.uniform(0) == 0.5 * 2.0 ** -24
+    assert O.uniform(0xFFFFFFFF) == 1.0 - 0.5 * 2.0 ** -24
+    # strict '<' never picks a zero-weight category (Appendix A.5)
+    p = [0.0, 0.5, 0.0, 0.5]
+    assert O.inverse_cdf(p, 1e-9)[0] == 1
+    assert O.inverse_cdf(p, 0.5)[0] == 3
+    assert O.inverse_cdf(p, 0.4999999)[0] == 1
+    assert O.inverse_cdf(p, 0.4999999)[1]       # within 1e-6 of the boundary -> flagged
+    assert not O.inverse_cdf(p, 0.3)[1]
+
+
+# ---- P2 model tables ---------------------------------------------------------------------
+def test_transition_examples():
+    g = GOLD["transition_up_open"]
+    m = O.Model.grid(open3x3(goal=8))
+    up = m.action_ids.index(1)
+    assert m.T(4, up, 1) == pytest.approx(g["T_up_N1"], abs=1e-15)
+    assert m.T(4, up, 4) == pytest.approx(g["T_up_stay"], abs=1e-15)
+    assert m.T(4, up, 0) == pytest.approx(g["T_up_N0"], abs=1e-15)
+    assert m.T(4, up, 2) == pytest.approx(g["T_up_N2"], abs=1e-15)
+    mb = O.Model.grid(open3x3(goal=8, blocked=(1,)))
+    assert mb.T(4, up, 4) == pytest.approx(g["T_up_stay_N1_blocked"], abs=1e-15)
+    assert mb.T(4, up, 0) == pytest.approx(0.05, abs=1e-15)
+    # diagonal laterals are ring neighbours (R3): up-left (0) -> {3, 1}
+    ul = m.action_ids.index(0)
+    assert m.T(4, ul, 3) == pytest.approx(0.05) and m.T(4, ul, 1) == pytest.approx(0.05)
+    assert m.T(4, ul, 0) == pytest.approx(0.8) and m.T(4, ul, 4) == pytest.approx(0.1)
+    # stay is deterministic (R2)
+    assert m.T(4, m.action_ids.index(4), 4) == 1.0
+
+
+def test_table_invariants_random_map():
+    gm = W.random_map(9, 11, 0.25, seed=7)
+    m = O.Model.grid(gm)
+    T = dense_T(m)
+    assert np.allclose(T.sum(axis=2), 1.0, atol=1e-12)
+    occ = gm.occupancy.astype(bool)
+    free = ~occ
+    # T(x, a, y) = 0 for occupied y and free x
+    assert np.all(T[np.ix_(free, np.arange(m.na), occ)] == 0.0)
+    Ot = m.O_table()
+    assert np.allclose(Ot.sum(axis=1), 1.0, atol=1e-12)
+
+
+def test_observation_examples():
+    g = GOLD["observation"]
+    m = O.Model.grid(open3x3(goal=8))
+    assert m.sig(4) == 0
+    assert m.O(4, 0) == pytest.approx(g["all_free_z0"], abs=1e-15)
+    assert m.O(4, 1) == pytest.approx(g["all_free_z1"], abs=1e-15)
+    # corner (0,0): up (bit0) and left (bit1) off-map read occupied
+    assert m.sig(0) == 0b0011
+    assert m.sig(8) == 0b1100
+    # acc = 1 -> exactly one observation with likelihood 1
+    m1 = O.Model.grid(open3x3(goal=8), acc=1.0)
+    row = np.array([m1.O(4, z) for z in range(16)])
+    assert row[0] == 1.0 and row.sum() == 1.0
+
+
+def test_reward_examples():
+    m = O.Model.grid(open3x3(goal=0))
+    R = [m.R(4, a) for a in range(9)]
+    assert np.allclose(R, GOLD["reward_centre_goal_topleft_3x3"]["R"], atol=1e-15)
+    assert m.R(0, 4) == 0.0            # stay at goal
+    assert m.R(8, 4) == -2.0           # stay off goal
+
+
+# ---- P3 / P4 / P11 Eq. 3 -------------------------------------------------------------------
+def test_bayes_two_state_example():
+    T = np.zeros((2, 1, 2)); T[0, 0, 0] = 1; T[1, 0, 1] = 1
+    Om = np.array([[0.9, 0.1], [0.2, 0.8]])
+    R = np.zeros((2, 1))
+    m = O.Model.dense(T, Om, R, 0.95)
+    post, p = m.belief_update(np.array([0.5, 0.5]), 0, 0)
+    g = GOLD["bayes_two_state"]
+    assert p == pytest.approx(g["p_obs"], abs=1e-15)
+    assert np.allclose(post, g["posterior"], atol=1e-15)
+    assert m.marginal(m.predict(np.array([0.5, 0.5]), 0)) == pytest.approx([0.55, 0.45])
+
+
+def test_bayes_point_mass_chain_and_uniform_invariance():
+    T = np.zeros((2, 1, 2)); T[0, 0, 1] = 1; T[1, 0, 1] = 1
+    Om = np.array([[0.7, 0.3], [0.5, 0.5]])
+    m = O.Model.dense(T, Om, np.zeros((2, 1)), 0.9)
+    post, _ = m.belief_update(np.array([1.0, 0.0]), 0, 0)
+    assert np.array_equal(post, [0.0, 1.0])
+    T2 = np.zeros((3, 1, 3))
+    for i in range(3):
+        T2[i, 0, i] = 1
+    m2 = O.Model.dense(T2, np.full((3, 2), 0.5), np.zeros((3, 1)), 0.9)
+    b = np.ones(3) / 3
+    post, _ = m2.belief_update(b, 0, 1)
+    assert np.allclose(post, b, atol=1e-15)
+
+
+def test_zero_likelihood():
+    T = np.zeros((2, 1, 2)); T[0, 0, 0] = 1; T[1, 0, 1] = 1
+    Om = np.array([[1.0, 0.0], [1.0, 0.0]])
+    m = O.Model.dense(T, Om, np.zeros((2, 1)), 0.9)
+    with pytest.raises(O.OracleError) as e:
+        m.belief_update(np.array([0.5, 0.5]), 0, 1)
+    assert e.value.code == O.ERR_ZERO_LIKELIHOOD
+
+
+def test_belief_reward_example():
+    T = np.zeros((3, 1, 3))
+    for i in range(3):
+        T[i, 0, i] = 1
+    m = O.Model.dense(T, np.ones((3, 1)), np.array([[-2.0], [-1.0], [0.0]]), 0.9)
+    assert m.belief_reward(np.array([0.2, 0.3, 0.5]), 0) == pytest.approx(GOLD["belief_reward"]["value"], abs=1e-15)
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_predict_matches_dense_product_and_total_probability(seed):
+    gm = W.random_map(7, 9, 0.2, seed=seed)
+    m = O.Model.grid(gm)
+    T = dense_T(m)
+    b = W.random_belief(gm, seed + 10)
+    for a in range(m.na):
+        bbar = m.predict(b, a)
+        assert np.allclose(bbar, T[:, a, :].T @ b, atol=1e-15)
+        assert bbar.sum() == pytest.approx(1.0, abs=1e-12)
+        P = m.marginal(bbar)
+        assert P.sum() == pytest.approx(1.0, abs=1e-12)
+        recon = np.zeros(m.nx)
+        for z in range(16):
+            post, p = m.belief_update(b, a, z)
+            assert p == pytest.approx(P[z], abs=1e-15)
+            assert post.sum() == pytest.approx(1.0, abs=1e-12)           # P11
+            assert np.all(post[gm.occupancy == 1] == 0.0)                # P11 support
+            recon += p * post
+        assert np.allclose(recon, bbar, atol=1e-12)                      # P4
+
+
+# ---- P5 value iteration --------------------------------------------------------------------
+@pytest.mark.parametrize("L", [3, 6])
+def test_vi_corridor_closed_form(L):
+    m = O.Model.grid(W.corridor(L), action_mask=W.A9, p_int=1.0, p_stay=0.0, p_lat=0.0)
+    st, V, Q, sweeps, res = m.value_iteration(1e-9)
+    assert st == O.OK and res < 1e-9
+    assert np.allclose(V, GOLD["corridor_vi"][f"L{L}"], atol=1e-8)
+
+
+def test_vi_constant_reward_dense():
+    rng = np.random.default_rng(0)
+    T = rng.random((4, 2, 4)); T /= T.sum(axis=2, keepdims=True)
+    m = O.Model.dense(T, np.ones((4, 1)), np.full((4, 2), -3.0), 0.9)
+    st, V, Q, _, res = m.value_iteration(1e-11)
+    assert st == O.OK
+    assert np.allclose(V, -3.0 / (1 - 0.9), atol=1e-9)
+
+
+def test_vi_fixed_point_random_map():
+    gm = W.random_map(20, 23, 0.2, seed=5)
+    m = O.Model.grid(gm, action_mask=W.A8)
+    st, V, Q, sweeps, res = m.value_iteration(1e-9)
+    assert st == O.OK and res < 1e-9 and sweeps > 50
+    free = gm.occupancy == 0
+    assert np.allclose(Q.max(axis=0)[free], V[free], atol=2e-8)
+    T = dense_T(m)
+    R = m.R_table()
+    for a in range(m.na):   # Q = R + gamma T V on free cells
+        assert np.allclose((R[a] + 0.95 * T[:, a, :] @ V)[free], Q[a][free], atol=1e-12)
+    assert np.all(V[free] < 0) and V[gm.goal] > -12
+
+
+# ---- P6 / P7 / P8 plan step -----------------------------------------------------------------
+def _small(seed=3, acc=0.95, mask=W.A4, H=5, Wd=6):
+    gm = W.random_map(H, Wd, 0.15, seed=seed)
+    m = O.Model.grid(gm, action_mask=mask, acc=acc)
+    st, V, Q, _, _ = m.value_iteration(1e-10)
+    return gm, m, Q
+
+
+def test_depth0_is_qmdp():
+    gm, m, Q = _small()
+    b = W.random_belief(gm, 1)
+    r = m.plan(Q, b, depth=0, n=4)
+    assert np.allclose(r.qroot, Q @ b, atol=1e-14)
+    assert r.action == m.action_ids[int(np.argmax(Q @ b))]
+
+
+def _dense_brute(T, Om, R, Q, gamma, b, depth):
+    """Eq. 2 written with dense matrices (brute force over all z, tiny inputs)."""
+    na = T.shape[1]
+    qs = []
+    for a in range(na):
+        bbar = T[:, a, :].T @ b
+        val = R[a] @ b
+        for z in range(Om.shape[1]):
+            pz = Om[:, z] @ bbar
+            if pz <= 1e-300:
+                continue
+            child = Om[:, z] * bbar / pz
+            if depth == 1:
+                v = (Q @ child).max()
+            else:
+                v = max(_dense_brute(T, Om, R, Q, gamma, child, depth - 1))
+            val += gamma * pz * v
+        qs.append(val)
+    return qs
+
+
+def test_depth1_closed_form_unnormalised():
+    gm, m, Q = _small(seed=4, mask=W.A8)
+    T, Om, R = dense_T(m), m.O_table(), m.R_table()
+    b = W.uniform_belief(gm)
+    r = m.plan(Q, b, depth=1, n=4, mode=O.MODE_BRUTE)
+    for a in range(m.na):
+        bbar = T[:, a, :].T @ b
+        expect = R[a] @ b + 0.95 * sum((Q @ (Om[:, z] * bbar)).max() for z in range(16))
+        assert r.qroot[a] == pytest.approx(expect, abs=1e-12)
+
+
+@pytest.mark.parametrize("depth", [1, 2])
+def test_brute_force_matches_dense_recursion(depth):
+    gm, m, Q = _small(seed=6, acc=0.8, H=4, Wd=4)
+    T, Om, R = dense_T(m), m.O_table(), m.R_table()
+    b = W.random_belief(gm, 3)
+    r = m.plan(Q, b, depth=depth, n=4, mode=O.MODE_BRUTE)
+    assert np.allclose(r.qroot, _dense_brute(T, Om, R, Q, 0.95, b, depth), atol=1e-12)
+
+
+def test_exact_mode_with_covering_samples_equals_brute():
+    gm, m, Q = _small(seed=6, acc=0.75, H=4, Wd=4)
+    b = W.uniform_belief(gm)
+    brute = m.plan(Q, b, depth=2, n=4, mode=O.MODE_BRUTE)
+    ex = m.plan(Q, b, depth=2, n=4096, mode=O.MODE_EXACT, trace=True)
+    covered = (ex.trace.q_cnt > 0) | (ex.trace.q_P <= 1e-300)
+    assert covered.all()
+    assert np.allclose(ex.qroot, brute.qroot, atol=1e-12)
+    fr = m.plan(Q, b, depth=2, n=4096, mode=O.MODE_FREQ)
+    assert np.allclose(fr.qroot, brute.qroot, atol=0.05)   # O(n^-1/2) sampling gap (R31)
+
+
+# ---- P9 sampling distribution ---------------------------------------------------------------
+def test_sampling_frequencies_and_ancestral_equivalence():
+    gm = W.random_map(8, 8, 0.2, seed=2)
+    m = O.Model.grid(gm, action_mask=W.A9, acc=0.8)
+    b = W.random_belief(gm, 4)
+    a = 1
+    n = 60000
+    P, R, z, flag, cnt = m.qnode_sample(b, a, qpath=0x12, n=n, seed=9)
+    assert cnt.sum() == n and np.array_equal(np.bincount(z, minlength=16), cnt)
+    sd = np.sqrt(n * P * (1 - P))
+    assert np.all(np.abs(cnt - n * P) <= 5 * sd + 1)
+    anc = np.zeros(16)
+    for j in range(n):
+        anc[m.ancestral_sample(b, a, [j, 0x12, 0, 7], [9, 0])] += 1
+    tv = 0.5 * np.abs(anc / n - cnt / n).sum()
+    assert tv < 0.015
+
+
+def test_draw_keying_follows_appendix_a():
+    gm = W.random_map(6, 6, 0.2, seed=8)
+    m = O.Model.grid(gm, acc=0.9)
+    b = W.uniform_belief(gm)
+    qpath = 0x0000_0001_0000_0003
+    P, R, z, flag, cnt = m.qnode_sample(b, 2, qpath=qpath, n=16, seed=77, step=5, episode=3)
+    for j in range(16):
+        w = O.philox([j, qpath & 0xFFFFFFFF, qpath >> 32, 5], [77, 3])
+        k, f = O.inverse_cdf(P, O.uniform(w[0]))
+        assert z[j] == k and flag[j] == f
+
+
+# ---- P12 / P15 backup recompute and determinism ---------------------------------------------
+def test_backup_recompute_bit_exact_and_determinism():
+    gm = W.CONFIGS["C1"]["map"]()
+    m = O.Model.grid(gm, action_mask=W.A4)
+    _, _, Q, _, _ = m.value_iteration(1e-9)
+    b = W.uniform_belief(gm)
+    r = m.plan(Q, b, depth=2, n=4, seed=1, trace=True, capture_beliefs=True)
+    r2 = m.plan(Q, b, depth=2, n=4, seed=1, trace=True, capture_beliefs=True)
+    assert np.array_equal(r.qroot, r2.qroot)
+    assert np.array_equal(r.trace.q_Q, r2.trace.q_Q) and np.array_equal(r.trace.q_z, r2.trace.q_z)
+    t = r.trace
+    vval = {int(p): v for p, v in zip(t.v_path, t.v_V)}
+    qval = {(int(p), int(l)): q for p, l, q in zip(t.q_path, t.q_level, t.q_Q)}
+    n = 4
+    for i in range(len(t.q_path)):
+        p, lvl = int(t.q_path[i]), int(t.q_level[i])
+        acc = 0.0
+        for z in range(16):
+            c = int(t.q_cnt[i, z])
+            if c:
+                acc += (c / n) * vval[O.vpath_child(p, lvl, z)]
+        assert t.q_R[i] + 0.95 * acc == t.q_Q[i]
+    for i in range(len(t.v_path)):
+        p, lvl = int(t.v_path[i]), int(t.v_level[i])
+        if lvl < 2:
+            kids = [qval[(O.qpath_child(p, lvl, a), lvl)] for a in m.action_ids]
+            assert max(kids) == t.v_V[i]
+    # root Q-nodes
+    roots = [qval[(O.qpath_child(0, 0, a), 0)] for a in m.action_ids]
+    assert np.array_equal(np.array(roots), r.qroot)
+    # the tree is 12 / ~123 V-nodes at C1 (SURVEY §8.0 sizing)
+    assert 8 <= (t.v_level == 1).sum() <= 16
+
+
+# ---- P13 symmetry ---------------------------------------------------------------------------
+def test_mirror_symmetry_exact():
+    gm = W.from_ascii("""
+#...#
+..#..
+.....
+..G..
+""")
+    m = O.Model.grid(gm, action_mask=W.A9, acc=0.9)
+    _, _, Q, _, _ = m.value_iteration(1e-10)
+    b = W.uniform_belief(gm)
+    r = m.plan(Q, b, depth=2, n=4, mode=O.MODE_BRUTE)
+    q = dict(zip(m.action_ids, r.qroot))
+    for a, ma in ((0, 2), (3, 5), (6, 8)):
+        assert q[a] == pytest.approx(q[ma], abs=1e-12)
+
+
+# ---- P10 / P14 episodes -----------------------------------------------------------------------
+def _bfs_dist(gm, start, diag=True):
+    H, Wd = gm.height, gm.width
+    dist = {start: 0}
+    dq = deque([start])
+    moves = [(dr, dc) for dr in (-1, 0, 1) for dc in (-1, 0, 1) if (dr, dc) != (0, 0)
+             and (diag or dr == 0 or dc == 0)]
+    while dq:
+        x = dq.popleft()
+        r, c = divmod(x, Wd)
+        for dr, dc in moves:
+            rr, cc = r + dr, c + dc
+            if 0 <= rr < H and 0 <= cc < Wd and gm.occupancy[rr * Wd + cc] == 0:
+                y = rr * Wd + cc
+                if y not in dist:
+                    dist[y] = dist[x] + 1
+                    dq.append(y)
+    return dist
+
+
+@pytest.mark.parametrize("planner", [O.PLANNER_QVTS, O.PLANNER_MDP, O.PLANNER_ASTAR])
+def test_noise_free_episode_length_equals_bfs(planner):
+    gm = W.random_map(9, 10, 0.2, seed=11)
+    m = O.Model.grid(gm, action_mask=W.A9, p_int=1.0, p_stay=0.0, p_lat=0.0, acc=1.0)
+    _, _, Q, _, _ = m.value_iteration(1e-10)
+    dist = _bfs_dist(gm, gm.goal)
+    for s in range(3):
+        start = W.free_cell(gm, 100 + s)
+        rec, la, lz, lx = m.run_episode(Q, W.point_belief(gm, start), planner, depth=2, n=4,
+                                        max_steps=200, seed=5, episode=s)
+        assert rec.outcome == 0 and rec.collisions == 0
+        assert rec.steps == dist[start] + 3
+        assert m.astar_length(start) == dist[start]
+
+
+def test_episode_bookkeeping_replay():
+    gm = W.random_map(8, 8, 0.2, seed=12)
+    m = O.Model.grid(gm, action_mask=W.A9, acc=0.9)
+    _, _, Q, _, _ = m.value_iteration(1e-10)
+    b0 = W.uniform_belief(gm)
+    rec, la, lz, lx = m.run_episode(Q, b0, O.PLANNER_MDP, max_steps=60, seed=3, episode=2)
+    b = b0.copy()
+    x = rec.x0
+    ret, disc = 0.0, 1.0
+    for s in range(rec.steps):
+        a_idx = m.action_ids.index(int(la[s]))
+        mode = m.belief_mode(b)
+        assert m.action_ids[int(np.argmax(Q[:, mode]))] == la[s]     # MDP on the replayed belief
+        ret += disc * m.R(x, a_idx)
+        disc *= 0.95
+        b, _ = m.belief_update(b, a_idx, int(lz[s]))
+        x = int(lx[s])
+    assert ret == pytest.approx(rec.disc_return, abs=1e-12)
+    assert x == rec.x_final
