@@ -1,0 +1,131 @@
+// qvts_internal.cuh — internal structures of libqvts (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/qvts.h"
+
+namespace qvts {
+
+constexpr int kHistThreads = 256;   // threads per hist CTA (one class stream per thread)
+constexpr int kMaxLevels = 9;       // depth <= 8
+
+void set_error(const std::string &msg);
+
+#define QVTS_CUDA(call)                                                                   \
+    do {                                                                                  \
+        cudaError_t e__ = (call);                                                         \
+        if (e__ != cudaSuccess) {                                                         \
+            ::qvts::set_error(std::string(#call) + ": " + cudaGetErrorString(e__));       \
+            return e__ == cudaErrorMemoryAllocation ? QVTS_ERR_OUT_OF_MEMORY : QVTS_ERR_CUDA; \
+        }                                                                                 \
+    } while (0)
+
+#define QVTS_TRY(expr)                          \
+    do {                                        \
+        qvts_status s__ = (expr);               \
+        if (s__ != QVTS_OK) return s__;         \
+    } while (0)
+
+// Growable device buffer (capacity only grows; contents are not preserved on growth).
+struct DevBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+    qvts_status ensure(size_t bytes);
+    void release();
+    template <class T> T *as() const { return static_cast<T *>(p); }
+};
+
+// One row band of the grid processed by one hist CTA: rows [row0, row0+nrows), with a
+// class-partitioned slot list (SURVEY §7 "signature binning": every thread owns a stream of
+// cells that share one wall signature, so its bin index is fixed in registers).
+struct BandInfo {
+    int row0, nrows, L, pad;
+    long long slot_off;           // first slot; slot (i, t) = slot_off + i*kHistThreads + t
+    int cs[17];                   // threads [cs[c], cs[c+1]) own class c; >= cs[16] idle
+    int pad2[3];
+};
+
+struct BandSet {
+    int nb = 0, rows = 0, tile_floats = 0;
+    long long total_slots = 0;
+    std::vector<BandInfo> h_bands;
+    std::vector<int32_t> h_slot_cell;
+    DevBuf bands, entries, slot_cell, qlist;
+};
+
+// Per-level node arrays of the level-batched tree (SoA).
+struct VLevel {
+    long long n = 0;                  // V-nodes at this level
+    DevBuf path, parent_q, z, f, root, V, belief;
+};
+struct QLevel {
+    long long nwork = 0;              // parents expanded at this level (owned subset when sharded)
+    DevBuf vmap;                      // work index -> V-node index (only when sharded)
+    bool mapped = false;
+    DevBuf R, P, cnt, umask, U, off, Q, zdraw, leafV;
+};
+
+struct Model {
+    int device = 0;
+    int H = 0, W = 0, HW = 0, HWp = 0, NA = 0, NAP = 0, goal = 0;
+    uint32_t mask = 0;
+    int action_id[9] = {0};
+    double p_int = 0, p_stay = 0, p_lat = 0, acc = 0, gamma = 0;
+    std::vector<uint8_t> occ, m8, sig;
+    std::vector<double> R64;          // [NA][HW]
+    // device tables
+    DevBuf d_m8, d_sig, d_cell /* sig | occ<<4 */, d_ctab, d_R64, d_O64, d_O32, d_gc_cell, d_gc_act, d_gc_val, d_free;
+    int ngc = 0;
+    BandSet band_big, band_small;
+    // value iteration
+    bool have_q = false;
+    double qbar = 0.0;
+    DevBuf d_V[2], d_resid, d_Q64;
+    // plan workspace
+    VLevel vl[kMaxLevels + 1];
+    QLevel ql[kMaxLevels];
+    DevBuf part, scan_tmp, total, counters, vshard;
+    int last_depth = -1, last_n = 0, last_shard_level = -1;
+    bool last_trace = false;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // instrumentation
+    bool prof = false;
+    qvts_profile pstat{};
+    std::vector<cudaEvent_t> evpool;
+    struct EvRec { int cat; cudaEvent_t a, b; };
+    std::vector<EvRec> evrecs;
+    size_t evnext = 0;
+    long long n_free = 0;
+    // belief_update scratch
+    DevBuf bu_R, bu_P, bu_cnt, bu_umask, bu_U, bu_off, bu_path, bu_root, bu_key;
+    // episodes
+    DevBuf ep_b[2], ep_state, ep_root_step, ep_root_ep;
+};
+
+// instrumentation helpers (model.cu)
+void prof_begin(Model &m, int cat, cudaStream_t st, cudaEvent_t *out);
+void prof_end(Model &m, int cat, cudaStream_t st, cudaEvent_t a);
+void prof_collect(Model &m);   // after a stream sync: fold recorded event pairs into pstat
+
+// model.cu
+qvts_status build_bands(Model &m, BandSet &bs, int rows);
+qvts_status build_qlists(Model &m, cudaStream_t st);
+
+// plan.cu
+struct RootBatch {
+    const float *beliefs;       // [n][stride]
+    long long stride;
+    long long n;
+    const uint32_t *step_dev;   // [n] per-root step keys (device)
+    const uint32_t *episode_dev;// [n] per-root episode keys (device)
+};
+qvts_status plan_levels(Model &m, const RootBatch &roots, const qvts_plan_cfg &cfg, const qvts_comm *comm,
+                        cudaStream_t st, long long *nv_out /*[depth+1]*/);
+
+}  // namespace qvts
+
+struct qvts_model : public qvts::Model {};

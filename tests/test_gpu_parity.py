@@ -1,0 +1,249 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle, element by element on
+the same seeded inputs.  Run on a B200 with `pytest -m gpu`."""
+import numpy as np
+import pytest
+
+import oracle as O
+import workloads as W
+from tests import parity as PT
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def Q():
+    assert torch.cuda.is_available(), "GPU tests need CUDA"
+    from paper_1810_00204_b200 import qvts
+    qvts.lib()
+    return qvts
+
+
+def pair(Q, gm, mask, acc=0.95, p=(0.8, 0.1, 0.05)):
+    gmod = Q.Model(gm, action_mask=mask, p_intended=p[0], p_stay=p[1], p_lateral=p[2], sensor_acc=acc)
+    code, sweeps, res = gmod.value_iteration(1e-9)
+    assert code == 0 and res < 1e-9
+    omod = O.Model.grid(gm, action_mask=mask, p_int=p[0], p_stay=p[1], p_lat=p[2], acc=acc)
+    st, V, Qo, osw, ores = omod.value_iteration(1e-9)
+    assert st == O.OK
+    return gmod, omod, Qo, sweeps, osw
+
+
+def dev(b):
+    return torch.tensor(np.asarray(b, np.float32), device="cuda")
+
+
+MAPS = {
+    "C1": (lambda: W.CONFIGS["C1"]["map"](), W.A4),
+    "ragged": (lambda: W.random_map(29, 37, 0.2, seed=9), W.A8),
+    "paper": (lambda: W.paper_style(50, 50, 6, 12, seed=1), W.A9),
+}
+
+
+@pytest.mark.parametrize("name", list(MAPS))
+def test_tables_and_value_iteration(Q, name):
+    gm, mask = MAPS[name][0](), MAPS[name][1]
+    g, o, Qo, sweeps, osw = pair(Q, gm, mask)
+    R, sig = g.tables()
+    assert np.array_equal(sig, o.sig_table().astype(np.uint8))
+    assert np.max(np.abs(R.astype(np.float64) - o.R_table())) <= 2.5e-7
+    assert abs(sweeps - osw) <= 1
+    assert np.max(np.abs(g.q() - Qo)) <= 1e-7
+
+
+@pytest.mark.parametrize("name", list(MAPS))
+def test_belief_update(Q, name):
+    gm, mask = MAPS[name][0](), MAPS[name][1]
+    g, o, _, _, _ = pair(Q, gm, mask)
+    for seed in (1, 2):
+        b = W.random_belief(gm, seed, sparsity=0.3 if seed == 2 else 0.0)
+        bd = dev(b)
+        b32 = np.asarray(b, np.float32).astype(np.float64)
+        out = torch.empty_like(bd)
+        for a in g.action_ids:
+            ai = o.action_ids.index(a)
+            for z in (0, 3, 5, 15):
+                ref, pref = o.belief_update(b32, ai, z)
+                p = g.belief_update(bd, a, z, out)
+                assert abs(p - pref) <= 1e-7, (a, z, p, pref)
+                got = out.cpu().numpy().astype(np.float64)
+                assert np.max(np.abs(got - ref)) <= PT.TOL
+                assert np.max(np.abs(got - ref)) <= 1e-5 * max(1e-3, ref.max())
+                assert np.all(got[gm.occupancy == 1] == 0.0)
+
+
+def test_belief_update_zero_likelihood(Q):
+    gm = W.pillars(6, 6, 1, seed=3)
+    g = Q.Model(gm, action_mask=W.A9, sensor_acc=1.0)
+    g.value_iteration()
+    b = dev(W.point_belief(gm, W.free_cell(gm, 1)))
+    out = torch.empty_like(b)
+    o = O.Model.grid(gm, action_mask=W.A9, acc=1.0)
+    P = o.marginal(o.predict(np.asarray(b.cpu(), np.float64), 4))
+    z = int(np.flatnonzero(P == 0)[0])
+    with pytest.raises(Q.QvtsError) as e:
+        g.belief_update(b, 4, z, out)
+    assert e.value.code == 5
+
+
+def run_parity(Q, gm, mask, depth, n, b0, seed=1, step=0, episode=0, beliefs=True):
+    g, o, Qo, _, _ = pair(Q, gm, mask)
+    b32 = np.asarray(b0, np.float32)
+    res = g.plan_step(dev(b32), depth, n, seed=seed, step=step, episode=episode, want_trace=True)
+    gq, gv, gbel, _ = PT.gpu_tree(g, n, with_beliefs=beliefs)
+    ores = o.plan(Qo, b32.astype(np.float64), depth, n, seed=seed, step=step, episode=episode, trace=True,
+                  capture_beliefs=beliefs)
+    oq, ov, obel = PT.oracle_tree(ores)
+    replay, nmis = PT.draw_mismatches(gq, oq)
+    if replay:   # flagged draws decided differently: replay the GPU's decision in the oracle
+        ores = o.plan(Qo, b32.astype(np.float64), depth, n, seed=seed, step=step, episode=episode, trace=True,
+                      capture_beliefs=beliefs, replay=replay)
+        oq, ov, obel = PT.oracle_tree(ores)
+        PT.draw_mismatches(gq, oq)
+    err = PT.compare_trees(gq, gv, oq, ov, gbel if beliefs else None, obel if beliefs else None)
+    assert np.max(np.abs(np.array(res.q_root[:g.n_actions]) - ores.qroot)) <= PT.TOL
+    PT.check_action(res.action, ores.action, ores.qroot, g.action_ids)
+    assert res.n_belief_updates == len(ov)
+    return res, err, nmis
+
+
+def test_plan_C1_full_tree(Q):
+    gm = W.CONFIGS["C1"]["map"]()
+    res, err, _ = run_parity(Q, gm, W.A4, 2, 4, W.uniform_belief(gm))
+    assert res.n_vnodes[1] >= 8
+
+
+@pytest.mark.parametrize("seed,step", [(1, 0), (7, 3)])
+def test_plan_ragged_depth3(Q, seed, step):
+    gm = W.random_map(29, 37, 0.2, seed=9)
+    run_parity(Q, gm, W.A8, 3, 8, W.random_belief(gm, 5), seed=seed, step=step, episode=2)
+
+
+def test_plan_paper_style_A9(Q):
+    gm = W.paper_style(50, 50, 6, 12, seed=1)
+    run_parity(Q, gm, W.A9, 3, 16, W.uniform_belief(gm), beliefs=False)
+
+
+def test_plan_depth1_and_large_n(Q):
+    gm = W.random_map(13, 11, 0.2, seed=2)
+    run_parity(Q, gm, W.A9, 1, 300, W.random_belief(gm, 3))
+    run_parity(Q, gm, W.A4, 4, 2, W.uniform_belief(gm))
+
+
+def test_plan_C3_full(Q):
+    gm = W.CONFIGS["C3"]["map"]()
+    res, err, nmis = run_parity(Q, gm, W.A8, 3, 8, W.uniform_belief(gm), beliefs=False)
+    assert res.n_belief_updates > 10000
+
+
+def test_plan_deterministic(Q):
+    gm = W.random_map(40, 40, 0.2, seed=4)
+    g, _, _, _, _ = pair(Q, gm, W.A8)
+    b = dev(W.uniform_belief(gm, np.float32))
+    r1 = g.plan_step(b, 3, 8, seed=3, want_trace=True)
+    t1 = g.trace(with_draws=True, n_samples=8)
+    r2 = g.plan_step(b, 3, 8, seed=3, want_trace=True)
+    t2 = g.trace(with_draws=True, n_samples=8)
+    assert list(r1.q_root) == list(r2.q_root)
+    for d in range(3):
+        for k in ("R", "P", "Q", "z", "cnt"):
+            assert np.array_equal(t1["levels"][d]["q"][k], t2["levels"][d]["q"][k])
+    assert np.array_equal(t1["leafV"], t2["leafV"])
+
+
+@pytest.mark.parametrize("G", [2, 3])
+def test_sharded_plan_matches_single_gpu_bitwise(Q, G):
+    """Run the G ranks of a sharded plan step serially on one GPU: first pass collects each rank's
+    zero-padded shard-level values, second pass feeds back their exact sum."""
+    gm = W.random_map(40, 44, 0.2, seed=6)
+    g, _, _, _, _ = pair(Q, gm, W.A8)
+    b = dev(W.uniform_belief(gm, np.float32))
+    ref = g.plan_step(b, 3, 8, seed=5)
+    partials = {}
+
+    def collect(r):
+        def fn(ptr, count, stream):
+            t = torch.as_tensor(Q._CudaArray(ptr, count), device="cuda")
+            partials[r] = t.cpu().numpy().copy()
+        return fn
+
+    for r in range(G):
+        g.plan_step(b, 3, 8, seed=5, comm=Q.make_callback_comm(r, G, collect(r), min_nodes_per_rank=4))
+    total = sum(partials[r] for r in range(G))
+    for r in range(G):
+        assert np.count_nonzero(partials[r]) > 0
+    nz = [set(np.flatnonzero(partials[r])) for r in range(G)]
+    for r in range(G):
+        for s in range(r + 1, G):
+            assert not (nz[r] & nz[s])    # disjoint ownership
+
+    def feed(ptr, count, stream):
+        t = torch.as_tensor(Q._CudaArray(ptr, count), device="cuda")
+        t.copy_(torch.from_numpy(total).cuda())
+
+    for r in range(G):
+        res = g.plan_step(b, 3, 8, seed=5, comm=Q.make_callback_comm(r, G, feed, min_nodes_per_rank=4))
+        assert list(res.q_root) == list(ref.q_root)
+        assert res.action == ref.action
+
+
+def test_C4_full_size_sampled_parity(Q):
+    """BASELINE config 4 (256x256, A8, depth 4, n = 16), launched as bench.py times it: sampled
+    nodes on every level recomputed one by one by the oracle along their own paths."""
+    cfg = W.CONFIGS["C4"]
+    gm = cfg["map"]()
+    g, o, Qo, _, _ = pair(Q, gm, W.A8)
+    b32 = W.uniform_belief(gm, np.float32)
+    D, n = cfg["depth"], cfg["n"]
+    res = g.plan_step(dev(b32), D, n, seed=1, want_trace=True)
+    assert res.n_belief_updates > 1_000_000
+    na = g.n_actions
+    rng = np.random.default_rng(0)
+    # level-0 Q-nodes: exact
+    lq0 = Q.qvts_trace_qnodes(g.h, 0, na, n, True)
+    b = b32.astype(np.float64)
+    for ai, a in enumerate(g.action_ids):
+        P, R, z, flag, cnt = o.qnode_sample(b, ai, O.qpath_child(0, 0, a), n, seed=1)
+        assert abs(lq0["R"][ai] - R) <= PT.TOL and np.max(np.abs(lq0["P"][ai] - P)) <= 1e-7
+        assert np.all((lq0["z"][ai] == z) | flag)
+    # random root-to-level-(D-1) paths followed by the oracle
+    _, nv, nqw = Q.qvts_trace_counts(g.h)
+    vlev = [Q.qvts_trace_vnodes(g.h, d, nv[d]) for d in range(D)]
+    qlev = [Q.qvts_trace_qnodes(g.h, d, nqw[d] * na, n, True) for d in range(D)]
+    for trial in range(6):
+        i = int(rng.integers(nv[D - 1]))
+        chain = [i]
+        for d in range(D - 1, 0, -1):
+            chain.append(int(vlev[d]["parent_q"][chain[-1]]) // na)
+        chain = chain[::-1]           # V-node indices at levels 0..D-1
+        bo = b32.astype(np.float64)
+        for d in range(1, D):
+            vi = chain[d]
+            qi = int(vlev[d]["parent_q"][vi])
+            ai = qi % na
+            qpath = int(qlev[d - 1]["path"][qi])
+            P, R, z, flag, cnt = o.qnode_sample(bo, ai, qpath, n, seed=1)
+            assert abs(qlev[d - 1]["R"][qi] - R) <= PT.TOL
+            assert np.max(np.abs(qlev[d - 1]["P"][qi] - P)) <= 1e-6
+            mism = qlev[d - 1]["z"][qi] != z
+            assert not np.any(mism & ~flag)
+            zz = int(vlev[d]["z"][vi])
+            assert cnt[zz] > 0 or np.any(mism)
+            bo, _ = o.belief_update(bo, ai, zz)
+            gb = Q.qvts_trace_belief(g.h, d, vi, g.n_cells).astype(np.float64)
+            assert np.max(np.abs(gb - bo)) <= PT.TOL
+        # value of the level-(D-1) node with its subtree (its Q-nodes are the leaf Q-level)
+        vpath = int(vlev[D - 1]["path"][chain[-1]])
+        Vo, qv = o.vnode_value(Qo, bo, vpath, D - 1, D, n, seed=1)
+        assert abs(vlev[D - 1]["V"][chain[-1]] - Vo) <= PT.TOL
+        w = chain[-1]
+        assert np.max(np.abs(qlev[D - 1]["Q"][w * na:(w + 1) * na] - qv)) <= PT.TOL
+    # backup identity at the root from the GPU's own arrays (fp64 recompute)
+    for d in range(D - 2, -1, -1):
+        lq, lc = qlev[d], vlev[d + 1]
+        off = np.concatenate([[0], np.cumsum([int((c > 0).sum()) for c in lq["cnt"]])])
+        for qi in rng.integers(0, len(lq["R"]), size=min(200, len(lq["R"]))):
+            s = sum((lc["f"][c] / n) * lc["V"][c] for c in range(off[qi], off[qi + 1]))
+            assert abs(lq["R"][qi] + 0.95 * s - lq["Q"][qi]) <= 1e-9
+    assert np.max(np.abs(np.array(res.q_root[:na]) - qlev[0]["Q"])) == 0.0
