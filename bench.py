@@ -160,7 +160,10 @@ class ClockSampler:
 
 
 # ---- our arm -----------------------------------------------------------------------------------
-FLOPS_PER_LEAF_CELL = {8: 193, 9: 228, 4: 65}   # FP32 ops per (parent, free cell) in k_hist<leaf>; DESIGN.md
+# Algorithmic FP32 work of S1+S2+S5 per (leaf parent, free cell):
+# per moving action a 4-tap predict (8 flops); per action the histogram add (1), the R(b,a)
+# multiply-add (2) and |A| multiply-adds into the signature bins (2|A|).
+FLOPS_PER_LEAF_CELL = {8: 8 * 8 + 8 * (3 + 2 * 8), 9: 8 * 8 + 9 * (3 + 2 * 9), 4: 4 * 8 + 4 * (3 + 2 * 4)}
 
 
 def main():
@@ -291,7 +294,7 @@ def main():
         "roofline": {"bound": "alu", "kernel": "k_hist<A8,leaf> (S1+S2+S5)", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
                      "traffic": None,
-                     "algorithmic": f"{FLOPS_PER_LEAF_CELL[na]} FP32 flops per (leaf parent, free cell) x "
+                     "algorithmic": f"{FLOPS_PER_LEAF_CELL[na]} FP32 flops (FMA = 2) per (leaf parent, free cell) x "
                                     f"{prof['leaf_cells'] / leaf_launches:.3e} per launch; "
                                     "peak = 148 SM x 128 FP32 lanes x 2 x 1965 MHz (guide unit counts)",
                      "avg_launch_ms": leaf_ms / leaf_launches},

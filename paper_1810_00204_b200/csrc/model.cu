@@ -88,7 +88,8 @@ qvts_status build_bands(Model &m, BandSet &bs, int rows) {
     const int T = kHistThreads;
     const int H = m.H, W = m.W, TW = W + 2;
     rows = std::max(1, std::min(rows, H));
-    while (rows > 1 && (long long)(rows + 2) * TW > 65535) --rows;
+    // two parents' tiles per hist CTA must fit in shared memory (~190 KB) and index in 16 bits
+    while (rows > 1 && ((long long)(rows + 2) * TW > 65535 || (long long)(rows + 2) * TW * 8 > 190000)) --rows;
     if ((long long)(rows + 2) * TW > 65535) {
         set_error("grid too wide for the band tile (W+2)*3 > 65535");
         return QVTS_ERR_INVALID_ARG;
@@ -122,23 +123,55 @@ qvts_status build_bands(Model &m, BandSet &bs, int rows) {
         if (total == 0) L = 1;
         bi.L = L;
         bi.slot_off = off;
+        // thread ranges per class
+        std::vector<int> cls_of(T, -1);
         int t0 = 0;
-        std::vector<uint32_t> e((size_t)L * T, 0u);
-        std::vector<int32_t> sc((size_t)L * T, -1);
         for (int c = 0; c < 16; ++c) {
             bi.cs[c] = t0;
-            int n = (int)cls[c].size();
-            int k = (n + L - 1) / L;
-            for (int i = 0; i < n; ++i) {
-                int j = i % k, step = i / k;
-                int x = cls[c][i];
-                int r = x / W, cc = x % W;
-                int ti = (r - bi.row0 + 1) * TW + (cc + 1);
-                e[(size_t)step * T + t0 + j] = (uint32_t)ti | ((uint32_t)m.m8[x] << 16);
-                sc[(size_t)step * T + t0 + j] = x;
-            }
+            const int k = ((int)cls[c].size() + L - 1) / L;
+            for (int j = 0; j < k; ++j) cls_of[t0 + j] = c;
             t0 += k;
         }
+        // Deal the cells step by step.  Within each group of 16 slot-threads (one half-warp per
+        // parent) the 16 cells of a step get distinct tile residues mod 16, so the 9 neighbour
+        // loads of a warp hit 32 distinct shared-memory banks (the second parent's tile sits 16
+        // banks further).
+        std::vector<std::vector<int>> bucket[16];
+        std::vector<size_t> head[16];
+        for (int c = 0; c < 16; ++c) {
+            bucket[c].assign(16, {});
+            head[c].assign(16, 0);
+            for (int x : cls[c]) {
+                int r = x / W, cc = x % W;
+                int ti = (r - bi.row0 + 1) * TW + (cc + 1);
+                bucket[c][ti & 15].push_back(x);
+            }
+        }
+        std::vector<uint32_t> e((size_t)L * T, 0u);
+        std::vector<int32_t> sc((size_t)L * T, -1);
+        for (int step = 0; step < L; ++step)
+            for (int g = 0; g < T / 16; ++g) {
+                unsigned used = 0;
+                for (int tt = 16 * g; tt < 16 * g + 16; ++tt) {
+                    const int c = cls_of[tt];
+                    if (c < 0) continue;
+                    int best = -1, bestn = 0, anyr = -1, anyn = 0;
+                    for (int r = 0; r < 16; ++r) {
+                        int left = (int)(bucket[c][r].size() - head[c][r]);
+                        if (left <= 0) continue;
+                        if (!(used >> r & 1) && left > bestn) { best = r; bestn = left; }
+                        if (left > anyn) { anyr = r; anyn = left; }
+                    }
+                    if (best < 0) best = anyr;
+                    if (best < 0) continue;            // class exhausted: padding slot
+                    const int x = bucket[c][best][head[c][best]++];
+                    used |= 1u << best;
+                    int r = x / W, cc = x % W;
+                    int ti = (r - bi.row0 + 1) * TW + (cc + 1);
+                    e[(size_t)step * T + tt] = (uint32_t)ti | ((uint32_t)m.m8[x] << 16);
+                    sc[(size_t)step * T + tt] = x;
+                }
+            }
         bi.cs[16] = t0;
         entries.insert(entries.end(), e.begin(), e.end());
         bs.h_slot_cell.insert(bs.h_slot_cell.end(), sc.begin(), sc.end());

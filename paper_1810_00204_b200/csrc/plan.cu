@@ -42,174 +42,199 @@ __device__ __forceinline__ int action_of(int j) {
 }
 
 // ---- S1 + S2 (+ S5): signature-binned histograms ----------------------------------------------
+// Linear form of the clamped predict: with the 8 clamped source fields
+//   h_k(y) = b(y - d_k) + occ(y + d_k) b(y)          (k = the 8 moving stencil directions)
+// every action's prediction is bbar_a = p_stay b + p_int h_a + p_lat (h_l1 + h_l2) (stay: b).
+// Everything the Q-node needs is linear in bbar, so the kernel accumulates per wall-signature
+// class s (the observation class of O(y,z)) only
+//   mass_s = sum b,  HM_s[k] = sum h_k,  and for leaves Zb_s[a'] = sum b Q'(.,a'),
+//   H_s[k][a'] = sum h_k Q'(.,a')   (Q' = Q - qbar, SURVEY c.6 rule 5)
+// plus E[k] = sum occ(y + d_k) b(y) for R(b,a); k_reduce recombines them per action in fp64.
+// One CTA = 2 parents x one row band; its 512 threads are 256 slot-threads x 2 parents, with the
+// two parents in the two half-warps so the static per-slot loads (entry, Q') are shared.
 struct HistArgs {
     const float *beliefs;
     long long bstride;
     const int32_t *vmap;
+    long long nwork;
     const BandInfo *bands;
     int nb;
     const uint32_t *entries;
     const float4 *qlist;
-    const float *ctab;
-    int H, W, TW, region_floats;
-    float p_int, p_lat;
+    int H, W, TW, tstride, region_floats;
     double *part;
     int pstride;
 };
 
 template <uint32_t MASK, bool LEAF>
-constexpr int hist_nv() {
-    return mask_count(MASK) * (LEAF ? 1 + mask_count(MASK) : 1) + mask_count(MASK) + 1;
+__host__ __device__ constexpr int hist_cb() {      // class-binned values per thread
+    return 1 + 8 + (LEAF ? mask_count(MASK) * 9 : 0);
 }
-
-// One CTA = one (parent, band).  The band (+1-cell zero halo) is staged in shared memory; thread t
-// walks its class-homogeneous slot stream, predicting bbar_a(y) for every action (gather form of
-// the clamped stencil) and accumulating
-//   M_a  += bbar_a(y)                   (bin = the thread's class sig(y); Eq. 3 normaliser)
-//   Rp_a += c_a(y) b(y)                 (R(b,a) = (p_stay-1) sum b - sum c_a b + goal terms)
-//   S_a,a' += bbar_a(y) Q'(y,a')        (LEAF only; Q' = Q - qbar)
-// in fp32 registers, then reduces the per-thread values class by class in fixed order in fp64.
 template <uint32_t MASK, bool LEAF>
-__global__ void __launch_bounds__(kHistThreads) k_hist(HistArgs a) {
+__host__ __device__ constexpr int hist_nv() { return hist_cb<MASK, LEAF>() + 8; }
+
+// direction index di (0..7) <-> stencil id k != 4
+__host__ __device__ constexpr int dir_k(int di) { return di < 4 ? di : di + 1; }
+
+template <uint32_t MASK, bool LEAF>
+__global__ void __launch_bounds__(kPairThreads, 1) k_hist(HistArgs a) {
     constexpr int NA = mask_count(MASK);
     constexpr int NAP = (NA + 3) & ~3;
+    constexpr int CB = hist_cb<MASK, LEAF>();
     constexpr int NV = hist_nv<MASK, LEAF>();
     constexpr int T = kHistThreads;
     extern __shared__ float4 smem4[];
     float *smem = reinterpret_cast<float *>(smem4);
-    float *tile = smem;
-    float *ctab = smem + a.region_floats;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int p = lane >> 4;                       // parent of this half-warp
+    const int st = warp * 16 + (lane & 15);        // slot-thread 0..255
     const int band = blockIdx.x % a.nb;
-    const long long w = blockIdx.x / a.nb;
-    const long long v = a.vmap ? (long long)a.vmap[w] : w;
+    const long long pair = blockIdx.x / a.nb;
+    const long long w = 2 * pair + p;
+    const bool valid = w < a.nwork;
     const BandInfo *bi = a.bands + band;
     const int row0 = bi->row0, nrows = bi->nrows, L = bi->L;
     const long long soff = bi->slot_off;
-    const float *__restrict__ b = a.beliefs + v * a.bstride;
     const int TW = a.TW, TH = nrows + 2;
 
-    for (int i = t; i < 256 * NAP; i += T) ctab[i] = a.ctab[i];
-    for (int tr = warp; tr < TH; tr += T / 32) {
-        const int r = row0 - 1 + tr;
-        const bool rok = (r >= 0) && (r < a.H);
-        const float *brow = b + (size_t)r * a.W;
-        for (int tc = lane; tc < TW; tc += 32) {
-            const int c = tc - 1;
-            float val = 0.f;
-            if (rok && c >= 0 && c < a.W) val = __ldg(brow + c);
-            tile[tr * TW + tc] = val;
+    // stage both parents' bands (+ zero halo); a missing second parent stages zeros
+    for (int pp = 0; pp < 2; ++pp) {
+        const long long wp = 2 * pair + pp;
+        const bool vp = wp < a.nwork;
+        const long long vv = vp ? (a.vmap ? (long long)a.vmap[wp] : wp) : 0;
+        const float *__restrict__ b = a.beliefs + vv * a.bstride;
+        float *tile = smem + pp * a.tstride;
+        for (int tr = warp; tr < TH; tr += kPairThreads / 32) {
+            const int r = row0 - 1 + tr;
+            const bool rok = vp && (r >= 0) && (r < a.H);
+            const float *brow = b + (long long)r * a.W;
+            for (int tc = lane; tc < TW; tc += 32) {
+                const int c = tc - 1;
+                float val = 0.f;
+                if (rok && c >= 0 && c < a.W) val = __ldg(brow + c);
+                tile[tr * TW + tc] = val;
+            }
         }
     }
     __syncthreads();
-
+    const float *tile = smem + p * a.tstride;
     int off[9];
 #pragma unroll
     for (int k = 0; k < 9; ++k) off[k] = st_dr(k) * TW + st_dc(k);
 
-    float M[NA], Rp[NA], S[LEAF ? NA : 1][LEAF ? NA : 1];
-    float mass = 0.f;
+    float mass = 0.f, HM[8], E[8];
+    float Zb[LEAF ? NA : 1], Hq[LEAF ? 8 : 1][LEAF ? NA : 1];
 #pragma unroll
-    for (int j = 0; j < NA; ++j) {
-        M[j] = 0.f;
-        Rp[j] = 0.f;
-    }
+    for (int d = 0; d < 8; ++d) { HM[d] = 0.f; E[d] = 0.f; }
     if (LEAF) {
 #pragma unroll
-        for (int j = 0; j < (LEAF ? NA : 1); ++j)
+        for (int j = 0; j < (LEAF ? NA : 1); ++j) {
+            Zb[j] = 0.f;
 #pragma unroll
-            for (int j2 = 0; j2 < (LEAF ? NA : 1); ++j2) S[j][j2] = 0.f;
-    }
-    const float p_int = a.p_int, p_lat = a.p_lat;
-
-    for (int i = 0; i < L; ++i) {
-        const long long slot = soff + (long long)i * T + t;
-        const uint32_t e = __ldg(a.entries + slot);
-        if (e == 0u) continue;
-        const int ti = (int)(e & 0xFFFFu);
-        const int m8 = (int)((e >> 16) & 0xFFu);
-        float nb[9];
-#pragma unroll
-        for (int k = 0; k < 9; ++k) nb[k] = tile[ti + off[k]];
-        float c[NAP];
-        const float4 *c4 = reinterpret_cast<const float4 *>(ctab + m8 * NAP);
-#pragma unroll
-        for (int h = 0; h < NAP / 4; ++h) {
-            const float4 cv = c4[h];
-            c[4 * h] = cv.x; c[4 * h + 1] = cv.y; c[4 * h + 2] = cv.z; c[4 * h + 3] = cv.w;
+            for (int d = 0; d < (LEAF ? 8 : 1); ++d) Hq[d][j] = 0.f;
         }
+    }
+    // software pipeline: the next slot's entry and Q' are in flight while this one computes
+    uint32_t e_n = 0;
+    float4 q_n[LEAF ? NAP / 4 : 1];
+    if (L > 0) {
+        const long long slot = soff + st;
+        e_n = __ldg(a.entries + slot);
+        if (LEAF) {
+#pragma unroll
+            for (int h = 0; h < (LEAF ? NAP / 4 : 0); ++h) q_n[h] = __ldg(a.qlist + slot * (NAP / 4) + h);
+        }
+    }
+    for (int i = 0; i < L; ++i) {
+        const uint32_t e = e_n;
         float q[LEAF ? NAP : 1];
         if (LEAF) {
 #pragma unroll
             for (int h = 0; h < (LEAF ? NAP / 4 : 0); ++h) {
-                const float4 qv = __ldg(a.qlist + slot * (NAP / 4) + h);
-                q[4 * h] = qv.x; q[4 * h + 1] = qv.y; q[4 * h + 2] = qv.z; q[4 * h + 3] = qv.w;
+                q[4 * h] = q_n[h].x; q[4 * h + 1] = q_n[h].y; q[4 * h + 2] = q_n[h].z; q[4 * h + 3] = q_n[h].w;
             }
         }
-        const float b0 = nb[4];
-        mass += b0;
-#pragma unroll
-        for (int j = 0; j < NA; ++j) {
-            const int k = mask_action(MASK, j);
-            float bb;
-            if (k == 4) {
-                bb = b0;
-            } else {
-                const float tt = c[j] * b0;
-                Rp[j] += tt;
-                bb = fmaf(p_int, nb[8 - k], tt);
-                bb = fmaf(p_lat, nb[8 - lat1(k)] + nb[8 - lat2(k)], bb);
-            }
-            M[j] += bb;
+        if (i + 1 < L) {
+            const long long slot = soff + (long long)(i + 1) * T + st;
+            e_n = __ldg(a.entries + slot);
             if (LEAF) {
 #pragma unroll
-                for (int j2 = 0; j2 < (LEAF ? NA : 1); ++j2) S[j][j2] = fmaf(bb, q[j2], S[j][j2]);
+                for (int h = 0; h < (LEAF ? NAP / 4 : 0); ++h) q_n[h] = __ldg(a.qlist + slot * (NAP / 4) + h);
+            }
+        }
+        if (e == 0u) continue;                       // padding slot
+        const int ti = (int)(e & 0xFFFFu);
+        const uint32_t m8 = (e >> 16) & 0xFFu;
+        float nb[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) nb[k] = tile[ti + off[k]];
+        const float b0 = nb[4];
+        mass += b0;
+        if (LEAF) {
+#pragma unroll
+            for (int j = 0; j < (LEAF ? NA : 1); ++j) Zb[j] = fmaf(b0, q[j], Zb[j]);
+        }
+#pragma unroll
+        for (int d = 0; d < 8; ++d) {
+            const int k = dir_k(d);
+            float h = nb[8 - k];
+            if (m8 & (1u << d)) {                    // blocked target: the mass stays at y
+                h += b0;
+                E[d] += b0;
+            }
+            HM[d] += h;
+            if (LEAF) {
+#pragma unroll
+                for (int j = 0; j < (LEAF ? NA : 1); ++j) Hq[d][j] = fmaf(h, q[j], Hq[d][j]);
             }
         }
     }
-    __syncthreads();   // the tile is dead; reuse the region for the reduction
-    constexpr int RS = T + 1;   // padded row stride: no bank conflicts in the column sums
-    float *red = smem;
+    __syncthreads();   // tiles are dead; reuse the region for the fixed-order class reduction
+    constexpr int RS = T + 1;
+    float *red = smem + p * NV * RS;
+    red[0 * RS + st] = mass;
 #pragma unroll
-    for (int j = 0; j < NA; ++j) red[j * RS + t] = M[j];
+    for (int d = 0; d < 8; ++d) red[(1 + d) * RS + st] = HM[d];
     if (LEAF) {
 #pragma unroll
-        for (int j = 0; j < (LEAF ? NA : 1); ++j)
+        for (int j = 0; j < (LEAF ? NA : 1); ++j) {
+            red[(9 + j) * RS + st] = Zb[j];
 #pragma unroll
-            for (int j2 = 0; j2 < (LEAF ? NA : 1); ++j2) red[(NA + j * NA + j2) * RS + t] = S[j][j2];
+            for (int d = 0; d < (LEAF ? 8 : 1); ++d) red[(9 + NA + d * NA + j) * RS + st] = Hq[d][j];
+        }
     }
-    constexpr int RPV = LEAF ? NA + NA * NA : NA;
 #pragma unroll
-    for (int j = 0; j < NA; ++j) red[(RPV + j) * RS + t] = Rp[j];
-    red[(NV - 1) * RS + t] = mass;
+    for (int d = 0; d < 8; ++d) red[(CB + d) * RS + st] = E[d];
     __syncthreads();
-    constexpr int NCLS = 16 * RPV;       // class-binned outputs
-    constexpr int NOUT = NCLS + NA + 1;
-    double *dst = a.part + (w * a.nb + band) * (long long)a.pstride;
-    for (int o = t; o < NOUT; o += T) {
+    constexpr int NOUT = 16 * CB + 8;
+    for (int o = t; o < 2 * NOUT; o += kPairThreads) {
+        const int pp = o / NOUT, oo = o % NOUT;
+        const long long wp = 2 * pair + pp;
+        if (wp >= a.nwork) continue;
+        const float *rp = smem + pp * NV * RS;
         int vv, t0, t1;
-        if (o < NCLS) {
-            int cls;
-            if (o < 16 * NA) { cls = o / NA; vv = o % NA; }
-            else { const int r = o - 16 * NA; cls = r / (NA * NA); vv = NA + r % (NA * NA); }
+        if (oo < 16 * CB) {
+            const int cls = oo / CB;
+            vv = oo % CB;
             t0 = bi->cs[cls];
             t1 = bi->cs[cls + 1];
         } else {
-            vv = RPV + (o - NCLS);
+            vv = CB + (oo - 16 * CB);
             t0 = 0;
             t1 = T;
         }
-        double s = 0.0;
-        for (int th = t0; th < t1; ++th) s += (double)red[vv * RS + th];
-        dst[o] = s;
+        double sum = 0.0;
+        for (int th = t0; th < t1; ++th) sum += (double)rp[vv * RS + th];
+        a.part[(wp * a.nb + band) * (long long)a.pstride + oo] = sum;
     }
+    (void)valid;
 }
 
-// ---- S2 tail + S3 (+ S5 tail + S6 leaf backup): one warp per Q-node ---------------------------
+// ---- S2 tail + S3 (+ S5 tail + S6 leaf backup): one warp per parent V-node ---------------------
 struct ReduceArgs {
     const double *part;
     int pstride, nb;
-    long long nq;
+    long long nwork;
     const int32_t *vmap;
     const float *beliefs;
     long long bstride;
@@ -223,141 +248,184 @@ struct ReduceArgs {
     const int32_t *gc_cell, *gc_act;
     const double *gc_val;
     int goal;
-    double p_stay, gamma, qbar;
+    double p_stay, p_int, p_lat, gamma, qbar;
     double *R, *P;
     uint16_t *cnt, *umask;
     int32_t *U;
     uint8_t *zdraw;
     double *Q, *leafV;
-    unsigned long long *nflag;
+    unsigned long long *counters;   // [0] flagged draws, [1] leaf V-nodes
 };
 
-__device__ __forceinline__ double warp_sum_xor(double x) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    return x;
-}
+constexpr int kReduceWarps = 4;
 
 template <uint32_t MASK, bool LEAF>
-__global__ void __launch_bounds__(256) k_reduce(ReduceArgs a) {
+__host__ __device__ constexpr int reduce_smem_doubles(int pstride) {
+    return kReduceWarps * (pstride + (LEAF ? 16 * mask_count(MASK) + 16 * mask_count(MASK) : 0));
+}
+
+// The warp first sums the parent's band partials into shared memory (coalesced, fixed band
+// order, fp64), then handles the parent's |A| Q-nodes one after another: per-action
+// recombination of the linear fields -> M[s], P(z|b,a) (Eq. 3 normaliser), R(b,a),
+// n Philox draws (lane j = sample j), counts by ballot; for the leaf level also the Q_MDP value
+// of every sampled child, V(z) = qbar + max_a' [sum_s O[s][z] S[s][a']] / P(z), and the Q-node's
+// backup Q = R + gamma sum_z (f_z/n) V(z) (Alg. 6 with gamma, R13).
+template <uint32_t MASK, bool LEAF>
+__global__ void __launch_bounds__(kReduceWarps * 32) k_reduce(ReduceArgs a) {
     constexpr int NA = mask_count(MASK);
-    const int lane = threadIdx.x & 31;
-    const long long q = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-    if (q >= a.nq) return;
-    const long long w = q / NA;
-    const int j = (int)(q % NA);
-    const int k = action_of<MASK>(j);
-    const long long v = a.vmap ? (long long)a.vmap[w] : w;
+    constexpr int CB = hist_cb<MASK, LEAF>();
+    extern __shared__ double rsm[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long w = (long long)blockIdx.x * kReduceWarps + warp;
+    if (w >= a.nwork) return;
+    const int per_warp = a.pstride + (LEAF ? 32 * NA : 0);
+    double *sp = rsm + warp * per_warp;
+    double *sS = sp + a.pstride;            // [16][NA] S of the current action
+    double *sR = sS + 16 * NA;              // [16][NA] ratios of the current action
     const double *pp = a.part + w * a.nb * (long long)a.pstride;
-    constexpr int ROFF = LEAF ? 16 * NA * (1 + NA) : 16 * NA;
-
-    double Ms = 0.0, tmp = 0.0;
-    if (lane < 16)
-        for (int bd = 0; bd < a.nb; ++bd) Ms += pp[(long long)bd * a.pstride + lane * NA + j];
-    else if (lane == 16)
-        for (int bd = 0; bd < a.nb; ++bd) tmp += pp[(long long)bd * a.pstride + ROFF + NA];
-    else if (lane == 17)
-        for (int bd = 0; bd < a.nb; ++bd) tmp += pp[(long long)bd * a.pstride + ROFF + j];
-    const double mass = __shfl_sync(0xffffffffu, tmp, 16);
-    const double Rp = __shfl_sync(0xffffffffu, tmp, 17);
-
-    // R(b,a) = sum_x R(x,a) b(x) via the stencil identity of model.cu
+    for (int i = lane; i < a.pstride; i += 32) {
+        double acc = 0.0;
+        for (int bd = 0; bd < a.nb; ++bd) acc += pp[(long long)bd * a.pstride + i];
+        sp[i] = acc;
+    }
+    __syncwarp();
+    const long long v = a.vmap ? (long long)a.vmap[w] : w;
     const float *bp = a.beliefs + v * a.bstride;
-    double R = 0.0;
-    if (lane == 0) {
-        if (k == 4) {
-            R = -2.0 * mass + 2.0 * (double)bp[a.goal];
-        } else {
-            R = (a.p_stay - 1.0) * mass - Rp;
-            for (int g = 0; g < a.ngc; ++g)
-                if (a.gc_act[g] == j) R += a.gc_val[g] * (double)bp[a.gc_cell[g]];
-        }
-    }
-    // P(z|b,a) = sum_s O[s][z] M[s]   (Eq. 3 normaliser, fixed s order)
-    double Pz = 0.0;
+    const double mass_s = lane < 16 ? sp[lane * CB] : 0.0;
+    double mass = 0.0;
 #pragma unroll
-    for (int s = 0; s < 16; ++s) {
-        const double m = __shfl_sync(0xffffffffu, Ms, s);
-        if (lane < 16) Pz += a.O64[s * 16 + lane] * m;
-    }
-    double C[16];
-    double acc = 0.0;
-#pragma unroll
-    for (int z = 0; z < 16; ++z) {
-        acc += __shfl_sync(0xffffffffu, Pz, z);
-        C[z] = acc;
-    }
-    // S3: n draws keyed by tree path (Appendix A.2-A.5)
-    const uint64_t qpath = a.vpath[v] | ((uint64_t)(k + 1) << (8 * a.level));
+    for (int s = 0; s < 16; ++s) mass += __shfl_sync(0xffffffffu, mass_s, s);
+    const uint64_t vpath = a.vpath[v];
     const int root = a.vroot[v];
     const uint32_t step = a.root_step[root], ep = a.root_ep[root];
-    int cntk = 0, nflag = 0;
-    for (int j0 = 0; j0 < a.n; j0 += 32) {
-        const int jj = j0 + lane;
-        const bool act = jj < a.n;
-        int z = -1;
-        if (act) {
-            const uint4 r = philox4x32_10(make_uint4((uint32_t)jj, (uint32_t)qpath, (uint32_t)(qpath >> 32), step),
-                                          make_uint2(a.seed, ep));
-            const double u = ((double)(r.x >> 8) + 0.5) * (1.0 / 16777216.0);
-            const double tt = u * C[15];
-            z = 0;
-            double gap = INFINITY;
+    int leaves = 0, nflag = 0;
+
+    for (int j = 0; j < NA; ++j) {
+        const long long q = w * NA + j;
+        const int k = action_of<MASK>(j);
+        const int da = k == 4 ? 0 : nbit(k), d1 = k == 4 ? 0 : nbit(lat1(k)), d2 = k == 4 ? 0 : nbit(lat2(k));
+        // M[s]: bbar_a summed over signature class s
+        double Ms = 0.0;
+        if (lane < 16) {
+            const double *c = sp + lane * CB;
+            Ms = (k == 4) ? c[0] : a.p_stay * c[0] + a.p_int * c[1 + da] + a.p_lat * (c[1 + d1] + c[1 + d2]);
+        }
+        // R(b,a) = (p_stay - 1) sum b - sum c_a b + goal terms, sum c_a b = p_stay mass + p_int E_a + p_lat (E_l1 + E_l2)
+        double R = 0.0;
+        if (lane == 0) {
+            if (k == 4) {
+                R = -2.0 * mass + 2.0 * (double)bp[a.goal];
+            } else {
+                const double *E = sp + 16 * CB;
+                const double Rp = a.p_stay * mass + a.p_int * E[da] + a.p_lat * (E[d1] + E[d2]);
+                R = (a.p_stay - 1.0) * mass - Rp;
+                for (int g = 0; g < a.ngc; ++g)
+                    if (a.gc_act[g] == j) R += a.gc_val[g] * (double)bp[a.gc_cell[g]];
+            }
+        }
+        // P(z|b,a) = sum_s O[s][z] M[s]  (fixed s order)
+        double Pz = 0.0;
+#pragma unroll
+        for (int s = 0; s < 16; ++s) {
+            const double m = __shfl_sync(0xffffffffu, Ms, s);
+            if (lane < 16) Pz += a.O64[s * 16 + lane] * m;
+        }
+        double C[16];
+        double acc = 0.0;
+#pragma unroll
+        for (int z = 0; z < 16; ++z) {
+            acc += __shfl_sync(0xffffffffu, Pz, z);
+            C[z] = acc;
+        }
+        // S3: n draws keyed by the tree path (Appendix A.2-A.5)
+        const uint64_t qpath = vpath | ((uint64_t)(k + 1) << (8 * a.level));
+        int cntk = 0;
+        for (int j0 = 0; j0 < a.n; j0 += 32) {
+            const int jj = j0 + lane;
+            int z = -1;
+            if (jj < a.n) {
+                const uint4 r = philox4x32_10(make_uint4((uint32_t)jj, (uint32_t)qpath, (uint32_t)(qpath >> 32), step),
+                                              make_uint2(a.seed, ep));
+                const double u = ((double)(r.x >> 8) + 0.5) * (1.0 / 16777216.0);
+                const double tt = u * C[15];
+                z = 0;
+                double gap = INFINITY;
+#pragma unroll
+                for (int kk = 0; kk < 16; ++kk) {
+                    z += (C[kk] <= tt) ? 1 : 0;
+                    if (kk < 15) gap = fmin(gap, fabs(tt - C[kk]));
+                }
+                z = min(z, 15);
+                nflag += gap < 1e-6 ? 1 : 0;
+                if (a.zdraw) a.zdraw[q * a.n + jj] = (uint8_t)z;
+            }
 #pragma unroll
             for (int kk = 0; kk < 16; ++kk) {
-                z += (C[kk] <= tt) ? 1 : 0;
-                if (kk < 15) gap = fmin(gap, fabs(tt - C[kk]));
+                const unsigned bal = __ballot_sync(0xffffffffu, z == kk);
+                if (lane == kk) cntk += __popc(bal);
             }
-            z = min(z, 15);
-            nflag += gap < 1e-6 ? 1 : 0;
-            if (a.zdraw) a.zdraw[q * a.n + jj] = (uint8_t)z;
         }
+        const unsigned um = __ballot_sync(0xffffffffu, lane < 16 && cntk > 0) & 0xFFFFu;
+        const int U = __popc(um);
+        leaves += U;
+        if (lane < 16) {
+            a.P[q * 16 + lane] = Pz;
+            a.cnt[q * 16 + lane] = (uint16_t)cntk;
+        }
+        if (lane == 0) {
+            a.R[q] = R;
+            a.umask[q] = (uint16_t)um;
+            a.U[q] = U;
+        }
+        if (LEAF) {
+            // S[s][a'] of this action from the linear fields, staged for the (z, a') dot products
+            if (lane < 16) {
+                const double *c = sp + lane * CB;
 #pragma unroll
-        for (int kk = 0; kk < 16; ++kk) {
-            const unsigned bal = __ballot_sync(0xffffffffu, z == kk);
-            if (lane == kk) cntk += __popc(bal);
+                for (int j2 = 0; j2 < NA; ++j2) {
+                    const double zb = c[9 + j2];
+                    sS[lane * NA + j2] = (k == 4) ? zb
+                                                  : a.p_stay * zb + a.p_int * c[9 + NA + da * NA + j2] +
+                                                        a.p_lat * (c[9 + NA + d1 * NA + j2] + c[9 + NA + d2 * NA + j2]);
+                }
+            }
+            __syncwarp();
+            // lane -> (u, a'): ratio = sum_s O[s][z_u] S[s][a'] / P(z_u)
+            for (int idx = lane; idx < U * NA; idx += 32) {
+                const int u = idx / NA, j2 = idx % NA;
+                unsigned rem = um;
+                for (int i = 0; i < u; ++i) rem &= rem - 1;
+                const int z = __ffs(rem) - 1;
+                double num = 0.0;
+#pragma unroll
+                for (int s = 0; s < 16; ++s) num += a.O64[s * 16 + z] * sS[s * NA + j2];
+                sR[u * NA + j2] = num;
+            }
+            __syncwarp();
+            // frequencies live in lanes 0..15: gather them for lane 0 in z order
+            double accq = 0.0;
+            unsigned rem = um;
+            for (int u = 0; u < U; ++u) {
+                const int z = __ffs(rem) - 1;
+                rem &= rem - 1;
+                const int f = __shfl_sync(0xffffffffu, cntk, z);
+                const double Pzz = __shfl_sync(0xffffffffu, Pz, z);
+                if (lane == 0) {
+                    double best = -INFINITY;
+                    for (int j2 = 0; j2 < NA; ++j2) best = fmax(best, sR[u * NA + j2]);
+                    const double Vz = a.qbar + best / Pzz;
+                    accq += ((double)f / (double)a.n) * Vz;
+                    if (a.leafV) a.leafV[q * 16 + z] = Vz;
+                }
+            }
+            if (lane == 0) a.Q[q] = R + a.gamma * accq;
+            __syncwarp();
         }
     }
-    const unsigned um = __ballot_sync(0xffffffffu, lane < 16 && cntk > 0) & 0xFFFFu;
     for (int o = 16; o > 0; o >>= 1) nflag += __shfl_xor_sync(0xffffffffu, nflag, o);
-    if (lane < 16) {
-        a.P[q * 16 + lane] = Pz;
-        a.cnt[q * 16 + lane] = (uint16_t)cntk;
-    }
-    if (lane == 0) {
-        a.R[q] = R;
-        a.umask[q] = (uint16_t)um;
-        a.U[q] = __popc(um);
-        if (nflag && a.nflag) atomicAdd(a.nflag, (unsigned long long)nflag);
-    }
-    if (LEAF) {
-        // S5: V(b') = qbar + max_a' [sum_s O[s][z] S[s][a']] / [sum_s O[s][z] M[s]]
-        double Sv[LEAF ? NA : 1];
-#pragma unroll
-        for (int j2 = 0; j2 < (LEAF ? NA : 1); ++j2) Sv[j2] = 0.0;
-        if (lane < 16)
-            for (int bd = 0; bd < a.nb; ++bd) {
-                const double *ps = pp + (long long)bd * a.pstride + 16 * NA + (lane * NA + j) * NA;
-#pragma unroll
-                for (int j2 = 0; j2 < (LEAF ? NA : 1); ++j2) Sv[j2] += ps[j2];
-            }
-        const double Rq = __shfl_sync(0xffffffffu, R, 0);
-        double accq = 0.0;
-        unsigned rem = um;
-        while (rem) {
-            const int z = __ffs(rem) - 1;
-            rem &= rem - 1;
-            const double Oz = lane < 16 ? a.O64[lane * 16 + z] : 0.0;
-            const double Pzz = __shfl_sync(0xffffffffu, Pz, z);
-            const int f = __shfl_sync(0xffffffffu, cntk, z);
-            double best = -INFINITY;
-#pragma unroll
-            for (int j2 = 0; j2 < (LEAF ? NA : 1); ++j2) best = fmax(best, warp_sum_xor(Oz * Sv[j2]) / Pzz);
-            const double Vz = a.qbar + best;
-            accq += ((double)f / (double)a.n) * Vz;
-            if (a.leafV && lane == 0) a.leafV[q * 16 + z] = Vz;
-        }
-        if (lane == 0) a.Q[q] = Rq + a.gamma * accq;
+    if (lane == 0 && a.counters) {
+        if (nflag) atomicAdd(&a.counters[0], (unsigned long long)nflag);
+        if (LEAF) atomicAdd(&a.counters[1], (unsigned long long)leaves);
     }
 }
 
@@ -399,12 +467,16 @@ __global__ void __launch_bounds__(1024) k_scan(const int32_t *__restrict__ U, in
 }
 
 // ---- S4: Bayes correction of every unique z of a Q-node ----------------------------------------
+// One CTA = one Q-node x 1024 cells (4 consecutive cells of one row per thread).  The thread
+// predicts bbar_a for its 4 cells once (linear form of k_hist) and writes every child
+// b'_z = O(y,z) bbar_a(y) / P(z|b,a) (Eq. 3) with float4 stores; w_z[s] = O[s][z] / P(z) is
+// formed in fp64 and staged in shared memory.
 struct CorrectArgs {
     const float *beliefs;
     long long bstride;
     const int32_t *vmap;
     const uint8_t *m8, *cell;
-    const float *ctab, *O32;
+    const double *O64;
     const double *P;
     const uint16_t *cnt, *umask;
     const int32_t *off;
@@ -415,10 +487,42 @@ struct CorrectArgs {
     long long cstride;
     uint64_t *cpath;
     int32_t *cparent, *cz, *cf, *croot;
-    int H, W, HW, NAP, ntiles;
-    float p_int, p_lat;
+    int H, W, G, ntiles;
+    float p_int, p_stay, p_lat;
     long long qsel;   // >= 0: only this Q-node (belief_update)
 };
+
+// bbar_a for 4 consecutive cells (r, c0..c0+3): bbar = p_stay b + p_int h_a + p_lat (h_l1 + h_l2),
+// h_k = b(y - d_k) + occ(y + d_k) b(y); stay: bbar = b.  nbh holds rows r-1..r+1, cols c0-1..c0+4.
+template <int K>
+__device__ __forceinline__ void correct_predict(const CorrectArgs &a, int r, int c0, const float (&nbh)[3][6],
+                                                float (&bb)[4], int (&sg)[4]) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int c = c0 + i;
+        bb[i] = 0.f;
+        sg[i] = 0;
+        if (c >= a.W) continue;
+        const int x = r * a.W + c;
+        const int info = __ldg(a.cell + x);
+        sg[i] = info & 15;
+        if (info & 16) continue;                      // occupied: no mass
+        const float b0 = nbh[1][1 + i];
+        if (K == 4) {
+            bb[i] = b0;
+        } else {
+            const int m8 = __ldg(a.m8 + x);
+            constexpr int L1 = lat1(K), L2 = lat2(K);
+            const float sa = nbh[1 - st_dr(K)][1 + i - st_dc(K)];
+            const float s1 = nbh[1 - st_dr(L1)][1 + i - st_dc(L1)];
+            const float s2 = nbh[1 - st_dr(L2)][1 + i - st_dc(L2)];
+            const float ha = ((m8 >> nbit(K)) & 1) ? sa + b0 : sa;
+            const float h1 = ((m8 >> nbit(L1)) & 1) ? s1 + b0 : s1;
+            const float h2 = ((m8 >> nbit(L2)) & 1) ? s2 + b0 : s2;
+            bb[i] = fmaf(a.p_lat, h1 + h2, fmaf(a.p_int, ha, a.p_stay * b0));
+        }
+    }
+}
 
 template <uint32_t MASK>
 __global__ void __launch_bounds__(256) k_correct(CorrectArgs a) {
@@ -432,16 +536,17 @@ __global__ void __launch_bounds__(256) k_correct(CorrectArgs a) {
     const unsigned um = a.umask[q];
     const int U = __popc(um);
     const long long base = a.qsel >= 0 ? 0 : a.off[q];
-    __shared__ float s_inv[16];
-    __shared__ int s_z[16];
-    if (threadIdx.x < 16) {
-        const int z = threadIdx.x;
-        if ((um >> z) & 1u) {
-            const int rank = __popc(um & ((1u << z) - 1u));
-            s_z[rank] = z;
-            s_inv[rank] = (float)(1.0 / a.P[q * 16 + z]);
-            if (tile == 0 && a.cpath) {
-                const long long c = base + rank;
+    __shared__ float s_w[16][16];   // [rank u][signature s] = O[s][z_u] / P(z_u)
+    {
+        const int t = threadIdx.x;
+        const int u = t >> 4, sg = t & 15;
+        if (u < U) {
+            unsigned rem = um;
+            for (int i = 0; i < u; ++i) rem &= rem - 1;
+            const int z = __ffs(rem) - 1;
+            s_w[u][sg] = (float)(a.O64[sg * 16 + z] / a.P[q * 16 + z]);
+            if (tile == 0 && sg == 0 && a.cpath) {
+                const long long c = base + u;
                 a.cpath[c] = a.vpath[v] | ((uint64_t)(k + 1) << (8 * a.level)) | ((uint64_t)z << (8 * a.level + 4));
                 a.cparent[c] = (int32_t)q;
                 a.cz[c] = z;
@@ -451,49 +556,50 @@ __global__ void __launch_bounds__(256) k_correct(CorrectArgs a) {
         }
     }
     __syncthreads();
-    const long long x0 = ((long long)tile * blockDim.x + threadIdx.x) * 4;
-    if (x0 >= a.HW) return;
+    const int idx = tile * 256 + threadIdx.x;
+    const int r = idx / a.G, g = idx - (idx / a.G) * a.G;
+    if (r >= a.H) return;
+    const int W = a.W, c0 = 4 * g;
     const float *__restrict__ b = a.beliefs + v * a.bstride;
+    // rows r-1..r+1, columns c0-1..c0+4 (zero off-map)
+    float nbh[3][6];
+#pragma unroll
+    for (int dr = 0; dr < 3; ++dr) {
+        const int rr = r + dr - 1;
+        const bool rok = rr >= 0 && rr < a.H;
+        const float *row = b + (long long)rr * W;
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+            const int cc = c0 - 1 + i;
+            nbh[dr][i] = (rok && cc >= 0 && cc < W) ? __ldg(row + cc) : 0.f;
+        }
+    }
     float bb[4];
     int sg[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const long long x = x0 + i;
-        bb[i] = 0.f;
-        sg[i] = 0;
-        if (x >= a.HW) continue;
-        const int ci = a.cell[x];
-        sg[i] = ci & 15;
-        if (ci & 16) continue;                      // occupied: bbar = 0
-        const float b0 = b[x];
-        if (k == 4) { bb[i] = b0; continue; }
-        const int r = (int)(x / a.W), c = (int)(x % a.W);
-        auto src = [&](int kk) -> float {           // b(y - d_kk), zero off-map
-            const int rr = r - st_dr(kk), cc = c - st_dc(kk);
-            if (rr < 0 || rr >= a.H || cc < 0 || cc >= a.W) return 0.f;
-            return b[(long long)rr * a.W + cc];
-        };
-        const int m8 = a.m8[x];
-        // runtime stencil id k: the laterals come from the ring (reading R3)
-        const float s_int = src(k);
-        const float s_lat = src(lat1(k)) + src(lat2(k));
-        const float tt = a.ctab[m8 * a.NAP + j] * b0;
-        bb[i] = fmaf(a.p_lat, s_lat, fmaf(a.p_int, s_int, tt));
+    switch (k) {   // block-uniform: compile-time tap geometry per action
+        case 0: correct_predict<0>(a, r, c0, nbh, bb, sg); break;
+        case 1: correct_predict<1>(a, r, c0, nbh, bb, sg); break;
+        case 2: correct_predict<2>(a, r, c0, nbh, bb, sg); break;
+        case 3: correct_predict<3>(a, r, c0, nbh, bb, sg); break;
+        case 4: correct_predict<4>(a, r, c0, nbh, bb, sg); break;
+        case 5: correct_predict<5>(a, r, c0, nbh, bb, sg); break;
+        case 6: correct_predict<6>(a, r, c0, nbh, bb, sg); break;
+        case 7: correct_predict<7>(a, r, c0, nbh, bb, sg); break;
+        default: correct_predict<8>(a, r, c0, nbh, bb, sg); break;
     }
-    const bool vec = ((a.cstride & 3) == 0) && (x0 + 3 < a.HW) && ((reinterpret_cast<uintptr_t>(a.child) & 15) == 0);
+    const long long x0 = (long long)r * W + c0;
+    const bool vec = ((W & 3) == 0) && ((a.cstride & 3) == 0);
     for (int u = 0; u < U; ++u) {
-        const int z = s_z[u];
-        const float inv = s_inv[u];
         float o[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) o[i] = a.O32[sg[i] * 16 + z] * bb[i] * inv;
+        for (int i = 0; i < 4; ++i) o[i] = s_w[u][sg[i]] * bb[i];
         float *dst = a.child + (base + u) * a.cstride + x0;
         if (vec) {
             *reinterpret_cast<float4 *>(dst) = make_float4(o[0], o[1], o[2], o[3]);
         } else {
 #pragma unroll
             for (int i = 0; i < 4; ++i)
-                if (x0 + i < a.HW) dst[i] = o[i];
+                if (c0 + i < W) dst[i] = o[i];
         }
     }
 }
@@ -556,41 +662,42 @@ static inline unsigned nblk(long long n, int b) { return (unsigned)((n + b - 1) 
     } while (0)
 
 template <uint32_t MASK, bool LEAF>
-static size_t hist_smem(const BandSet &bs) {
-    constexpr int NA = mask_count(MASK), NAP = (NA + 3) & ~3;
-    const size_t region = std::max<size_t>(bs.tile_floats, (size_t)hist_nv<MASK, LEAF>() * (kHistThreads + 1));
-    return (region + 256 * NAP) * sizeof(float);
-}
-
-template <uint32_t MASK, bool LEAF>
 static qvts_status launch_hist(Model &m, const BandSet &bs, const float *beliefs, long long bstride,
                                const int32_t *vmap, long long nwork, int pstride, cudaStream_t st) {
-    constexpr int NAP = (mask_count(MASK) + 3) & ~3;
     HistArgs a;
-    a.beliefs = beliefs; a.bstride = bstride; a.vmap = vmap;
+    a.beliefs = beliefs; a.bstride = bstride; a.vmap = vmap; a.nwork = nwork;
     a.bands = bs.bands.as<BandInfo>(); a.nb = bs.nb;
     a.entries = bs.entries.as<uint32_t>();
     a.qlist = bs.qlist.as<float4>();
-    a.ctab = m.d_ctab.as<float>();
     a.H = m.H; a.W = m.W; a.TW = m.W + 2;
-    a.region_floats = (int)std::max<size_t>(bs.tile_floats, (size_t)hist_nv<MASK, LEAF>() * (kHistThreads + 1));
-    a.region_floats = (a.region_floats + 3) & ~3;
-    a.p_int = (float)m.p_int; a.p_lat = (float)m.p_lat;
+    // second tile offset = 16 banks modulo 32, so the two half-warps never share a bank
+    a.tstride = ((bs.tile_floats + 31) & ~31) + 16;
+    const size_t red = (size_t)2 * hist_nv<MASK, LEAF>() * (kHistThreads + 1);
+    a.region_floats = (int)std::max<size_t>((size_t)2 * a.tstride, red);
     a.part = m.part.as<double>(); a.pstride = pstride;
-    const size_t smem = (a.region_floats + 256 * NAP) * sizeof(float);
+    const size_t smem = (size_t)a.region_floats * sizeof(float);
     QVTS_CUDA(cudaFuncSetAttribute(k_hist<MASK, LEAF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const long long nblocks = nwork * bs.nb;
+    const long long nblocks = ((nwork + 1) / 2) * bs.nb;
     if (nblocks > 0x7FFFFFFFLL) { set_error("too many hist blocks"); return QVTS_ERR_INVALID_ARG; }
-    QVTS_PROF(LEAF ? 0 : 1, k_hist<MASK, LEAF><<<(unsigned)nblocks, kHistThreads, smem, st>>>(a));
+    QVTS_PROF(LEAF ? 0 : 1, k_hist<MASK, LEAF><<<(unsigned)nblocks, kPairThreads, smem, st>>>(a));
     QVTS_CUDA(cudaGetLastError());
     (LEAF ? m.pstat.leaf_cells : m.pstat.hist_cells) += nwork * m.n_free;
     return QVTS_OK;
 }
 
+template <uint32_t MASK, bool LEAF>
+static qvts_status launch_reduce(Model &m, const ReduceArgs &r, cudaStream_t st) {
+    constexpr int NA = mask_count(MASK);
+    const size_t smem = sizeof(double) * kReduceWarps * (r.pstride + (LEAF ? 32 * NA : 0));
+    QVTS_CUDA(cudaFuncSetAttribute(k_reduce<MASK, LEAF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    QVTS_PROF(LEAF ? 2 : 3, k_reduce<MASK, LEAF><<<nblk(r.nwork, kReduceWarps), kReduceWarps * 32, smem, st>>>(r));
+    QVTS_CUDA(cudaGetLastError());
+    return QVTS_OK;
+}
+
 template <uint32_t MASK>
 static int pstride_of(bool leaf) {
-    constexpr int NA = mask_count(MASK);
-    return 16 * NA * (leaf ? 1 + NA : 1) + NA + 1;
+    return 16 * (leaf ? hist_cb<MASK, true>() : hist_cb<MASK, false>()) + 8;
 }
 
 template <uint32_t MASK>
@@ -647,26 +754,26 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
             if (leaf) QVTS_TRY(ql.leafV.ensure(sizeof(double) * 16 * std::max(1LL, nq)));
         }
         if (nwork > 0) {
-            const BandSet &bs = (nwork * m.band_big.nb < 4 * 148) ? m.band_small : m.band_big;
+            const BandSet &bs = (((nwork + 1) / 2) * m.band_big.nb < 2 * 148) ? m.band_small : m.band_big;
             const int pstride = pstride_of<MASK>(leaf);
             QVTS_TRY(m.part.ensure(sizeof(double) * (size_t)nwork * bs.nb * pstride));
             if (leaf) QVTS_TRY((launch_hist<MASK, true>(m, bs, bel, bstride, vmap, nwork, pstride, st)));
             else QVTS_TRY((launch_hist<MASK, false>(m, bs, bel, bstride, vmap, nwork, pstride, st)));
             ReduceArgs r;
-            r.part = m.part.as<double>(); r.pstride = pstride; r.nb = bs.nb; r.nq = nq; r.vmap = vmap;
+            r.part = m.part.as<double>(); r.pstride = pstride; r.nb = bs.nb; r.nwork = nwork; r.vmap = vmap;
             r.beliefs = bel; r.bstride = bstride; r.vpath = vl.path.as<uint64_t>(); r.vroot = vl.root.as<int32_t>();
             r.root_step = roots.step_dev; r.root_ep = roots.episode_dev; r.seed = cfg.seed;
             r.level = d; r.n = n; r.O64 = m.d_O64.as<double>();
             r.ngc = m.ngc; r.gc_cell = m.d_gc_cell.as<int32_t>(); r.gc_act = m.d_gc_act.as<int32_t>();
             r.gc_val = m.d_gc_val.as<double>(); r.goal = m.goal;
-            r.p_stay = m.p_stay; r.gamma = m.gamma; r.qbar = m.qbar;
+            r.p_stay = m.p_stay; r.p_int = m.p_int; r.p_lat = m.p_lat; r.gamma = m.gamma; r.qbar = m.qbar;
             r.R = ql.R.as<double>(); r.P = ql.P.as<double>(); r.cnt = ql.cnt.as<uint16_t>();
             r.umask = ql.umask.as<uint16_t>(); r.U = ql.U.as<int32_t>();
             r.zdraw = trace ? ql.zdraw.as<uint8_t>() : nullptr;
             r.Q = ql.Q.as<double>(); r.leafV = (trace && leaf) ? ql.leafV.as<double>() : nullptr;
-            r.nflag = m.counters.as<unsigned long long>();
-            if (leaf) QVTS_PROF(2, k_reduce<MASK, true><<<nblk(nq * 32, 256), 256, 0, st>>>(r));
-            else QVTS_PROF(3, k_reduce<MASK, false><<<nblk(nq * 32, 256), 256, 0, st>>>(r));
+            r.counters = m.counters.as<unsigned long long>();
+            if (leaf) QVTS_TRY((launch_reduce<MASK, true>(m, r, st)));
+            else QVTS_TRY((launch_reduce<MASK, false>(m, r, st)));
             QVTS_CUDA(cudaGetLastError());
         }
         if (leaf) break;
@@ -692,34 +799,22 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
         if (nq > 0) {
             CorrectArgs c;
             c.beliefs = bel; c.bstride = bstride; c.vmap = vmap;
-            c.m8 = m.d_m8.as<uint8_t>(); c.cell = m.d_cell.as<uint8_t>(); c.ctab = m.d_ctab.as<float>();
-            c.O32 = m.d_O32.as<float>(); c.P = ql.P.as<double>(); c.cnt = ql.cnt.as<uint16_t>();
+            c.m8 = m.d_m8.as<uint8_t>(); c.cell = m.d_cell.as<uint8_t>();
+            c.O64 = m.d_O64.as<double>(); c.P = ql.P.as<double>(); c.cnt = ql.cnt.as<uint16_t>();
             c.umask = ql.umask.as<uint16_t>(); c.off = ql.off.as<int32_t>();
             c.vpath = vl.path.as<uint64_t>(); c.vroot = vl.root.as<int32_t>(); c.level = d;
             c.child = vc.belief.as<float>(); c.cstride = m.HWp;
             c.cpath = vc.path.as<uint64_t>(); c.cparent = vc.parent_q.as<int32_t>(); c.cz = vc.z.as<int32_t>();
             c.cf = vc.f.as<int32_t>(); c.croot = vc.root.as<int32_t>();
-            c.H = m.H; c.W = m.W; c.HW = m.HW; c.NAP = m.NAP;
-            c.ntiles = (int)((m.HW + 1023) / 1024);
-            c.p_int = (float)m.p_int; c.p_lat = (float)m.p_lat; c.qsel = -1;
+            c.H = m.H; c.W = m.W; c.G = (m.W + 3) / 4;
+            c.ntiles = (int)(((long long)m.H * c.G + 255) / 256);
+            c.p_int = (float)m.p_int; c.p_stay = (float)m.p_stay; c.p_lat = (float)m.p_lat; c.qsel = -1;
             const long long nblocks = nq * c.ntiles;
             if (nblocks > 0x7FFFFFFFLL) { set_error("too many correct blocks"); return QVTS_ERR_INVALID_ARG; }
             QVTS_PROF(5, k_correct<MASK><<<(unsigned)nblocks, 256, 0, st>>>(c));
             QVTS_CUDA(cudaGetLastError());
             m.pstat.correct_cells_written += total * (long long)m.HW;
         }
-    }
-    // leaf V-node count (not materialised): sum of unique counts of the last Q-level
-    {
-        QLevel &ql = m.ql[D - 1];
-        long long nq = ql.nwork * NA, total = 0;
-        if (nq > 0) {
-            QVTS_PROF(4, k_scan<<<1, 1024, 0, st>>>(ql.U.as<int32_t>(), ql.off.as<int32_t>(), nq, m.total.as<long long>()));
-            QVTS_CUDA(cudaGetLastError());
-            QVTS_CUDA(cudaMemcpyAsync(&total, m.total.p, sizeof(long long), cudaMemcpyDeviceToHost, st));
-            QVTS_CUDA(cudaStreamSynchronize(st));
-        }
-        nv_out[D] = total;
     }
     // S6 backup, bottom-up
     for (int d = D - 1; d >= 0; --d) {
@@ -747,6 +842,12 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
             }
         }
     }
+    // leaf V-node count (not materialised) and flagged-draw count, accumulated by k_reduce
+    unsigned long long cnts[2] = {0, 0};
+    QVTS_CUDA(cudaMemcpyAsync(cnts, m.counters.p, sizeof(cnts), cudaMemcpyDeviceToHost, st));
+    QVTS_CUDA(cudaStreamSynchronize(st));
+    nv_out[D] = (long long)cnts[1];
+    m.last_flagged = (long long)cnts[0];
     m.last_depth = D;
     m.last_shard_level = shard_level;
     m.last_n = n;
@@ -846,15 +947,15 @@ extern "C" qvts_status qvts_belief_update(qvts_model *m, const float *b_dev, int
         if (s == QVTS_OK) {                                                                                   \
             ReduceArgs r;                                                                                     \
             std::memset(&r, 0, sizeof(r));                                                                    \
-            r.part = m->part.as<double>(); r.pstride = ps; r.nb = bs.nb; r.nq = NA;                           \
+            r.part = m->part.as<double>(); r.pstride = ps; r.nb = bs.nb; r.nwork = 1;                          \
             r.beliefs = b_dev; r.bstride = m->HW; r.vpath = m->bu_path.as<uint64_t>();                        \
             r.vroot = m->bu_root.as<int32_t>(); r.root_step = m->bu_key.as<uint32_t>();                       \
             r.root_ep = m->bu_key.as<uint32_t>() + 1; r.n = 1; r.O64 = m->d_O64.as<double>();                 \
             r.ngc = m->ngc; r.gc_cell = m->d_gc_cell.as<int32_t>(); r.gc_act = m->d_gc_act.as<int32_t>();     \
-            r.gc_val = m->d_gc_val.as<double>(); r.goal = m->goal; r.p_stay = m->p_stay; r.gamma = m->gamma;  \
+            r.gc_val = m->d_gc_val.as<double>(); r.goal = m->goal; r.p_stay = m->p_stay; r.p_int = m->p_int; r.p_lat = m->p_lat; r.gamma = m->gamma;  \
             r.R = m->bu_R.as<double>(); r.P = m->bu_P.as<double>(); r.cnt = m->bu_cnt.as<uint16_t>();         \
             r.umask = m->bu_umask.as<uint16_t>(); r.U = m->bu_U.as<int32_t>();                                \
-            k_reduce<MASK, false><<<nblk((long long)NA * 32, 256), 256, 0, st>>>(r);                          \
+            s = launch_reduce<MASK, false>(*m, r, st);                                                        \
         }                                                                                                     \
     }
     QVTS_DISPATCH_MASK(m->mask, QVTS_BU_HIST);
@@ -873,11 +974,12 @@ extern "C" qvts_status qvts_belief_update(qvts_model *m, const float *b_dev, int
     CorrectArgs c;
     std::memset(&c, 0, sizeof(c));
     c.beliefs = b_dev; c.bstride = m->HW; c.m8 = m->d_m8.as<uint8_t>(); c.cell = m->d_cell.as<uint8_t>();
-    c.ctab = m->d_ctab.as<float>(); c.O32 = m->d_O32.as<float>(); c.P = m->bu_P.as<double>();
+    c.O64 = m->d_O64.as<double>(); c.P = m->bu_P.as<double>();
     c.cnt = m->bu_cnt.as<uint16_t>(); c.umask = m->bu_umask.as<uint16_t>(); c.off = m->bu_off.as<int32_t>();
     c.vpath = m->bu_path.as<uint64_t>(); c.vroot = m->bu_root.as<int32_t>();
-    c.child = out_dev; c.cstride = m->HW; c.H = m->H; c.W = m->W; c.HW = m->HW; c.NAP = m->NAP;
-    c.ntiles = (int)((m->HW + 1023) / 1024); c.p_int = (float)m->p_int; c.p_lat = (float)m->p_lat; c.qsel = j;
+    c.child = out_dev; c.cstride = m->HW; c.H = m->H; c.W = m->W; c.G = (m->W + 3) / 4;
+    c.ntiles = (int)(((long long)m->H * c.G + 255) / 256);
+    c.p_int = (float)m->p_int; c.p_stay = (float)m->p_stay; c.p_lat = (float)m->p_lat; c.qsel = j;
 #define QVTS_BU_CORR(MASK) k_correct<MASK><<<c.ntiles, 256, 0, st>>>(c)
     QVTS_DISPATCH_MASK(m->mask, QVTS_BU_CORR);
 #undef QVTS_BU_CORR

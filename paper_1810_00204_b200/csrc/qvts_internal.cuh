@@ -10,7 +10,8 @@
 
 namespace qvts {
 
-constexpr int kHistThreads = 256;   // threads per hist CTA (one class stream per thread)
+constexpr int kHistThreads = 256;   // slot-threads per band list (one class stream per slot-thread)
+constexpr int kPairThreads = 512;   // hist CTA: 2 parents x 256 slot-threads
 constexpr int kMaxLevels = 9;       // depth <= 8
 
 void set_error(const std::string &msg);
@@ -90,6 +91,7 @@ struct Model {
     QLevel ql[kMaxLevels];
     DevBuf part, scan_tmp, total, counters, vshard;
     int last_depth = -1, last_n = 0, last_shard_level = -1;
+    long long last_flagged = 0;
     bool last_trace = false;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // instrumentation
