@@ -86,10 +86,10 @@ void prof_collect(Model &m) {
 // 8-neighbour occupancy byte m8.
 qvts_status build_bands(Model &m, BandSet &bs, int rows) {
     const int T = kHistThreads;
-    const int H = m.H, W = m.W, TW = W + 2;
+    const int H = m.H, W = m.W, TW = (W + 5 + 3) & ~3;   // row pitch; grid column c at tile column c + 4
     rows = std::max(1, std::min(rows, H));
     // two parents' tiles per hist CTA must fit in shared memory (~190 KB) and index in 16 bits
-    while (rows > 1 && ((long long)(rows + 2) * TW > 65535 || (long long)(rows + 2) * TW * 8 > 190000)) --rows;
+    while (rows > 1 && ((long long)(rows + 2) * TW > 65535 || (long long)(rows + 2) * TW * 8 > 72000)) --rows;
     if ((long long)(rows + 2) * TW > 65535) {
         set_error("grid too wide for the band tile (W+2)*3 > 65535");
         return QVTS_ERR_INVALID_ARG;
@@ -97,6 +97,7 @@ qvts_status build_bands(Model &m, BandSet &bs, int rows) {
     bs.rows = rows;
     bs.nb = (H + rows - 1) / rows;
     bs.tile_floats = (rows + 2) * TW;
+    bs.tile_pitch = TW;
     bs.h_bands.assign(bs.nb, BandInfo{});
     std::vector<uint32_t> entries;
     bs.h_slot_cell.clear();
@@ -143,7 +144,7 @@ qvts_status build_bands(Model &m, BandSet &bs, int rows) {
             head[c].assign(16, 0);
             for (int x : cls[c]) {
                 int r = x / W, cc = x % W;
-                int ti = (r - bi.row0 + 1) * TW + (cc + 1);
+                int ti = (r - bi.row0 + 1) * TW + (cc + 4);
                 bucket[c][ti & 15].push_back(x);
             }
         }
@@ -167,7 +168,7 @@ qvts_status build_bands(Model &m, BandSet &bs, int rows) {
                     const int x = bucket[c][best][head[c][best]++];
                     used |= 1u << best;
                     int r = x / W, cc = x % W;
-                    int ti = (r - bi.row0 + 1) * TW + (cc + 1);
+                    int ti = (r - bi.row0 + 1) * TW + (cc + 4);
                     e[(size_t)step * T + tt] = (uint32_t)ti | ((uint32_t)m.m8[x] << 16);
                     sc[(size_t)step * T + tt] = x;
                 }
@@ -417,8 +418,8 @@ extern "C" qvts_status qvts_model_create(const qvts_model_desc *d, qvts_model **
         if ((st = upload(m->d_gc_act, gc_act)) != QVTS_OK) break;
         if ((st = upload(m->d_gc_val, gc_val)) != QVTS_OK) break;
         // band sets: ~16K cells per band for many parents, ~2K for few (more CTAs per parent)
-        if ((st = build_bands(*m, m->band_big, std::max(1, 16384 / W))) != QVTS_OK) break;
-        if ((st = build_bands(*m, m->band_small, std::max(1, 2048 / W))) != QVTS_OK) break;
+        if ((st = build_bands(*m, m->band_big, std::max(1, 8192 / W))) != QVTS_OK) break;
+        if ((st = build_bands(*m, m->band_small, std::max(1, 1024 / W))) != QVTS_OK) break;
         if (cudaEventCreate(&m->ev0) != cudaSuccess || cudaEventCreate(&m->ev1) != cudaSuccess) {
             set_error("cudaEventCreate failed"); st = QVTS_ERR_CUDA; break;
         }

@@ -14,6 +14,8 @@
 #include <cmath>
 #include <cstring>
 
+#include <cooperative_groups.h>
+
 #include "qvts_internal.cuh"
 #include "stencil.cuh"
 
@@ -50,8 +52,10 @@ __device__ __forceinline__ int action_of(int j) {
 //   mass_s = sum b,  HM_s[k] = sum h_k,  and for leaves Zb_s[a'] = sum b Q'(.,a'),
 //   H_s[k][a'] = sum h_k Q'(.,a')   (Q' = Q - qbar, SURVEY c.6 rule 5)
 // plus E[k] = sum occ(y + d_k) b(y) for R(b,a); k_reduce recombines them per action in fp64.
-// One CTA = 2 parents x one row band; its 512 threads are 256 slot-threads x 2 parents, with the
-// two parents in the two half-warps so the static per-slot loads (entry, Q') are shared.
+// One CTA = 2 parents x one row band: 256 threads = 128 slot-threads x 2 parents, the parents in
+// the two half-warps so the static per-slot loads (entry, Q') are shared.  The CTAs of the bands
+// of one parent pair form a thread-block cluster and sum their class totals through DSMEM, so a
+// single fp64 partial per parent reaches HBM.
 struct HistArgs {
     const float *beliefs;
     long long bstride;
@@ -61,7 +65,9 @@ struct HistArgs {
     int nb;
     const uint32_t *entries;
     const float4 *qlist;
-    int H, W, TW, tstride, region_floats;
+    int H, W, TW, tstride, red_off, sums_off;
+    int vec16;            // 16-byte cp.async staging (W % 4 == 0, 16-byte aligned rows)
+    int cluster;          // 1: bands of a pair form one cluster and reduce through DSMEM
     double *part;
     int pstride;
 };
@@ -72,107 +78,97 @@ __host__ __device__ constexpr int hist_cb() {      // class-binned values per th
 }
 template <uint32_t MASK, bool LEAF>
 __host__ __device__ constexpr int hist_nv() { return hist_cb<MASK, LEAF>() + 8; }
+constexpr int kRedChunk = 48;                       // values per reduction round
 
 // direction index di (0..7) <-> stencil id k != 4
 __host__ __device__ constexpr int dir_k(int di) { return di < 4 ? di : di + 1; }
 
 template <uint32_t MASK, bool LEAF>
-__global__ void __launch_bounds__(kPairThreads, 1) k_hist(HistArgs a) {
+__global__ void __launch_bounds__(kPairThreads, 2) k_hist(HistArgs a) {
     constexpr int NA = mask_count(MASK);
     constexpr int NAP = (NA + 3) & ~3;
     constexpr int CB = hist_cb<MASK, LEAF>();
     constexpr int NV = hist_nv<MASK, LEAF>();
+    constexpr int NOUT = 16 * CB + 8;
     constexpr int T = kHistThreads;
+    constexpr int ZB = 9, HQ = 9 + NA;               // offsets in the flat accumulator array
     extern __shared__ float4 smem4[];
     float *smem = reinterpret_cast<float *>(smem4);
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int p = lane >> 4;                       // parent of this half-warp
-    const int st = warp * 16 + (lane & 15);        // slot-thread 0..255
+    const int st = warp * 16 + (lane & 15);        // slot-thread 0..T-1
     const int band = blockIdx.x % a.nb;
     const long long pair = blockIdx.x / a.nb;
-    const long long w = 2 * pair + p;
-    const bool valid = w < a.nwork;
     const BandInfo *bi = a.bands + band;
     const int row0 = bi->row0, nrows = bi->nrows, L = bi->L;
     const long long soff = bi->slot_off;
-    const int TW = a.TW, TH = nrows + 2;
+    const int TH = nrows + 2;
 
-    // stage both parents' bands (+ zero halo); a missing second parent stages zeros
+    // stage both parents' bands (+ zero halo) with cp.async; rows off the map and a missing
+    // second parent are zero-filled by the copy itself (src-size 0)
+    const int TP = a.TW;                              // tile row pitch; column c sits at c + 4
+#pragma unroll
     for (int pp = 0; pp < 2; ++pp) {
         const long long wp = 2 * pair + pp;
         const bool vp = wp < a.nwork;
         const long long vv = vp ? (a.vmap ? (long long)a.vmap[wp] : wp) : 0;
         const float *__restrict__ b = a.beliefs + vv * a.bstride;
         float *tile = smem + pp * a.tstride;
-        for (int tr = warp; tr < TH; tr += kPairThreads / 32) {
-            const int r = row0 - 1 + tr;
-            const bool rok = vp && (r >= 0) && (r < a.H);
-            const float *brow = b + (long long)r * a.W;
-            for (int tc = lane; tc < TW; tc += 32) {
-                const int c = tc - 1;
-                float val = 0.f;
-                if (rok && c >= 0 && c < a.W) val = __ldg(brow + c);
-                tile[tr * TW + tc] = val;
+        const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tile);
+        if (a.vec16) {
+            const int W4 = a.W >> 2;
+            for (int i = t; i < TH * W4; i += kPairThreads) {
+                const int tr = i / W4, c4 = i - tr * W4;
+                const int r = row0 - 1 + tr;
+                const bool ok = vp && r >= 0 && r < a.H;
+                const float *src = ok ? b + (long long)r * a.W + 4 * c4 : b;
+                const uint32_t dst = sbase + 4u * (uint32_t)(tr * TP + 4 + 4 * c4);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0));
+            }
+        } else {
+            for (int i = t; i < TH * a.W; i += kPairThreads) {
+                const int tr = i / a.W, c = i - tr * a.W;
+                const int r = row0 - 1 + tr;
+                const bool ok = vp && r >= 0 && r < a.H;
+                const float *src = ok ? b + (long long)r * a.W + c : b;
+                const uint32_t dst = sbase + 4u * (uint32_t)(tr * TP + 4 + c);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 4 : 0));
             }
         }
+        for (int tr = t; tr < TH; tr += kPairThreads) {      // halo columns
+            tile[tr * TP + 3] = 0.f;
+            tile[tr * TP + 4 + a.W] = 0.f;
+        }
     }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();
     const float *tile = smem + p * a.tstride;
-    int off[9];
-#pragma unroll
-    for (int k = 0; k < 9; ++k) off[k] = st_dr(k) * TW + st_dc(k);
 
-    float mass = 0.f, HM[8], E[8];
-    float Zb[LEAF ? NA : 1], Hq[LEAF ? 8 : 1][LEAF ? NA : 1];
+    float acc[NV];
 #pragma unroll
-    for (int d = 0; d < 8; ++d) { HM[d] = 0.f; E[d] = 0.f; }
-    if (LEAF) {
-#pragma unroll
-        for (int j = 0; j < (LEAF ? NA : 1); ++j) {
-            Zb[j] = 0.f;
-#pragma unroll
-            for (int d = 0; d < (LEAF ? 8 : 1); ++d) Hq[d][j] = 0.f;
-        }
-    }
-    // software pipeline: the next slot's entry and Q' are in flight while this one computes
-    uint32_t e_n = 0;
-    float4 q_n[LEAF ? NAP / 4 : 1];
-    if (L > 0) {
-        const long long slot = soff + st;
-        e_n = __ldg(a.entries + slot);
-        if (LEAF) {
-#pragma unroll
-            for (int h = 0; h < (LEAF ? NAP / 4 : 0); ++h) q_n[h] = __ldg(a.qlist + slot * (NAP / 4) + h);
-        }
-    }
-    for (int i = 0; i < L; ++i) {
-        const uint32_t e = e_n;
+    for (int i = 0; i < NV; ++i) acc[i] = 0.f;
+    // one cell of the slot stream: neighbours at ti +- 1 (immediate) and ti +- TP
+    auto cell = [&](uint32_t e, const float4 (&qv)[LEAF ? NAP / 4 : 1]) {
+        if (e == 0u) return;                          // padding slot
+        const float *c0 = tile + (e & 0xFFFFu);
+        const uint32_t m8 = (e >> 16) & 0xFFu;
+        const float *cu = c0 - TP, *cd = c0 + TP;
+        float nb[9];
+        nb[0] = cu[-1]; nb[1] = cu[0]; nb[2] = cu[1];
+        nb[3] = c0[-1]; nb[4] = c0[0]; nb[5] = c0[1];
+        nb[6] = cd[-1]; nb[7] = cd[0]; nb[8] = cd[1];
         float q[LEAF ? NAP : 1];
         if (LEAF) {
 #pragma unroll
             for (int h = 0; h < (LEAF ? NAP / 4 : 0); ++h) {
-                q[4 * h] = q_n[h].x; q[4 * h + 1] = q_n[h].y; q[4 * h + 2] = q_n[h].z; q[4 * h + 3] = q_n[h].w;
+                q[4 * h] = qv[h].x; q[4 * h + 1] = qv[h].y; q[4 * h + 2] = qv[h].z; q[4 * h + 3] = qv[h].w;
             }
         }
-        if (i + 1 < L) {
-            const long long slot = soff + (long long)(i + 1) * T + st;
-            e_n = __ldg(a.entries + slot);
-            if (LEAF) {
-#pragma unroll
-                for (int h = 0; h < (LEAF ? NAP / 4 : 0); ++h) q_n[h] = __ldg(a.qlist + slot * (NAP / 4) + h);
-            }
-        }
-        if (e == 0u) continue;                       // padding slot
-        const int ti = (int)(e & 0xFFFFu);
-        const uint32_t m8 = (e >> 16) & 0xFFu;
-        float nb[9];
-#pragma unroll
-        for (int k = 0; k < 9; ++k) nb[k] = tile[ti + off[k]];
         const float b0 = nb[4];
-        mass += b0;
+        acc[0] += b0;
         if (LEAF) {
 #pragma unroll
-            for (int j = 0; j < (LEAF ? NA : 1); ++j) Zb[j] = fmaf(b0, q[j], Zb[j]);
+            for (int j = 0; j < (LEAF ? NA : 0); ++j) acc[ZB + j] = fmaf(b0, q[j], acc[ZB + j]);
         }
 #pragma unroll
         for (int d = 0; d < 8; ++d) {
@@ -180,54 +176,102 @@ __global__ void __launch_bounds__(kPairThreads, 1) k_hist(HistArgs a) {
             float h = nb[8 - k];
             if (m8 & (1u << d)) {                    // blocked target: the mass stays at y
                 h += b0;
-                E[d] += b0;
+                acc[CB + d] += b0;
             }
-            HM[d] += h;
+            acc[1 + d] += h;
             if (LEAF) {
 #pragma unroll
-                for (int j = 0; j < (LEAF ? NA : 1); ++j) Hq[d][j] = fmaf(h, q[j], Hq[d][j]);
+                for (int j = 0; j < (LEAF ? NA : 0); ++j) acc[HQ + d * NA + j] = fmaf(h, q[j], acc[HQ + d * NA + j]);
             }
         }
+    };
+    auto fetch = [&](int i, uint32_t &e, float4 (&qv)[LEAF ? NAP / 4 : 1]) {
+        if (i < L) {
+            const long long slot = soff + (long long)i * T + st;
+            e = __ldg(a.entries + slot);
+            if (LEAF) {
+#pragma unroll
+                for (int h = 0; h < (LEAF ? NAP / 4 : 0); ++h) qv[h] = __ldg(a.qlist + slot * (NAP / 4) + h);
+            }
+        } else {
+            e = 0u;
+        }
+    };
+    // software pipeline, ping-pong: slot i+1 is in flight while slot i computes
+    uint32_t eA, eB;
+    float4 qA[LEAF ? NAP / 4 : 1], qB[LEAF ? NAP / 4 : 1];
+    fetch(0, eA, qA);
+    for (int i = 0; i < L; i += 2) {
+        fetch(i + 1, eB, qB);
+        cell(eA, qA);
+        fetch(i + 2, eA, qA);
+        cell(eB, qB);
     }
     __syncthreads();   // tiles are dead; reuse the region for the fixed-order class reduction
     constexpr int RS = T + 1;
-    float *red = smem + p * NV * RS;
-    red[0 * RS + st] = mass;
+    float *red = smem + a.red_off;                   // [2][kRedChunk][RS]
+    double *sums = reinterpret_cast<double *>(smem + a.sums_off);   // [2][NOUT]
 #pragma unroll
-    for (int d = 0; d < 8; ++d) red[(1 + d) * RS + st] = HM[d];
-    if (LEAF) {
+    for (int c0 = 0; c0 < NV; c0 += kRedChunk) {
 #pragma unroll
-        for (int j = 0; j < (LEAF ? NA : 1); ++j) {
-            red[(9 + j) * RS + st] = Zb[j];
-#pragma unroll
-            for (int d = 0; d < (LEAF ? 8 : 1); ++d) red[(9 + NA + d * NA + j) * RS + st] = Hq[d][j];
+        for (int i = 0; i < kRedChunk; ++i)
+            if (c0 + i < NV) red[(p * kRedChunk + i) * RS + st] = acc[c0 + i];
+        __syncthreads();
+        // outputs of this chunk: (class, parent, value) with the class varying slowest, so each
+        // thread's outputs fall in different classes (class 0 holds ~40% of the slot-threads);
+        // every sum runs in a fixed order over 4 interleaved fp64 accumulators.
+        const int nvals = (NV - c0 < kRedChunk) ? NV - c0 : kRedChunk;
+        for (int o = t; o < 17 * 2 * nvals; o += kPairThreads) {
+            const int cls = o / (2 * nvals), r = o % (2 * nvals);
+            const int pp = r / nvals, vi = r % nvals, vv = c0 + vi;
+            const float *rp = red + (pp * kRedChunk + vi) * RS;
+            int t0, t1;
+            if (cls < 16) {
+                if (vv >= CB) continue;
+                t0 = bi->cs[cls];
+                t1 = bi->cs[cls + 1];
+            } else {
+                if (vv < CB) continue;
+                t0 = 0;
+                t1 = T;
+            }
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            int th = t0;
+            for (; th + 3 < t1; th += 4) {
+                s0 += (double)rp[th];
+                s1 += (double)rp[th + 1];
+                s2 += (double)rp[th + 2];
+                s3 += (double)rp[th + 3];
+            }
+            for (; th < t1; ++th) s0 += (double)rp[th];
+            const double sm = (s0 + s1) + (s2 + s3);
+            if (cls < 16) sums[pp * NOUT + cls * CB + vv] = sm;
+            else sums[pp * NOUT + 16 * CB + (vv - CB)] = sm;
+        }
+        __syncthreads();
+    }
+    if (a.cluster) {
+        // sum the class totals of the cluster's bands in fixed rank order through DSMEM
+        namespace cg = cooperative_groups;
+        cg::cluster_group cl = cg::this_cluster();
+        cl.sync();
+        const int nr = a.nb, rank = band;
+        const int per = (2 * NOUT + nr - 1) / nr;
+        for (int o = rank * per + t; o < min(2 * NOUT, (rank + 1) * per); o += kPairThreads) {
+            const int pp = o / NOUT, oo = o % NOUT;
+            const long long wp = 2 * pair + pp;
+            double sm = 0.0;
+            for (int rr = 0; rr < nr; ++rr) sm += cl.map_shared_rank(sums, rr)[o];
+            if (wp < a.nwork) a.part[wp * (long long)a.pstride + oo] = sm;
+        }
+        cl.sync();
+    } else {
+        for (int o = t; o < 2 * NOUT; o += kPairThreads) {
+            const int pp = o / NOUT, oo = o % NOUT;
+            const long long wp = 2 * pair + pp;
+            if (wp < a.nwork) a.part[(wp * a.nb + band) * (long long)a.pstride + oo] = sums[o];
         }
     }
-#pragma unroll
-    for (int d = 0; d < 8; ++d) red[(CB + d) * RS + st] = E[d];
-    __syncthreads();
-    constexpr int NOUT = 16 * CB + 8;
-    for (int o = t; o < 2 * NOUT; o += kPairThreads) {
-        const int pp = o / NOUT, oo = o % NOUT;
-        const long long wp = 2 * pair + pp;
-        if (wp >= a.nwork) continue;
-        const float *rp = smem + pp * NV * RS;
-        int vv, t0, t1;
-        if (oo < 16 * CB) {
-            const int cls = oo / CB;
-            vv = oo % CB;
-            t0 = bi->cs[cls];
-            t1 = bi->cs[cls + 1];
-        } else {
-            vv = CB + (oo - 16 * CB);
-            t0 = 0;
-            t1 = T;
-        }
-        double sum = 0.0;
-        for (int th = t0; th < t1; ++th) sum += (double)rp[vv * RS + th];
-        a.part[(wp * a.nb + band) * (long long)a.pstride + oo] = sum;
-    }
-    (void)valid;
 }
 
 // ---- S2 tail + S3 (+ S5 tail + S6 leaf backup): one warp per parent V-node ---------------------
@@ -663,25 +707,41 @@ static inline unsigned nblk(long long n, int b) { return (unsigned)((n + b - 1) 
 
 template <uint32_t MASK, bool LEAF>
 static qvts_status launch_hist(Model &m, const BandSet &bs, const float *beliefs, long long bstride,
-                               const int32_t *vmap, long long nwork, int pstride, cudaStream_t st) {
+                               const int32_t *vmap, long long nwork, int pstride, cudaStream_t st, int *nb_eff) {
+    constexpr int NOUT = 16 * hist_cb<MASK, LEAF>() + 8;
     HistArgs a;
     a.beliefs = beliefs; a.bstride = bstride; a.vmap = vmap; a.nwork = nwork;
     a.bands = bs.bands.as<BandInfo>(); a.nb = bs.nb;
     a.entries = bs.entries.as<uint32_t>();
     a.qlist = bs.qlist.as<float4>();
-    a.H = m.H; a.W = m.W; a.TW = m.W + 2;
+    a.H = m.H; a.W = m.W; a.TW = bs.tile_pitch;
+    a.vec16 = ((m.W & 3) == 0 && (bstride & 3) == 0 && (reinterpret_cast<uintptr_t>(beliefs) & 15) == 0) ? 1 : 0;
     // second tile offset = 16 banks modulo 32, so the two half-warps never share a bank
     a.tstride = ((bs.tile_floats + 31) & ~31) + 16;
-    const size_t red = (size_t)2 * hist_nv<MASK, LEAF>() * (kHistThreads + 1);
-    a.region_floats = (int)std::max<size_t>((size_t)2 * a.tstride, red);
+    a.red_off = 0;
+    a.sums_off = ((2 * kRedChunk * (kHistThreads + 1)) + 3) & ~3;
+    const int region = std::max(2 * a.tstride, a.sums_off + 2 * 2 * NOUT);
+    a.cluster = bs.nb <= 8 ? 1 : 0;
     a.part = m.part.as<double>(); a.pstride = pstride;
-    const size_t smem = (size_t)a.region_floats * sizeof(float);
+    const size_t smem = (size_t)region * sizeof(float);
     QVTS_CUDA(cudaFuncSetAttribute(k_hist<MASK, LEAF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const long long nblocks = ((nwork + 1) / 2) * bs.nb;
     if (nblocks > 0x7FFFFFFFLL) { set_error("too many hist blocks"); return QVTS_ERR_INVALID_ARG; }
-    QVTS_PROF(LEAF ? 0 : 1, k_hist<MASK, LEAF><<<(unsigned)nblocks, kPairThreads, smem, st>>>(a));
-    QVTS_CUDA(cudaGetLastError());
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)nblocks);
+    cfg.blockDim = dim3(kPairThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = a.cluster ? bs.nb : 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    QVTS_PROF(LEAF ? 0 : 1, QVTS_CUDA(cudaLaunchKernelEx(&cfg, k_hist<MASK, LEAF>, a)));
     (LEAF ? m.pstat.leaf_cells : m.pstat.hist_cells) += nwork * m.n_free;
+    *nb_eff = a.cluster ? 1 : bs.nb;
     return QVTS_OK;
 }
 
@@ -754,13 +814,18 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
             if (leaf) QVTS_TRY(ql.leafV.ensure(sizeof(double) * 16 * std::max(1LL, nq)));
         }
         if (nwork > 0) {
-            const BandSet &bs = (((nwork + 1) / 2) * m.band_big.nb < 2 * 148) ? m.band_small : m.band_big;
+            // band set: a function of (level, roots) only, never of rank-local counts, so the
+            // summation order -- and every value -- is identical for any number of ranks
+            double expect = (double)roots.n;
+            for (int i = 0; i < d; ++i) expect *= 10.0;
+            const BandSet &bs = expect < 1000.0 ? m.band_small : m.band_big;
             const int pstride = pstride_of<MASK>(leaf);
-            QVTS_TRY(m.part.ensure(sizeof(double) * (size_t)nwork * bs.nb * pstride));
-            if (leaf) QVTS_TRY((launch_hist<MASK, true>(m, bs, bel, bstride, vmap, nwork, pstride, st)));
-            else QVTS_TRY((launch_hist<MASK, false>(m, bs, bel, bstride, vmap, nwork, pstride, st)));
+            QVTS_TRY(m.part.ensure(sizeof(double) * (size_t)(nwork + 1) * bs.nb * pstride));
+            int nb_eff = bs.nb;
+            if (leaf) QVTS_TRY((launch_hist<MASK, true>(m, bs, bel, bstride, vmap, nwork, pstride, st, &nb_eff)));
+            else QVTS_TRY((launch_hist<MASK, false>(m, bs, bel, bstride, vmap, nwork, pstride, st, &nb_eff)));
             ReduceArgs r;
-            r.part = m.part.as<double>(); r.pstride = pstride; r.nb = bs.nb; r.nwork = nwork; r.vmap = vmap;
+            r.part = m.part.as<double>(); r.pstride = pstride; r.nb = nb_eff; r.nwork = nwork; r.vmap = vmap;
             r.beliefs = bel; r.bstride = bstride; r.vpath = vl.path.as<uint64_t>(); r.vroot = vl.root.as<int32_t>();
             r.root_step = roots.step_dev; r.root_ep = roots.episode_dev; r.seed = cfg.seed;
             r.level = d; r.n = n; r.O64 = m.d_O64.as<double>();
@@ -942,12 +1007,13 @@ extern "C" qvts_status qvts_belief_update(qvts_model *m, const float *b_dev, int
 #define QVTS_BU_HIST(MASK)                                                                                    \
     {                                                                                                         \
         const int ps = pstride_of<MASK>(false);                                                               \
-        s = m->part.ensure(sizeof(double) * (size_t)bs.nb * ps);                                              \
-        if (s == QVTS_OK) s = launch_hist<MASK, false>(*m, bs, b_dev, m->HW, nullptr, 1, ps, st);             \
+        int nb_eff = bs.nb;                                                                                   \
+        s = m->part.ensure(sizeof(double) * (size_t)2 * bs.nb * ps);                                          \
+        if (s == QVTS_OK) s = launch_hist<MASK, false>(*m, bs, b_dev, m->HW, nullptr, 1, ps, st, &nb_eff);    \
         if (s == QVTS_OK) {                                                                                   \
             ReduceArgs r;                                                                                     \
             std::memset(&r, 0, sizeof(r));                                                                    \
-            r.part = m->part.as<double>(); r.pstride = ps; r.nb = bs.nb; r.nwork = 1;                          \
+            r.part = m->part.as<double>(); r.pstride = ps; r.nb = nb_eff; r.nwork = 1;                         \
             r.beliefs = b_dev; r.bstride = m->HW; r.vpath = m->bu_path.as<uint64_t>();                        \
             r.vroot = m->bu_root.as<int32_t>(); r.root_step = m->bu_key.as<uint32_t>();                       \
             r.root_ep = m->bu_key.as<uint32_t>() + 1; r.n = 1; r.O64 = m->d_O64.as<double>();                 \

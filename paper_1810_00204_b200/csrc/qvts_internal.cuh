@@ -10,8 +10,8 @@
 
 namespace qvts {
 
-constexpr int kHistThreads = 256;   // slot-threads per band list (one class stream per slot-thread)
-constexpr int kPairThreads = 512;   // hist CTA: 2 parents x 256 slot-threads
+constexpr int kHistThreads = 128;   // slot-threads per band list (one class stream per slot-thread)
+constexpr int kPairThreads = 256;   // hist CTA: 2 parents x 128 slot-threads
 constexpr int kMaxLevels = 9;       // depth <= 8
 
 void set_error(const std::string &msg);
@@ -51,7 +51,7 @@ struct BandInfo {
 };
 
 struct BandSet {
-    int nb = 0, rows = 0, tile_floats = 0;
+    int nb = 0, rows = 0, tile_floats = 0, tile_pitch = 0;   // tile column c at c + 4
     long long total_slots = 0;
     std::vector<BandInfo> h_bands;
     std::vector<int32_t> h_slot_cell;
