@@ -183,11 +183,16 @@ QVTS_API qvts_status qvts_trace_belief(const qvts_model *model, int32_t level, i
  * Environment draws use Philox ctr = (0, 0, 0, step), key = (seed, episode): word 0 motion,
  * word 1 observation, word 2 the initial state (Appendix A.2).  Episodes with
  * e % nranks != rank are skipped when comm != NULL and their records reduced across ranks. */
-typedef enum { QVTS_PLANNER_QVTS = 0, QVTS_PLANNER_MDP = 1 } qvts_planner;
+/* Planners: QVTS; MDP = one Q table lookup at the belief mode; A* = unit-cost A* (reading R29)
+ * from the belief mode, run on the host (the paper's two comparators). */
+typedef enum { QVTS_PLANNER_QVTS = 0, QVTS_PLANNER_MDP = 1, QVTS_PLANNER_ASTAR = 2 } qvts_planner;
 typedef struct {
     int32_t n_episodes, max_steps, stop_patience, planner, depth, n_samples;
     uint32_t seed;
     const float *b0_dev;          /* device fp32 [H*W]; NULL = uniform over free cells         */
+    /* optional host logs [n_episodes][max_steps] (-1 after the episode ended): executed action
+     * (stencil id), observation z, true state after the step.  NULL = not recorded. */
+    int32_t *log_actions, *log_obs, *log_states;
 } qvts_episode_cfg;
 typedef struct {
     int32_t outcome;              /* 0 success, 1 wrong stop, 2 step cap, 3 zero likelihood    */

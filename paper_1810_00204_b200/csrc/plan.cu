@@ -18,20 +18,9 @@
 
 #include "qvts_internal.cuh"
 #include "stencil.cuh"
+#include "philox.cuh"
 
 namespace qvts {
-
-// ---- Philox4x32-10 (Salmon et al. 2011) ---------------------------------
-__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
-#pragma unroll
-    for (int i = 0; i < 10; ++i) {
-        if (i) { k.x += 0x9E3779B9u; k.y += 0xBB67AE85u; }
-        const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
-        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
-        c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
-    }
-    return c;
-}
 
 template <uint32_t MASK>
 __device__ __forceinline__ int action_of(int j) {
@@ -390,7 +379,7 @@ __global__ void __launch_bounds__(kReduceWarps * 32) k_reduce(ReduceArgs a) {
             if (jj < a.n) {
                 const uint4 r = philox4x32_10(make_uint4((uint32_t)jj, (uint32_t)qpath, (uint32_t)(qpath >> 32), step),
                                               make_uint2(a.seed, ep));
-                const double u = ((double)(r.x >> 8) + 0.5) * (1.0 / 16777216.0);
+                const double u = philox_uniform(r.x);
                 const double tt = u * C[15];
                 z = 0;
                 double gap = INFINITY;
@@ -534,6 +523,7 @@ struct CorrectArgs {
     int H, W, G, ntiles;
     float p_int, p_stay, p_lat;
     long long qsel;   // >= 0: only this Q-node (belief_update)
+    const int32_t *sel_q, *sel_z, *sel_out;   // optional per-block-group selection (episodes)
 };
 
 // bbar_a for 4 consecutive cells (r, c0..c0+3): bbar = p_stay b + p_int h_a + p_lat (h_l1 + h_l2),
@@ -571,15 +561,16 @@ __device__ __forceinline__ void correct_predict(const CorrectArgs &a, int r, int
 template <uint32_t MASK>
 __global__ void __launch_bounds__(256) k_correct(CorrectArgs a) {
     constexpr int NA = mask_count(MASK);
-    const long long q = a.qsel >= 0 ? a.qsel : (long long)(blockIdx.x / a.ntiles);
+    const long long grp = blockIdx.x / a.ntiles;
+    const long long q = a.sel_q ? (long long)a.sel_q[grp] : (a.qsel >= 0 ? a.qsel : grp);
     const int tile = blockIdx.x % a.ntiles;
     const long long w = q / NA;
     const int j = (int)(q % NA);
     const int k = action_of<MASK>(j);
     const long long v = a.vmap ? (long long)a.vmap[w] : w;
-    const unsigned um = a.umask[q];
+    const unsigned um = a.sel_q ? (1u << a.sel_z[grp]) : a.umask[q];
     const int U = __popc(um);
-    const long long base = a.qsel >= 0 ? 0 : a.off[q];
+    const long long base = a.sel_q ? (long long)a.sel_out[grp] : (a.qsel >= 0 ? 0 : a.off[q]);
     __shared__ float s_w[16][16];   // [rank u][signature s] = O[s][z_u] / P(z_u)
     {
         const int t = threadIdx.x;
@@ -791,16 +782,22 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
         const long long bstride = d == 0 ? roots.stride : m.HWp;
         // sharding: first level d >= 1 with >= shard_min V-nodes
         ql.mapped = false;
+        ql.vmap_ptr = nullptr;
         long long nwork = vl.n;
-        if (G > 1 && shard_level < 0 && d >= 1 && vl.n >= shard_min) {
+        if (d == 0 && roots.active) {
+            nwork = roots.n_active;
+            ql.mapped = true;
+            ql.vmap_ptr = roots.active;
+        } else if (G > 1 && shard_level < 0 && d >= 1 && vl.n >= shard_min) {
             shard_level = d;
             nwork = vl.n > rank ? (vl.n - rank + G - 1) / G : 0;
             QVTS_TRY(ql.vmap.ensure(sizeof(int32_t) * std::max(1LL, nwork)));
             if (nwork) QVTS_PROF(7, k_iota_stride<<<nblk(nwork, 256), 256, 0, st>>>(ql.vmap.as<int32_t>(), nwork, rank, G));
             ql.mapped = true;
+            ql.vmap_ptr = ql.vmap.as<int32_t>();
         }
         ql.nwork = nwork;
-        const int32_t *vmap = ql.mapped ? ql.vmap.as<int32_t>() : nullptr;
+        const int32_t *vmap = ql.vmap_ptr;
         const long long nq = nwork * NA;
         QVTS_TRY(ql.R.ensure(sizeof(double) * std::max(1LL, nq)));
         QVTS_TRY(ql.P.ensure(sizeof(double) * 16 * std::max(1LL, nq)));
@@ -816,7 +813,7 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
         if (nwork > 0) {
             // band set: a function of (level, roots) only, never of rank-local counts, so the
             // summation order -- and every value -- is identical for any number of ranks
-            double expect = (double)roots.n;
+            double expect = 1.0;    // per root: the choice must not depend on batch or wave size either
             for (int i = 0; i < d; ++i) expect *= 10.0;
             const BandSet &bs = expect < 1000.0 ? m.band_small : m.band_big;
             const int pstride = pstride_of<MASK>(leaf);
@@ -874,6 +871,7 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
             c.H = m.H; c.W = m.W; c.G = (m.W + 3) / 4;
             c.ntiles = (int)(((long long)m.H * c.G + 255) / 256);
             c.p_int = (float)m.p_int; c.p_stay = (float)m.p_stay; c.p_lat = (float)m.p_lat; c.qsel = -1;
+            c.sel_q = c.sel_z = c.sel_out = nullptr;
             const long long nblocks = nq * c.ntiles;
             if (nblocks > 0x7FFFFFFFLL) { set_error("too many correct blocks"); return QVTS_ERR_INVALID_ARG; }
             QVTS_PROF(5, k_correct<MASK><<<(unsigned)nblocks, 256, 0, st>>>(c));
@@ -885,7 +883,7 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
     for (int d = D - 1; d >= 0; --d) {
         QLevel &ql = m.ql[d];
         VLevel &vl = m.vl[d];
-        const int32_t *vmap = ql.mapped ? ql.vmap.as<int32_t>() : nullptr;
+        const int32_t *vmap = ql.vmap_ptr;
         if (d == shard_level) QVTS_CUDA(cudaMemsetAsync(vl.V.p, 0, sizeof(double) * std::max(1LL, vl.n), st));
         if (ql.nwork > 0) {
             if (d == D - 1) {
@@ -918,6 +916,79 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
     m.last_n = n;
     m.last_trace = trace;
     return QVTS_OK;
+}
+
+template <uint32_t MASK>
+static qvts_status root_marginals_t(Model &m, const RootBatch &roots, cudaStream_t st) {
+    constexpr int NA = mask_count(MASK);
+    VLevel &v0 = m.vl[0];
+    QLevel &ql = m.ql[0];
+    v0.n = roots.n;
+    QVTS_TRY(v0.path.ensure(sizeof(uint64_t) * roots.n));
+    QVTS_TRY(v0.root.ensure(sizeof(int32_t) * roots.n));
+    QVTS_PROF(7, k_init_roots<<<nblk(roots.n, 256), 256, 0, st>>>(roots.n, v0.path.as<uint64_t>(), v0.root.as<int32_t>()));
+    const long long nwork = roots.active ? roots.n_active : roots.n;
+    ql.nwork = nwork;
+    ql.mapped = roots.active != nullptr;
+    ql.vmap_ptr = roots.active;
+    if (nwork == 0) return QVTS_OK;
+    const long long nq = nwork * NA;
+    QVTS_TRY(ql.R.ensure(sizeof(double) * nq));
+    QVTS_TRY(ql.P.ensure(sizeof(double) * 16 * nq));
+    QVTS_TRY(ql.cnt.ensure(sizeof(uint16_t) * 16 * nq));
+    QVTS_TRY(ql.umask.ensure(sizeof(uint16_t) * nq));
+    QVTS_TRY(ql.U.ensure(sizeof(int32_t) * nq));
+    const BandSet &bs = m.band_small;     // the level-0 band set of plan_levels (same sums)
+    const int pstride = pstride_of<MASK>(false);
+    QVTS_TRY(m.part.ensure(sizeof(double) * (size_t)(nwork + 1) * bs.nb * pstride));
+    int nb_eff = bs.nb;
+    QVTS_TRY((launch_hist<MASK, false>(m, bs, roots.beliefs, roots.stride, roots.active, nwork, pstride, st, &nb_eff)));
+    ReduceArgs r;
+    std::memset(&r, 0, sizeof(r));
+    r.part = m.part.as<double>(); r.pstride = pstride; r.nb = nb_eff; r.nwork = nwork; r.vmap = roots.active;
+    r.beliefs = roots.beliefs; r.bstride = roots.stride; r.vpath = v0.path.as<uint64_t>(); r.vroot = v0.root.as<int32_t>();
+    r.root_step = roots.step_dev; r.root_ep = roots.episode_dev; r.n = 1; r.O64 = m.d_O64.as<double>();
+    r.ngc = m.ngc; r.gc_cell = m.d_gc_cell.as<int32_t>(); r.gc_act = m.d_gc_act.as<int32_t>();
+    r.gc_val = m.d_gc_val.as<double>(); r.goal = m.goal; r.p_stay = m.p_stay; r.p_int = m.p_int; r.p_lat = m.p_lat;
+    r.gamma = m.gamma; r.R = ql.R.as<double>(); r.P = ql.P.as<double>(); r.cnt = ql.cnt.as<uint16_t>();
+    r.umask = ql.umask.as<uint16_t>(); r.U = ql.U.as<int32_t>();
+    return launch_reduce<MASK, false>(m, r, st);
+}
+
+template <uint32_t MASK>
+static qvts_status correct_selected_t(Model &m, const RootBatch &roots, const int32_t *sel_q, const int32_t *sel_z,
+                                      const int32_t *sel_out, long long n, float *out, long long ostride,
+                                      cudaStream_t st) {
+    if (n == 0) return QVTS_OK;
+    CorrectArgs c;
+    std::memset(&c, 0, sizeof(c));
+    c.beliefs = roots.beliefs; c.bstride = roots.stride; c.vmap = m.ql[0].vmap_ptr;
+    c.m8 = m.d_m8.as<uint8_t>(); c.cell = m.d_cell.as<uint8_t>(); c.O64 = m.d_O64.as<double>();
+    c.P = m.ql[0].P.as<double>(); c.cnt = m.ql[0].cnt.as<uint16_t>();
+    c.child = out; c.cstride = ostride; c.H = m.H; c.W = m.W; c.G = (m.W + 3) / 4;
+    c.ntiles = (int)(((long long)m.H * c.G + 255) / 256);
+    c.p_int = (float)m.p_int; c.p_stay = (float)m.p_stay; c.p_lat = (float)m.p_lat; c.qsel = -1;
+    c.sel_q = sel_q; c.sel_z = sel_z; c.sel_out = sel_out;
+    QVTS_PROF(5, k_correct<MASK><<<(unsigned)(n * c.ntiles), 256, 0, st>>>(c));
+    QVTS_CUDA(cudaGetLastError());
+    return QVTS_OK;
+}
+
+qvts_status root_marginals(Model &m, const RootBatch &roots, cudaStream_t st) {
+    qvts_status s = QVTS_ERR_INVALID_ARG;
+#define QVTS_RM(MASK) s = root_marginals_t<MASK>(m, roots, st)
+    QVTS_DISPATCH_MASK(m.mask, QVTS_RM);
+#undef QVTS_RM
+    return s;
+}
+
+qvts_status correct_selected(Model &m, const RootBatch &roots, const int32_t *sel_q, const int32_t *sel_z,
+                             const int32_t *sel_out, long long n, float *out, long long ostride, cudaStream_t st) {
+    qvts_status s = QVTS_ERR_INVALID_ARG;
+#define QVTS_CS(MASK) s = correct_selected_t<MASK>(m, roots, sel_q, sel_z, sel_out, n, out, ostride, st)
+    QVTS_DISPATCH_MASK(m.mask, QVTS_CS);
+#undef QVTS_CS
+    return s;
 }
 
 qvts_status plan_levels(Model &m, const RootBatch &roots, const qvts_plan_cfg &cfg, const qvts_comm *comm,
@@ -1046,6 +1117,7 @@ extern "C" qvts_status qvts_belief_update(qvts_model *m, const float *b_dev, int
     c.child = out_dev; c.cstride = m->HW; c.H = m->H; c.W = m->W; c.G = (m->W + 3) / 4;
     c.ntiles = (int)(((long long)m->H * c.G + 255) / 256);
     c.p_int = (float)m->p_int; c.p_stay = (float)m->p_stay; c.p_lat = (float)m->p_lat; c.qsel = j;
+    c.sel_q = c.sel_z = c.sel_out = nullptr;
 #define QVTS_BU_CORR(MASK) k_correct<MASK><<<c.ntiles, 256, 0, st>>>(c)
     QVTS_DISPATCH_MASK(m->mask, QVTS_BU_CORR);
 #undef QVTS_BU_CORR
@@ -1080,7 +1152,10 @@ extern "C" qvts_status qvts_trace_qnodes(const qvts_model *m, int32_t level, uin
         std::vector<uint64_t> vp(m->vl[level].n);
         std::vector<int32_t> vmap;
         QVTS_TRY(d2h(vp.data(), m->vl[level].path, vp.size()));
-        if (ql.mapped) { vmap.resize(ql.nwork); QVTS_TRY(d2h(vmap.data(), ql.vmap, vmap.size())); }
+        if (ql.mapped) {
+            vmap.resize(ql.nwork);
+            if (!vmap.empty()) QVTS_CUDA(cudaMemcpy(vmap.data(), ql.vmap_ptr, sizeof(int32_t) * vmap.size(), cudaMemcpyDeviceToHost));
+        }
         for (long long q = 0; q < nq; ++q) {
             const long long w = q / m->NA;
             const long long v = ql.mapped ? vmap[w] : w;

@@ -67,6 +67,7 @@ struct QLevel {
     long long nwork = 0;              // parents expanded at this level (owned subset when sharded)
     DevBuf vmap;                      // work index -> V-node index (only when sharded)
     bool mapped = false;
+    const int32_t *vmap_ptr = nullptr;   // the map in use (vmap, or the caller's active-root list)
     DevBuf R, P, cnt, umask, U, off, Q, zdraw, leafV;
 };
 
@@ -124,9 +125,16 @@ struct RootBatch {
     long long n;
     const uint32_t *step_dev;   // [n] per-root step keys (device)
     const uint32_t *episode_dev;// [n] per-root episode keys (device)
+    const int32_t *active = nullptr;   // optional: expand only these roots (device [n_active])
+    long long n_active = 0;
 };
 qvts_status plan_levels(Model &m, const RootBatch &roots, const qvts_plan_cfg &cfg, const qvts_comm *comm,
                         cudaStream_t st, long long *nv_out /*[depth+1]*/);
+// P(z|b,a) and R(b,a) of the (active) roots only, into ql[0] (S1+S2 without sampling)
+qvts_status root_marginals(Model &m, const RootBatch &roots, cudaStream_t st);
+// Bayes correction of selected (Q-node, z) pairs of level 0 into out[sel_out[g]*ostride]
+qvts_status correct_selected(Model &m, const RootBatch &roots, const int32_t *sel_q, const int32_t *sel_z,
+                             const int32_t *sel_out, long long n, float *out, long long ostride, cudaStream_t st);
 
 }  // namespace qvts
 

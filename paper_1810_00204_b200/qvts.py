@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(_HERE, "libqvts.so")
 QVTS_OK = 0
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "INVALID_MODEL", 3: "STATE", 4: "NOT_CONVERGED",
           5: "ZERO_LIKELIHOOD", 6: "OUT_OF_MEMORY", 7: "CUDA", 8: "COMM"}
-QVTS_PLANNER_QVTS, QVTS_PLANNER_MDP = 0, 1
+QVTS_PLANNER_QVTS, QVTS_PLANNER_MDP, QVTS_PLANNER_ASTAR = 0, 1, 2
 
 # Symbols include/qvts.h declares (checked by tests/test_abi.py).
 EXPORTS = [
@@ -70,7 +70,8 @@ class qvts_comm(C.Structure):
 class qvts_episode_cfg(C.Structure):
     _fields_ = [("n_episodes", C.c_int32), ("max_steps", C.c_int32), ("stop_patience", C.c_int32),
                 ("planner", C.c_int32), ("depth", C.c_int32), ("n_samples", C.c_int32), ("seed", C.c_uint32),
-                ("b0_dev", C.c_void_p)]
+                ("b0_dev", C.c_void_p), ("log_actions", C.c_void_p), ("log_obs", C.c_void_p),
+                ("log_states", C.c_void_p)]
 
 
 class qvts_episode_record(C.Structure):
@@ -253,13 +254,22 @@ def qvts_get_profile(h) -> dict:
 
 
 def qvts_run_episodes(h, n_episodes, max_steps=500, stop_patience=3, planner=QVTS_PLANNER_QVTS, depth=3,
-                      n_samples=8, seed=1, b0_dev=None, comm=None, stream=None):
+                      n_samples=8, seed=1, b0_dev=None, comm=None, stream=None, logs=False):
+    """Returns (records as a dict of numpy arrays, logs dict or None)."""
+    la = lz = lx = None
+    if logs:
+        la = np.full((n_episodes, max_steps), -1, np.int32)
+        lz = np.full((n_episodes, max_steps), -1, np.int32)
+        lx = np.full((n_episodes, max_steps), -1, np.int32)
     cfg = qvts_episode_cfg(int(n_episodes), int(max_steps), int(stop_patience), int(planner), int(depth),
-                           int(n_samples), int(seed), _ptr(b0_dev) or None)
-    recs = (qvts_episode_record * n_episodes)()
+                           int(n_samples), int(seed), _ptr(b0_dev) or None, _ptr(la) or None, _ptr(lz) or None,
+                           _ptr(lx) or None)
+    recs = (qvts_episode_record * max(1, n_episodes))()
     _check(lib().qvts_run_episodes(h, C.byref(cfg), C.byref(comm) if comm is not None else None, recs,
                                    _stream(stream)), "qvts_run_episodes")
-    return recs
+    out = {k: np.array([getattr(recs[i], k) for i in range(n_episodes)])
+           for k in ("outcome", "steps", "collisions", "x0", "x_final", "disc_return")}
+    return out, (dict(actions=la, obs=lz, states=lx) if logs else None)
 
 
 # ---- multi-rank plumbing: the all-reduce callback runs torch.distributed (NCCL) ----------------
@@ -339,6 +349,9 @@ class Model:
 
     def plan_step(self, root_dev, depth, n_samples, **kw):
         return qvts_plan_step(self.h, root_dev, depth, n_samples, **kw)
+
+    def run_episodes(self, n_episodes, **kw):
+        return qvts_run_episodes(self.h, n_episodes, **kw)
 
     def trace(self, with_draws=False, n_samples=0, beliefs=False):
         """Pull the whole tree of the last plan step to the host (small configs).  with_draws and
