@@ -15,8 +15,15 @@ void set_error(const std::string &msg) { g_last_error = msg; }
 qvts_status DevBuf::ensure(size_t bytes) {
     if (bytes <= cap && p) return QVTS_OK;
     release();
-    size_t want = std::max<size_t>(bytes, 256);
+    // headroom: tree levels vary from step to step; regrowing (cudaFree + cudaMalloc of tens of
+    // GB) would stall the device every time a step's tree is a little larger
+    size_t want = std::max<size_t>(bytes + bytes / 4, 256);
     cudaError_t e = cudaMalloc(&p, want);
+    if (e != cudaSuccess && want > bytes) {      // no room for headroom: exact size
+        cudaGetLastError();
+        want = std::max<size_t>(bytes, 256);
+        e = cudaMalloc(&p, want);
+    }
     if (e != cudaSuccess) {
         p = nullptr;
         cap = 0;

@@ -71,6 +71,13 @@ constexpr int kRedChunk = 48;                       // values per reduction roun
 
 // direction index di (0..7) <-> stencil id k != 4
 __host__ __device__ constexpr int dir_k(int di) { return di < 4 ? di : di + 1; }
+// orthogonal moves: their target's occupancy is the wall-signature bit (PAPER.md:336 sensors)
+__host__ __device__ constexpr bool is_orth(int k) { return k == 1 || k == 3 || k == 5 || k == 7; }
+__host__ __device__ constexpr int orth_bit(int k) { return k == 1 ? 0 : k == 3 ? 1 : k == 5 ? 2 : 3; }
+// occupancy of y + d_k for every cell of signature class s, or 0 when it is not class-constant
+__device__ __forceinline__ double class_blocked(int k, int s) {
+    return (k != 4 && is_orth(k) && ((s >> orth_bit(k)) & 1)) ? 1.0 : 0.0;
+}
 
 template <uint32_t MASK, bool LEAF>
 __global__ void __launch_bounds__(kPairThreads, 2) k_hist(HistArgs a) {
@@ -163,7 +170,9 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_hist(HistArgs a) {
         for (int d = 0; d < 8; ++d) {
             const int k = dir_k(d);
             float h = nb[8 - k];
-            if (m8 & (1u << d)) {                    // blocked target: the mass stays at y
+            // blocked target: the mass stays at y.  For the 4 orthogonal directions occupancy is a
+            // bit of the cell's wall signature, i.e. constant over the class: k_reduce adds it.
+            if (!is_orth(k) && (m8 & (1u << d))) {
                 h += b0;
                 acc[CB + d] += b0;
             }
@@ -315,6 +324,7 @@ __global__ void __launch_bounds__(kReduceWarps * 32) k_reduce(ReduceArgs a) {
     double *sp = rsm + warp * per_warp;
     double *sS = sp + a.pstride;            // [16][NA] S of the current action
     double *sR = sS + 16 * NA;              // [16][NA] ratios of the current action
+    double *sE = sp + 16 * CB;              // E totals, completed below for the orthogonal directions
     const double *pp = a.part + w * a.nb * (long long)a.pstride;
     for (int i = lane; i < a.pstride; i += 32) {
         double acc = 0.0;
@@ -328,6 +338,17 @@ __global__ void __launch_bounds__(kReduceWarps * 32) k_reduce(ReduceArgs a) {
     double mass = 0.0;
 #pragma unroll
     for (int s = 0; s < 16; ++s) mass += __shfl_sync(0xffffffffu, mass_s, s);
+    // blocked-mass totals E[d] = sum_y occ(y + d) b(y): the orthogonal directions come from the
+    // class masses (their occupancy is a signature bit), fixed class order
+    if (lane < 8) {
+        const int kd = lane < 4 ? lane : lane + 1;
+        if (is_orth(kd)) {
+            double e = 0.0;
+            for (int s2 = 0; s2 < 16; ++s2) e += class_blocked(kd, s2) * sp[s2 * CB];
+            sE[lane] = e;
+        }
+    }
+    __syncwarp();
     const uint64_t vpath = a.vpath[v];
     const int root = a.vroot[v];
     const uint32_t step = a.root_step[root], ep = a.root_ep[root];
@@ -338,10 +359,14 @@ __global__ void __launch_bounds__(kReduceWarps * 32) k_reduce(ReduceArgs a) {
         const int k = action_of<MASK>(j);
         const int da = k == 4 ? 0 : nbit(k), d1 = k == 4 ? 0 : nbit(lat1(k)), d2 = k == 4 ? 0 : nbit(lat2(k));
         // M[s]: bbar_a summed over signature class s
+        const int k1 = k == 4 ? 4 : lat1(k), k2 = k == 4 ? 4 : lat2(k);
         double Ms = 0.0;
         if (lane < 16) {
             const double *c = sp + lane * CB;
-            Ms = (k == 4) ? c[0] : a.p_stay * c[0] + a.p_int * c[1 + da] + a.p_lat * (c[1 + d1] + c[1 + d2]);
+            const double hma = c[1 + da] + class_blocked(k, lane) * c[0];
+            const double hm1 = c[1 + d1] + class_blocked(k1, lane) * c[0];
+            const double hm2 = c[1 + d2] + class_blocked(k2, lane) * c[0];
+            Ms = (k == 4) ? c[0] : a.p_stay * c[0] + a.p_int * hma + a.p_lat * (hm1 + hm2);
         }
         // R(b,a) = (p_stay - 1) sum b - sum c_a b + goal terms, sum c_a b = p_stay mass + p_int E_a + p_lat (E_l1 + E_l2)
         double R = 0.0;
@@ -349,8 +374,7 @@ __global__ void __launch_bounds__(kReduceWarps * 32) k_reduce(ReduceArgs a) {
             if (k == 4) {
                 R = -2.0 * mass + 2.0 * (double)bp[a.goal];
             } else {
-                const double *E = sp + 16 * CB;
-                const double Rp = a.p_stay * mass + a.p_int * E[da] + a.p_lat * (E[d1] + E[d2]);
+                const double Rp = a.p_stay * mass + a.p_int * sE[da] + a.p_lat * (sE[d1] + sE[d2]);
                 R = (a.p_stay - 1.0) * mass - Rp;
                 for (int g = 0; g < a.ngc; ++g)
                     if (a.gc_act[g] == j) R += a.gc_val[g] * (double)bp[a.gc_cell[g]];
@@ -414,12 +438,14 @@ __global__ void __launch_bounds__(kReduceWarps * 32) k_reduce(ReduceArgs a) {
             // S[s][a'] of this action from the linear fields, staged for the (z, a') dot products
             if (lane < 16) {
                 const double *c = sp + lane * CB;
+                const double oa = class_blocked(k, lane), o1 = class_blocked(k1, lane), o2 = class_blocked(k2, lane);
 #pragma unroll
                 for (int j2 = 0; j2 < NA; ++j2) {
                     const double zb = c[9 + j2];
-                    sS[lane * NA + j2] = (k == 4) ? zb
-                                                  : a.p_stay * zb + a.p_int * c[9 + NA + da * NA + j2] +
-                                                        a.p_lat * (c[9 + NA + d1 * NA + j2] + c[9 + NA + d2 * NA + j2]);
+                    const double ha = c[9 + NA + da * NA + j2] + oa * zb;
+                    const double h1 = c[9 + NA + d1 * NA + j2] + o1 * zb;
+                    const double h2 = c[9 + NA + d2 * NA + j2] + o2 * zb;
+                    sS[lane * NA + j2] = (k == 4) ? zb : a.p_stay * zb + a.p_int * ha + a.p_lat * (h1 + h2);
                 }
             }
             __syncwarp();

@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqvts.so")
+LIB_PATH = os.environ.get("QVTS_LIB") or os.path.join(_HERE, "libqvts.so")   # QVTS_LIB: A/B builds
 
 QVTS_OK = 0
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "INVALID_MODEL", 3: "STATE", 4: "NOT_CONVERGED",
