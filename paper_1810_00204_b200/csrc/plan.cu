@@ -546,7 +546,7 @@ struct CorrectArgs {
     long long cstride;
     uint64_t *cpath;
     int32_t *cparent, *cz, *cf, *croot;
-    int H, W, G, ntiles;
+    int H, W, G, ntiles, rows_cta;
     float p_int, p_stay, p_lat;
     long long qsel;   // >= 0: only this Q-node (belief_update)
     const int32_t *sel_q, *sel_z, *sel_out;   // optional per-block-group selection (episodes)
@@ -617,50 +617,61 @@ __global__ void __launch_bounds__(256) k_correct(CorrectArgs a) {
         }
     }
     __syncthreads();
-    const int idx = tile * 256 + threadIdx.x;
-    const int r = idx / a.G, g = idx - (idx / a.G) * a.G;
-    if (r >= a.H) return;
-    const int W = a.W, c0 = 4 * g;
+    // this CTA covers rows [tile * rows_cta, +rows_cta): 4 consecutive cells per thread, rows_it
+    // rows per pass
+    const int W = a.W;
     const float *__restrict__ b = a.beliefs + v * a.bstride;
-    // rows r-1..r+1, columns c0-1..c0+4 (zero off-map)
-    float nbh[3][6];
+    const bool vec = ((W & 3) == 0) && ((a.cstride & 3) == 0) && ((a.bstride & 3) == 0);
+    const int r_end = min(a.H, (tile + 1) * a.rows_cta);
+    for (int idx = threadIdx.x; idx < a.rows_cta * a.G; idx += 256) {
+        const int r = tile * a.rows_cta + idx / a.G, c0 = 4 * (idx % a.G);
+        if (r >= r_end) break;
+        // rows r-1..r+1, columns c0-1..c0+4 (zero off-map)
+        float nbh[3][6];
 #pragma unroll
-    for (int dr = 0; dr < 3; ++dr) {
-        const int rr = r + dr - 1;
-        const bool rok = rr >= 0 && rr < a.H;
-        const float *row = b + (long long)rr * W;
+        for (int dr = 0; dr < 3; ++dr) {
+            const int rr = r + dr - 1;
+            const bool rok = rr >= 0 && rr < a.H;
+            const float *row = b + (long long)rr * W;
+            if (vec) {
+                const float4 m4 = rok ? __ldg(reinterpret_cast<const float4 *>(row + c0)) : make_float4(0.f, 0.f, 0.f, 0.f);
+                nbh[dr][0] = (rok && c0 > 0) ? __ldg(row + c0 - 1) : 0.f;
+                nbh[dr][1] = m4.x; nbh[dr][2] = m4.y; nbh[dr][3] = m4.z; nbh[dr][4] = m4.w;
+                nbh[dr][5] = (rok && c0 + 4 < W) ? __ldg(row + c0 + 4) : 0.f;
+            } else {
 #pragma unroll
-        for (int i = 0; i < 6; ++i) {
-            const int cc = c0 - 1 + i;
-            nbh[dr][i] = (rok && cc >= 0 && cc < W) ? __ldg(row + cc) : 0.f;
+                for (int i = 0; i < 6; ++i) {
+                    const int cc = c0 - 1 + i;
+                    nbh[dr][i] = (rok && cc >= 0 && cc < W) ? __ldg(row + cc) : 0.f;
+                }
+            }
         }
-    }
-    float bb[4];
-    int sg[4];
-    switch (k) {   // block-uniform: compile-time tap geometry per action
-        case 0: correct_predict<0>(a, r, c0, nbh, bb, sg); break;
-        case 1: correct_predict<1>(a, r, c0, nbh, bb, sg); break;
-        case 2: correct_predict<2>(a, r, c0, nbh, bb, sg); break;
-        case 3: correct_predict<3>(a, r, c0, nbh, bb, sg); break;
-        case 4: correct_predict<4>(a, r, c0, nbh, bb, sg); break;
-        case 5: correct_predict<5>(a, r, c0, nbh, bb, sg); break;
-        case 6: correct_predict<6>(a, r, c0, nbh, bb, sg); break;
-        case 7: correct_predict<7>(a, r, c0, nbh, bb, sg); break;
-        default: correct_predict<8>(a, r, c0, nbh, bb, sg); break;
-    }
-    const long long x0 = (long long)r * W + c0;
-    const bool vec = ((W & 3) == 0) && ((a.cstride & 3) == 0);
-    for (int u = 0; u < U; ++u) {
-        float o[4];
+        float bb[4];
+        int sg[4];
+        switch (k) {   // block-uniform: compile-time tap geometry per action
+            case 0: correct_predict<0>(a, r, c0, nbh, bb, sg); break;
+            case 1: correct_predict<1>(a, r, c0, nbh, bb, sg); break;
+            case 2: correct_predict<2>(a, r, c0, nbh, bb, sg); break;
+            case 3: correct_predict<3>(a, r, c0, nbh, bb, sg); break;
+            case 4: correct_predict<4>(a, r, c0, nbh, bb, sg); break;
+            case 5: correct_predict<5>(a, r, c0, nbh, bb, sg); break;
+            case 6: correct_predict<6>(a, r, c0, nbh, bb, sg); break;
+            case 7: correct_predict<7>(a, r, c0, nbh, bb, sg); break;
+            default: correct_predict<8>(a, r, c0, nbh, bb, sg); break;
+        }
+        const long long x0 = (long long)r * W + c0;
+        for (int u = 0; u < U; ++u) {
+            float o[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) o[i] = s_w[u][sg[i]] * bb[i];
-        float *dst = a.child + (base + u) * a.cstride + x0;
-        if (vec) {
-            *reinterpret_cast<float4 *>(dst) = make_float4(o[0], o[1], o[2], o[3]);
-        } else {
+            for (int i = 0; i < 4; ++i) o[i] = s_w[u][sg[i]] * bb[i];
+            float *dst = a.child + (base + u) * a.cstride + x0;
+            if (vec) {
+                __stcs(reinterpret_cast<float4 *>(dst), make_float4(o[0], o[1], o[2], o[3]));   // streaming
+            } else {
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-                if (c0 + i < W) dst[i] = o[i];
+                for (int i = 0; i < 4; ++i)
+                    if (c0 + i < W) dst[i] = o[i];
+            }
         }
     }
 }
@@ -712,6 +723,10 @@ __global__ void k_iota_stride(int32_t *out, long long n, int r, int G) {
 
 // ---- host orchestration -------------------------------------------------------------------------
 static inline unsigned nblk(long long n, int b) { return (unsigned)((n + b - 1) / b); }
+// k_correct: a CTA covers ~1024 groups of 4 cells (4 passes of its 256 threads)
+static inline int correct_rows_per_cta(int H, int G) {
+    return std::min(H, std::max(1, 1024 / std::max(1, G)));
+}
 
 // bracket one launch with instrumentation events (no-op unless profiling is on)
 #define QVTS_PROF(cat, ...)                       \
@@ -895,7 +910,8 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
             c.cpath = vc.path.as<uint64_t>(); c.cparent = vc.parent_q.as<int32_t>(); c.cz = vc.z.as<int32_t>();
             c.cf = vc.f.as<int32_t>(); c.croot = vc.root.as<int32_t>();
             c.H = m.H; c.W = m.W; c.G = (m.W + 3) / 4;
-            c.ntiles = (int)(((long long)m.H * c.G + 255) / 256);
+            c.rows_cta = correct_rows_per_cta(m.H, c.G);
+            c.ntiles = (m.H + c.rows_cta - 1) / c.rows_cta;
             c.p_int = (float)m.p_int; c.p_stay = (float)m.p_stay; c.p_lat = (float)m.p_lat; c.qsel = -1;
             c.sel_q = c.sel_z = c.sel_out = nullptr;
             const long long nblocks = nq * c.ntiles;
@@ -992,7 +1008,8 @@ static qvts_status correct_selected_t(Model &m, const RootBatch &roots, const in
     c.m8 = m.d_m8.as<uint8_t>(); c.cell = m.d_cell.as<uint8_t>(); c.O64 = m.d_O64.as<double>();
     c.P = m.ql[0].P.as<double>(); c.cnt = m.ql[0].cnt.as<uint16_t>();
     c.child = out; c.cstride = ostride; c.H = m.H; c.W = m.W; c.G = (m.W + 3) / 4;
-    c.ntiles = (int)(((long long)m.H * c.G + 255) / 256);
+    c.rows_cta = correct_rows_per_cta(m.H, c.G);
+    c.ntiles = (m.H + c.rows_cta - 1) / c.rows_cta;
     c.p_int = (float)m.p_int; c.p_stay = (float)m.p_stay; c.p_lat = (float)m.p_lat; c.qsel = -1;
     c.sel_q = sel_q; c.sel_z = sel_z; c.sel_out = sel_out;
     QVTS_PROF(5, k_correct<MASK><<<(unsigned)(n * c.ntiles), 256, 0, st>>>(c));
@@ -1141,7 +1158,8 @@ extern "C" qvts_status qvts_belief_update(qvts_model *m, const float *b_dev, int
     c.cnt = m->bu_cnt.as<uint16_t>(); c.umask = m->bu_umask.as<uint16_t>(); c.off = m->bu_off.as<int32_t>();
     c.vpath = m->bu_path.as<uint64_t>(); c.vroot = m->bu_root.as<int32_t>();
     c.child = out_dev; c.cstride = m->HW; c.H = m->H; c.W = m->W; c.G = (m->W + 3) / 4;
-    c.ntiles = (int)(((long long)m->H * c.G + 255) / 256);
+    c.rows_cta = correct_rows_per_cta(m->H, c.G);
+    c.ntiles = (m->H + c.rows_cta - 1) / c.rows_cta;
     c.p_int = (float)m->p_int; c.p_stay = (float)m->p_stay; c.p_lat = (float)m->p_lat; c.qsel = j;
     c.sel_q = c.sel_z = c.sel_out = nullptr;
 #define QVTS_BU_CORR(MASK) k_correct<MASK><<<c.ntiles, 256, 0, st>>>(c)
