@@ -183,27 +183,30 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_hist(HistArgs a) {
             }
         }
     };
-    auto fetch = [&](int i, uint32_t &e, float4 (&qv)[LEAF ? NAP / 4 : 1]) {
-        if (i < L) {
+    auto fetch_e = [&](int i) -> uint32_t {
+        return i < L ? __ldg(a.entries + soff + (long long)i * T + st) : 0u;
+    };
+    auto fetch_q = [&](int i, float4 (&qv)[LEAF ? NAP / 4 : 1]) {
+        if (LEAF && i < L) {
             const long long slot = soff + (long long)i * T + st;
-            e = __ldg(a.entries + slot);
-            if (LEAF) {
 #pragma unroll
-                for (int h = 0; h < (LEAF ? NAP / 4 : 0); ++h) qv[h] = __ldg(a.qlist + slot * (NAP / 4) + h);
-            }
-        } else {
-            e = 0u;
+            for (int h = 0; h < (LEAF ? NAP / 4 : 0); ++h) qv[h] = __ldg(a.qlist + slot * (NAP / 4) + h);
         }
     };
-    // software pipeline, ping-pong: slot i+1 is in flight while slot i computes
-    uint32_t eA, eB;
+    // software pipeline: entries are loaded two slots ahead (one register each), Q' rows one
+    // slot ahead (ping-pong), so neither load's latency reaches the dependent instructions
+    uint32_t eA = fetch_e(0), eB = fetch_e(1), eC, eD;
     float4 qA[LEAF ? NAP / 4 : 1], qB[LEAF ? NAP / 4 : 1];
-    fetch(0, eA, qA);
+    fetch_q(0, qA);
     for (int i = 0; i < L; i += 2) {
-        fetch(i + 1, eB, qB);
+        eC = fetch_e(i + 2);
+        fetch_q(i + 1, qB);
         cell(eA, qA);
-        fetch(i + 2, eA, qA);
+        eD = fetch_e(i + 3);
+        fetch_q(i + 2, qA);
         cell(eB, qB);
+        eA = eC;
+        eB = eD;
     }
     __syncthreads();   // tiles are dead; reuse the region for the fixed-order class reduction
     constexpr int RS = T + 1;
