@@ -284,6 +284,11 @@ def main():
     f_mhz = 1965.0
     peak = 148 * 128 * 2 * f_mhz * 1e6 / 1e12     # FP32 FMA lanes x 2 flops x max SM clock
     share = {k: round(v / max(1e-9, sum(prof["ms"].values())), 4) for k, v in prof["ms"].items()}
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "r01_roofline_traffic.json")
+    if os.path.exists(tpath) and CFG_NAME == "C4":
+        t = json.load(open(tpath))
+        traffic = t["dram_bytes_read"] + t["dram_bytes_write"]
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -293,7 +298,7 @@ def main():
                                       "vi_sweeps": sweeps}),
         "roofline": {"bound": "alu", "kernel": "k_hist<A8,leaf> (S1+S2+S5)", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
-                     "traffic": None,
+                     "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram__bytes_read+write)",
                      "algorithmic": f"{FLOPS_PER_LEAF_CELL[na]} FP32 flops (FMA = 2) per (leaf parent, free cell) x "
                                     f"{prof['leaf_cells'] / leaf_launches:.3e} per launch; "
                                     "peak = 148 SM x 128 FP32 lanes x 2 x 1965 MHz (guide unit counts)",
