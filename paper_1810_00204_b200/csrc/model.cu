@@ -96,14 +96,14 @@ qvts_status build_bands(Model &m, BandSet &bs, int rows) {
     const int H = m.H, W = m.W, TW = (W + 5 + 3) & ~3;   // row pitch; grid column c at tile column c + 4
     rows = std::max(1, std::min(rows, H));
     // two parents' tiles per hist CTA must fit in shared memory (~190 KB) and index in 16 bits
-    while (rows > 1 && ((long long)(rows + 2) * TW > 65535 || (long long)(rows + 2) * TW * 8 > 72000)) --rows;
+    while (rows > 1 && ((long long)(rows + 5) * TW > 65535 || (long long)(rows + 5) * TW * 8 > 76000)) --rows;
     if ((long long)(rows + 2) * TW > 65535) {
         set_error("grid too wide for the band tile (W+2)*3 > 65535");
         return QVTS_ERR_INVALID_ARG;
     }
     bs.rows = rows;
     bs.nb = (H + rows - 1) / rows;
-    bs.tile_floats = (rows + 2) * TW;
+    bs.tile_floats = (rows + 2 + 3) * TW;      // + 3 zero rows holding the padding cell
     bs.tile_pitch = TW;
     bs.h_bands.assign(bs.nb, BandInfo{});
     std::vector<uint32_t> entries;
@@ -129,8 +129,12 @@ qvts_status build_bands(Model &m, BandSet &bs, int rows) {
             if (need <= T) break;
         }
         if (total == 0) L = 1;
-        bi.L = L;
+        // L rounded to the kernel's 2-cell unroll, plus trailing pad steps for its look-ahead loads
+        const int Lpad = ((L + 1) & ~1) + 4;
+        bi.L = (L + 1) & ~1;
         bi.slot_off = off;
+        // padding slots point at a cell of the 3 zero rows after the tile (zero neighbourhood)
+        const uint32_t pad_e = (uint32_t)((bi.nrows + 2 + 1) * TW + 5);
         // thread ranges per class
         std::vector<int> cls_of(T, -1);
         int t0 = 0;
@@ -155,8 +159,8 @@ qvts_status build_bands(Model &m, BandSet &bs, int rows) {
                 bucket[c][ti & 15].push_back(x);
             }
         }
-        std::vector<uint32_t> e((size_t)L * T, 0u);
-        std::vector<int32_t> sc((size_t)L * T, -1);
+        std::vector<uint32_t> e((size_t)Lpad * T, pad_e);
+        std::vector<int32_t> sc((size_t)Lpad * T, -1);
         for (int step = 0; step < L; ++step)
             for (int g = 0; g < T / 16; ++g) {
                 unsigned used = 0;
@@ -183,7 +187,7 @@ qvts_status build_bands(Model &m, BandSet &bs, int rows) {
         bi.cs[16] = t0;
         entries.insert(entries.end(), e.begin(), e.end());
         bs.h_slot_cell.insert(bs.h_slot_cell.end(), sc.begin(), sc.end());
-        off += (long long)L * T;
+        off += (long long)Lpad * T;
     }
     bs.total_slots = off;
     QVTS_TRY(upload(bs.bands, bs.h_bands));

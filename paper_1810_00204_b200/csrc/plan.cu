@@ -135,6 +135,7 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_hist(HistArgs a) {
             tile[tr * TP + 3] = 0.f;
             tile[tr * TP + 4 + a.W] = 0.f;
         }
+        for (int i = t; i < 3 * TP; i += kPairThreads) tile[TH * TP + i] = 0.f;   // zero rows: pad cell
     }
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();
@@ -143,16 +144,25 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_hist(HistArgs a) {
     float acc[NV];
 #pragma unroll
     for (int i = 0; i < NV; ++i) acc[i] = 0.f;
-    // one cell of the slot stream: neighbours at ti +- 1 (immediate) and ti +- TP
+    // one cell of the slot stream: 32-bit shared addresses, neighbours at immediate offsets from
+    // the cell and from the rows above / below.  Padding slots point at a cell of the zero rows
+    // after the tile (m8 = 0, Q' = 0), so they need no branch.
+    const uint32_t tbase = (uint32_t)__cvta_generic_to_shared(smem + p * a.tstride);
+    const uint32_t TP4 = 4u * (uint32_t)TP;
     auto cell = [&](uint32_t e, const float4 (&qv)[LEAF ? NAP / 4 : 1]) {
-        if (e == 0u) return;                          // padding slot
-        const float *c0 = tile + (e & 0xFFFFu);
-        const uint32_t m8 = (e >> 16) & 0xFFu;
-        const float *cu = c0 - TP, *cd = c0 + TP;
+        const uint32_t c0 = tbase + ((e & 0xFFFFu) << 2);
+        const uint32_t m8 = e >> 16;
+        const uint32_t cu = c0 - TP4, cd = c0 + TP4;
         float nb[9];
-        nb[0] = cu[-1]; nb[1] = cu[0]; nb[2] = cu[1];
-        nb[3] = c0[-1]; nb[4] = c0[0]; nb[5] = c0[1];
-        nb[6] = cd[-1]; nb[7] = cd[0]; nb[8] = cd[1];
+        asm volatile("ld.shared.f32 %0, [%1+-4];" : "=f"(nb[0]) : "r"(cu));
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(nb[1]) : "r"(cu));
+        asm volatile("ld.shared.f32 %0, [%1+4];" : "=f"(nb[2]) : "r"(cu));
+        asm volatile("ld.shared.f32 %0, [%1+-4];" : "=f"(nb[3]) : "r"(c0));
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(nb[4]) : "r"(c0));
+        asm volatile("ld.shared.f32 %0, [%1+4];" : "=f"(nb[5]) : "r"(c0));
+        asm volatile("ld.shared.f32 %0, [%1+-4];" : "=f"(nb[6]) : "r"(cd));
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(nb[7]) : "r"(cd));
+        asm volatile("ld.shared.f32 %0, [%1+4];" : "=f"(nb[8]) : "r"(cd));
         float q[LEAF ? NAP : 1];
         if (LEAF) {
 #pragma unroll
@@ -183,30 +193,34 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_hist(HistArgs a) {
             }
         }
     };
-    auto fetch_e = [&](int i) -> uint32_t {
-        return i < L ? __ldg(a.entries + soff + (long long)i * T + st) : 0u;
-    };
-    auto fetch_q = [&](int i, float4 (&qv)[LEAF ? NAP / 4 : 1]) {
-        if (LEAF && i < L) {
-            const long long slot = soff + (long long)i * T + st;
-#pragma unroll
-            for (int h = 0; h < (LEAF ? NAP / 4 : 0); ++h) qv[h] = __ldg(a.qlist + slot * (NAP / 4) + h);
-        }
-    };
-    // software pipeline: entries are loaded two slots ahead (one register each), Q' rows one
-    // slot ahead (ping-pong), so neither load's latency reaches the dependent instructions
-    uint32_t eA = fetch_e(0), eB = fetch_e(1), eC, eD;
+    // Slot streams are padded on the host by >= 4 steps (pads = the zero cell), so the loads
+    // below never need a bound check.  Entries run two slots ahead, Q' rows one (ping-pong).
+    const uint32_t *ep = a.entries + soff + st;
+    const float4 *qp = a.qlist + (soff + st) * (NAP / 4);
+    constexpr int QSTEP = T * (NAP / 4);
+    uint32_t eA = __ldg(ep), eB = __ldg(ep + T), eC, eD;
     float4 qA[LEAF ? NAP / 4 : 1], qB[LEAF ? NAP / 4 : 1];
-    fetch_q(0, qA);
+    if (LEAF) {
+#pragma unroll
+        for (int h = 0; h < (LEAF ? NAP / 4 : 0); ++h) qA[h] = __ldg(qp + h);
+    }
     for (int i = 0; i < L; i += 2) {
-        eC = fetch_e(i + 2);
-        fetch_q(i + 1, qB);
+        eC = __ldg(ep + 2 * T);
+        if (LEAF) {
+#pragma unroll
+            for (int h = 0; h < (LEAF ? NAP / 4 : 0); ++h) qB[h] = __ldg(qp + QSTEP + h);
+        }
         cell(eA, qA);
-        eD = fetch_e(i + 3);
-        fetch_q(i + 2, qA);
+        eD = __ldg(ep + 3 * T);
+        if (LEAF) {
+#pragma unroll
+            for (int h = 0; h < (LEAF ? NAP / 4 : 0); ++h) qA[h] = __ldg(qp + 2 * QSTEP + h);
+        }
         cell(eB, qB);
         eA = eC;
         eB = eD;
+        ep += 2 * T;
+        qp += 2 * QSTEP;
     }
     __syncthreads();   // tiles are dead; reuse the region for the fixed-order class reduction
     constexpr int RS = T + 1;
