@@ -316,192 +316,197 @@ struct ReduceArgs {
     unsigned long long *counters;   // [0] flagged draws, [1] leaf V-nodes
 };
 
-constexpr int kReduceWarps = 4;
-
+// One CTA per parent V-node, one warp per action (Q-node).  The CTA first sums the parent's band
+// partials into shared memory (coalesced, fixed band order, fp64); then each warp: per-action
+// recombination of the linear fields -> M[s], P(z|b,a) (Eq. 3 normaliser), R(b,a) (PAPER.md:58),
+// n Philox draws (lane j = sample j), counts by ballot; for the leaf level also the Q_MDP value of
+// every sampled child, V(z) = qbar + max_a' [sum_s O[s][z] S[s][a']] / P(z), and the Q-node's
+// backup Q = R + gamma sum_z (f_z/n) V(z) in ascending z (Alg. 6 with gamma, R13).
 template <uint32_t MASK, bool LEAF>
 __host__ __device__ constexpr int reduce_smem_doubles(int pstride) {
-    return kReduceWarps * (pstride + (LEAF ? 16 * mask_count(MASK) + 16 * mask_count(MASK) : 0));
+    return pstride + 8 + (LEAF ? mask_count(MASK) * 32 * mask_count(MASK) : 0);
 }
 
-// The warp first sums the parent's band partials into shared memory (coalesced, fixed band
-// order, fp64), then handles the parent's |A| Q-nodes one after another: per-action
-// recombination of the linear fields -> M[s], P(z|b,a) (Eq. 3 normaliser), R(b,a) (PAPER.md:58),
-// n Philox draws (lane j = sample j), counts by ballot; for the leaf level also the Q_MDP value
-// of every sampled child, V(z) = qbar + max_a' [sum_s O[s][z] S[s][a']] / P(z), and the Q-node's
-// backup Q = R + gamma sum_z (f_z/n) V(z) (Alg. 6 with gamma, R13).
 template <uint32_t MASK, bool LEAF>
-__global__ void __launch_bounds__(kReduceWarps * 32) k_reduce(ReduceArgs a) {
+__global__ void __launch_bounds__(mask_count(MASK) * 32) k_reduce(ReduceArgs a) {
     constexpr int NA = mask_count(MASK);
     constexpr int CB = hist_cb<MASK, LEAF>();
     extern __shared__ double rsm[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const long long w = (long long)blockIdx.x * kReduceWarps + warp;
-    if (w >= a.nwork) return;
-    const int per_warp = a.pstride + (LEAF ? 32 * NA : 0);
-    double *sp = rsm + warp * per_warp;
-    double *sS = sp + a.pstride;            // [16][NA] S of the current action
-    double *sR = sS + 16 * NA;              // [16][NA] ratios of the current action
-    double *sE = sp + 16 * CB;              // E totals, completed below for the orthogonal directions
+    const int lane = threadIdx.x & 31, j = threadIdx.x >> 5;   // warp j = action j
+    const long long w = blockIdx.x;
+    double *sp = rsm;                          // [pstride] band-summed partials
+    double *sE = rsm + a.pstride;              // [8] blocked-mass totals
+    double *sS = sE + 8 + j * 32 * NA;         // [16][NA] S of this warp's action
+    double *sR = sS + 16 * NA;                 // [16][NA] its (z, a') numerators
     const double *pp = a.part + w * a.nb * (long long)a.pstride;
-    for (int i = lane; i < a.pstride; i += 32) {
+    for (int i = threadIdx.x; i < a.pstride; i += NA * 32) {
         double acc = 0.0;
         for (int bd = 0; bd < a.nb; ++bd) acc += pp[(long long)bd * a.pstride + i];
         sp[i] = acc;
     }
-    __syncwarp();
+    __syncthreads();
+    // E[d] = sum_y occ(y + d) b(y); orthogonal directions come from the class masses (signature bit)
+    if (threadIdx.x < 8) {
+        const int d = threadIdx.x, kd = d < 4 ? d : d + 1;
+        double e = sp[16 * CB + d];
+        if (is_orth(kd)) {
+            e = 0.0;
+            for (int s2 = 0; s2 < 16; ++s2) e += class_blocked(kd, s2) * sp[s2 * CB];
+        }
+        sE[d] = e;
+    }
+    __syncthreads();
     const long long v = a.vmap ? (long long)a.vmap[w] : w;
     const float *bp = a.beliefs + v * a.bstride;
     const double mass_s = lane < 16 ? sp[lane * CB] : 0.0;
     double mass = 0.0;
 #pragma unroll
     for (int s = 0; s < 16; ++s) mass += __shfl_sync(0xffffffffu, mass_s, s);
-    // blocked-mass totals E[d] = sum_y occ(y + d) b(y): the orthogonal directions come from the
-    // class masses (their occupancy is a signature bit), fixed class order
-    if (lane < 8) {
-        const int kd = lane < 4 ? lane : lane + 1;
-        if (is_orth(kd)) {
-            double e = 0.0;
-            for (int s2 = 0; s2 < 16; ++s2) e += class_blocked(kd, s2) * sp[s2 * CB];
-            sE[lane] = e;
-        }
-    }
-    __syncwarp();
     const uint64_t vpath = a.vpath[v];
     const int root = a.vroot[v];
     const uint32_t step = a.root_step[root], ep = a.root_ep[root];
-    int leaves = 0, nflag = 0;
 
-    for (int j = 0; j < NA; ++j) {
-        const long long q = w * NA + j;
-        const int k = action_of<MASK>(j);
-        const int da = k == 4 ? 0 : nbit(k), d1 = k == 4 ? 0 : nbit(lat1(k)), d2 = k == 4 ? 0 : nbit(lat2(k));
-        // M[s]: bbar_a summed over signature class s
-        const int k1 = k == 4 ? 4 : lat1(k), k2 = k == 4 ? 4 : lat2(k);
-        double Ms = 0.0;
-        if (lane < 16) {
-            const double *c = sp + lane * CB;
-            const double hma = c[1 + da] + class_blocked(k, lane) * c[0];
-            const double hm1 = c[1 + d1] + class_blocked(k1, lane) * c[0];
-            const double hm2 = c[1 + d2] + class_blocked(k2, lane) * c[0];
-            Ms = (k == 4) ? c[0] : a.p_stay * c[0] + a.p_int * hma + a.p_lat * (hm1 + hm2);
-        }
-        // R(b,a) = (p_stay - 1) sum b - sum c_a b + goal terms, sum c_a b = p_stay mass + p_int E_a + p_lat (E_l1 + E_l2)
-        double R = 0.0;
-        if (lane == 0) {
-            if (k == 4) {
-                R = -2.0 * mass + 2.0 * (double)bp[a.goal];
-            } else {
-                const double Rp = a.p_stay * mass + a.p_int * sE[da] + a.p_lat * (sE[d1] + sE[d2]);
-                R = (a.p_stay - 1.0) * mass - Rp;
-                for (int g = 0; g < a.ngc; ++g)
-                    if (a.gc_act[g] == j) R += a.gc_val[g] * (double)bp[a.gc_cell[g]];
-            }
-        }
-        // P(z|b,a) = sum_s O[s][z] M[s]  (fixed s order)
-        double Pz = 0.0;
-#pragma unroll
-        for (int s = 0; s < 16; ++s) {
-            const double m = __shfl_sync(0xffffffffu, Ms, s);
-            if (lane < 16) Pz += a.O64[s * 16 + lane] * m;
-        }
-        double C[16];
-        double acc = 0.0;
-#pragma unroll
-        for (int z = 0; z < 16; ++z) {
-            acc += __shfl_sync(0xffffffffu, Pz, z);
-            C[z] = acc;
-        }
-        // S3: n draws keyed by the tree path (Appendix A.2-A.5)
-        const uint64_t qpath = vpath | ((uint64_t)(k + 1) << (8 * a.level));
-        int cntk = 0;
-        for (int j0 = 0; j0 < a.n; j0 += 32) {
-            const int jj = j0 + lane;
-            int z = -1;
-            if (jj < a.n) {
-                const uint4 r = philox4x32_10(make_uint4((uint32_t)jj, (uint32_t)qpath, (uint32_t)(qpath >> 32), step),
-                                              make_uint2(a.seed, ep));
-                const double u = philox_uniform(r.x);
-                const double tt = u * C[15];
-                z = 0;
-                double gap = INFINITY;
-#pragma unroll
-                for (int kk = 0; kk < 16; ++kk) {
-                    z += (C[kk] <= tt) ? 1 : 0;
-                    if (kk < 15) gap = fmin(gap, fabs(tt - C[kk]));
-                }
-                z = min(z, 15);
-                nflag += gap < 1e-6 ? 1 : 0;
-                if (a.zdraw) a.zdraw[q * a.n + jj] = (uint8_t)z;
-            }
-#pragma unroll
-            for (int kk = 0; kk < 16; ++kk) {
-                const unsigned bal = __ballot_sync(0xffffffffu, z == kk);
-                if (lane == kk) cntk += __popc(bal);
-            }
-        }
-        const unsigned um = __ballot_sync(0xffffffffu, lane < 16 && cntk > 0) & 0xFFFFu;
-        const int U = __popc(um);
-        leaves += U;
-        if (lane < 16) {
-            a.P[q * 16 + lane] = Pz;
-            a.cnt[q * 16 + lane] = (uint16_t)cntk;
-        }
-        if (lane == 0) {
-            a.R[q] = R;
-            a.umask[q] = (uint16_t)um;
-            a.U[q] = U;
-        }
-        if (LEAF) {
-            // S[s][a'] of this action from the linear fields, staged for the (z, a') dot products
-            if (lane < 16) {
-                const double *c = sp + lane * CB;
-                const double oa = class_blocked(k, lane), o1 = class_blocked(k1, lane), o2 = class_blocked(k2, lane);
-#pragma unroll
-                for (int j2 = 0; j2 < NA; ++j2) {
-                    const double zb = c[9 + j2];
-                    const double ha = c[9 + NA + da * NA + j2] + oa * zb;
-                    const double h1 = c[9 + NA + d1 * NA + j2] + o1 * zb;
-                    const double h2 = c[9 + NA + d2 * NA + j2] + o2 * zb;
-                    sS[lane * NA + j2] = (k == 4) ? zb : a.p_stay * zb + a.p_int * ha + a.p_lat * (h1 + h2);
-                }
-            }
-            __syncwarp();
-            // lane -> (u, a'): ratio = sum_s O[s][z_u] S[s][a'] / P(z_u)
-            for (int idx = lane; idx < U * NA; idx += 32) {
-                const int u = idx / NA, j2 = idx % NA;
-                unsigned rem = um;
-                for (int i = 0; i < u; ++i) rem &= rem - 1;
-                const int z = __ffs(rem) - 1;
-                double num = 0.0;
-#pragma unroll
-                for (int s = 0; s < 16; ++s) num += a.O64[s * 16 + z] * sS[s * NA + j2];
-                sR[u * NA + j2] = num;
-            }
-            __syncwarp();
-            // frequencies live in lanes 0..15: gather them for lane 0 in z order
-            double accq = 0.0;
-            unsigned rem = um;
-            for (int u = 0; u < U; ++u) {
-                const int z = __ffs(rem) - 1;
-                rem &= rem - 1;
-                const int f = __shfl_sync(0xffffffffu, cntk, z);
-                const double Pzz = __shfl_sync(0xffffffffu, Pz, z);
-                if (lane == 0) {
-                    double best = -INFINITY;
-                    for (int j2 = 0; j2 < NA; ++j2) best = fmax(best, sR[u * NA + j2]);
-                    const double Vz = a.qbar + best / Pzz;
-                    accq += ((double)f / (double)a.n) * Vz;
-                    if (a.leafV) a.leafV[q * 16 + z] = Vz;
-                }
-            }
-            if (lane == 0) a.Q[q] = R + a.gamma * accq;
-            __syncwarp();
+    const long long q = w * NA + j;
+    const int k = action_of<MASK>(j);
+    const int da = k == 4 ? 0 : nbit(k), d1 = k == 4 ? 0 : nbit(lat1(k)), d2 = k == 4 ? 0 : nbit(lat2(k));
+    const int k1 = k == 4 ? 4 : lat1(k), k2 = k == 4 ? 4 : lat2(k);
+    // M[s]: bbar_a summed over signature class s
+    double Ms = 0.0;
+    if (lane < 16) {
+        const double *c = sp + lane * CB;
+        const double hma = c[1 + da] + class_blocked(k, lane) * c[0];
+        const double hm1 = c[1 + d1] + class_blocked(k1, lane) * c[0];
+        const double hm2 = c[1 + d2] + class_blocked(k2, lane) * c[0];
+        Ms = (k == 4) ? c[0] : a.p_stay * c[0] + a.p_int * hma + a.p_lat * (hm1 + hm2);
+    }
+    // R(b,a) = (p_stay - 1) sum b - sum c_a b + goal terms, sum c_a b = p_stay mass + p_int E_a + p_lat (E_l1 + E_l2)
+    double R = 0.0;
+    if (lane == 0) {
+        if (k == 4) {
+            R = -2.0 * mass + 2.0 * (double)bp[a.goal];
+        } else {
+            const double Rp = a.p_stay * mass + a.p_int * sE[da] + a.p_lat * (sE[d1] + sE[d2]);
+            R = (a.p_stay - 1.0) * mass - Rp;
+            for (int g = 0; g < a.ngc; ++g)
+                if (a.gc_act[g] == j) R += a.gc_val[g] * (double)bp[a.gc_cell[g]];
         }
     }
+    // P(z|b,a) = sum_s O[s][z] M[s]  (fixed s order)
+    double Pz = 0.0;
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+        const double m = __shfl_sync(0xffffffffu, Ms, s);
+        if (lane < 16) Pz += a.O64[s * 16 + lane] * m;
+    }
+    double C[16];
+    double acc = 0.0;
+#pragma unroll
+    for (int z = 0; z < 16; ++z) {
+        acc += __shfl_sync(0xffffffffu, Pz, z);
+        C[z] = acc;
+    }
+    // S3: n draws keyed by the tree path (Appendix A.2-A.5)
+    const uint64_t qpath = vpath | ((uint64_t)(k + 1) << (8 * a.level));
+    int cntk = 0, nflag = 0;
+    for (int j0 = 0; j0 < a.n; j0 += 32) {
+        const int jj = j0 + lane;
+        int z = -1;
+        if (jj < a.n) {
+            const uint4 r = philox4x32_10(make_uint4((uint32_t)jj, (uint32_t)qpath, (uint32_t)(qpath >> 32), step),
+                                          make_uint2(a.seed, ep));
+            const double u = philox_uniform(r.x);
+            const double tt = u * C[15];
+            z = 0;
+            double gap = INFINITY;
+#pragma unroll
+            for (int kk = 0; kk < 16; ++kk) {
+                z += (C[kk] <= tt) ? 1 : 0;
+                if (kk < 15) gap = fmin(gap, fabs(tt - C[kk]));
+            }
+            z = min(z, 15);
+            nflag += gap < 1e-6 ? 1 : 0;
+            if (a.zdraw) a.zdraw[q * a.n + jj] = (uint8_t)z;
+        }
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) {
+            const unsigned bal = __ballot_sync(0xffffffffu, z == kk);
+            if (lane == kk) cntk += __popc(bal);
+        }
+    }
+    const unsigned um = __ballot_sync(0xffffffffu, lane < 16 && cntk > 0) & 0xFFFFu;
+    const int U = __popc(um);
+    if (lane < 16) {
+        a.P[q * 16 + lane] = Pz;
+        a.cnt[q * 16 + lane] = (uint16_t)cntk;
+    }
+    if (lane == 0) {
+        a.R[q] = R;
+        a.umask[q] = (uint16_t)um;
+        a.U[q] = U;
+    }
+    if (LEAF) {
+        // S[s][a'] of this action from the linear fields, staged for the (z, a') dot products
+        if (lane < 16) {
+            const double *c = sp + lane * CB;
+            const double oa = class_blocked(k, lane), o1 = class_blocked(k1, lane), o2 = class_blocked(k2, lane);
+#pragma unroll
+            for (int j2 = 0; j2 < NA; ++j2) {
+                const double zb = c[9 + j2];
+                const double ha = c[9 + NA + da * NA + j2] + oa * zb;
+                const double h1 = c[9 + NA + d1 * NA + j2] + o1 * zb;
+                const double h2 = c[9 + NA + d2 * NA + j2] + o2 * zb;
+                sS[lane * NA + j2] = (k == 4) ? zb : a.p_stay * zb + a.p_int * ha + a.p_lat * (h1 + h2);
+            }
+        }
+        __syncwarp();
+        // lane -> (u, a'): numerator sum_s O[s][z_u] S[s][a']
+        for (int idx = lane; idx < U * NA; idx += 32) {
+            const int u = idx / NA, j2 = idx % NA;
+            unsigned rem = um;
+            for (int i = 0; i < u; ++i) rem &= rem - 1;
+            const int z = __ffs(rem) - 1;
+            double num = 0.0;
+#pragma unroll
+            for (int s = 0; s < 16; ++s) num += a.O64[s * 16 + z] * sS[s * NA + j2];
+            sR[u * NA + j2] = num;
+        }
+        __syncwarp();
+        // lane u < U: V(z_u) = qbar + max_a' num / P(z_u); then the backup in ascending z on lane 0
+        double Vz = 0.0, wz = 0.0;
+        int zu = 0;
+        if (lane < U) {
+            unsigned rem = um;
+            for (int i = 0; i < lane; ++i) rem &= rem - 1;
+            zu = __ffs(rem) - 1;
+            double best = -INFINITY;
+            for (int j2 = 0; j2 < NA; ++j2) best = fmax(best, sR[lane * NA + j2]);
+            Vz = best;   // divided below by P(z), held by lane z
+        }
+        const int zsrc = lane < U ? zu : 0;
+        const double Pexact = __shfl_sync(0xffffffffu, Pz, zsrc);
+        const int f = __shfl_sync(0xffffffffu, cntk, zsrc);
+        if (lane < U) {
+            Vz = a.qbar + Vz / Pexact;
+            wz = (double)f / (double)a.n;
+            if (a.leafV) a.leafV[q * 16 + zu] = Vz;
+        }
+        double accq = 0.0;
+        for (int u = 0; u < U; ++u) accq += __shfl_sync(0xffffffffu, wz, u) * __shfl_sync(0xffffffffu, Vz, u);
+        if (lane == 0) a.Q[q] = R + a.gamma * accq;
+    }
+    // flagged-draw and leaf counts: per CTA in shared memory, one global atomic each
+    __shared__ unsigned int s_cnt[2];
+    if (threadIdx.x < 2) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
     for (int o = 16; o > 0; o >>= 1) nflag += __shfl_xor_sync(0xffffffffu, nflag, o);
-    if (lane == 0 && a.counters) {
-        if (nflag) atomicAdd(&a.counters[0], (unsigned long long)nflag);
-        if (LEAF) atomicAdd(&a.counters[1], (unsigned long long)leaves);
+    if (lane == 0) {
+        if (nflag) atomicAdd(&s_cnt[0], (unsigned)nflag);
+        if (LEAF) atomicAdd(&s_cnt[1], (unsigned)U);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && a.counters) {
+        if (s_cnt[0]) atomicAdd(&a.counters[0], (unsigned long long)s_cnt[0]);
+        if (LEAF) atomicAdd(&a.counters[1], (unsigned long long)s_cnt[1]);
     }
 }
 
@@ -797,9 +802,10 @@ static qvts_status launch_hist(Model &m, const BandSet &bs, const float *beliefs
 template <uint32_t MASK, bool LEAF>
 static qvts_status launch_reduce(Model &m, const ReduceArgs &r, cudaStream_t st) {
     constexpr int NA = mask_count(MASK);
-    const size_t smem = sizeof(double) * kReduceWarps * (r.pstride + (LEAF ? 32 * NA : 0));
+    const size_t smem = sizeof(double) * reduce_smem_doubles<MASK, LEAF>(r.pstride);
     QVTS_CUDA(cudaFuncSetAttribute(k_reduce<MASK, LEAF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    QVTS_PROF(LEAF ? 2 : 3, k_reduce<MASK, LEAF><<<nblk(r.nwork, kReduceWarps), kReduceWarps * 32, smem, st>>>(r));
+    if (r.nwork > 0x7FFFFFFFLL) { set_error("too many parents"); return QVTS_ERR_INVALID_ARG; }
+    QVTS_PROF(LEAF ? 2 : 3, k_reduce<MASK, LEAF><<<(unsigned)r.nwork, NA * 32, smem, st>>>(r));
     QVTS_CUDA(cudaGetLastError());
     return QVTS_OK;
 }
