@@ -2,6 +2,7 @@
 // and the fp64 value-iteration kernels (K1) behind qvts_value_iteration.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "qvts_internal.cuh"
@@ -96,7 +97,7 @@ qvts_status build_bands(Model &m, BandSet &bs, int rows) {
     const int H = m.H, W = m.W, TW = (W + 5 + 3) & ~3;   // row pitch; grid column c at tile column c + 4
     rows = std::max(1, std::min(rows, H));
     // two parents' tiles per hist CTA must fit in shared memory (~190 KB) and index in 16 bits
-    while (rows > 1 && ((long long)(rows + 5) * TW > 65535 || (long long)(rows + 5) * TW * 8 > 76000)) --rows;
+    while (rows > 1 && ((long long)(rows + 5) * TW > 65535 || (long long)(rows + 5) * TW * 8 > 100000)) --rows;
     if ((long long)(rows + 2) * TW > 65535) {
         set_error("grid too wide for the band tile (W+2)*3 > 65535");
         return QVTS_ERR_INVALID_ARG;
@@ -429,7 +430,14 @@ extern "C" qvts_status qvts_model_create(const qvts_model_desc *d, qvts_model **
         if ((st = upload(m->d_gc_act, gc_act)) != QVTS_OK) break;
         if ((st = upload(m->d_gc_val, gc_val)) != QVTS_OK) break;
         // band sets: ~16K cells per band for many parents, ~2K for few (more CTAs per parent)
-        if ((st = build_bands(*m, m->band_big, std::max(1, 8192 / W))) != QVTS_OK) break;
+        // big bands: as tall as two CTAs' tiles per SM allow, balanced over the grid
+        // (QVTS_BAND_ROWS overrides the row count for tuning experiments)
+        const int TWp = (W + 5 + 3) & ~3;
+        const int max_rows = std::max(1, (int)(100000 / ((long long)TWp * 8)) - 5);
+        const int nb_big = (H + max_rows - 1) / max_rows;
+        int big_rows = (H + nb_big - 1) / nb_big;
+        if (const char *ev = std::getenv("QVTS_BAND_ROWS")) big_rows = std::max(1, std::atoi(ev));
+        if ((st = build_bands(*m, m->band_big, big_rows)) != QVTS_OK) break;
         if ((st = build_bands(*m, m->band_small, std::max(1, 1024 / W))) != QVTS_OK) break;
         if (cudaEventCreate(&m->ev0) != cudaSuccess || cudaEventCreate(&m->ev1) != cudaSuccess) {
             set_error("cudaEventCreate failed"); st = QVTS_ERR_CUDA; break;

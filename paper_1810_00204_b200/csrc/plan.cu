@@ -12,6 +12,7 @@
 // Backup (S6): k_vmax (level D-1), k_backup (levels D-2..0).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include <cooperative_groups.h>
@@ -341,7 +342,13 @@ __global__ void __launch_bounds__(mask_count(MASK) * 32) k_reduce(ReduceArgs a) 
     const double *pp = a.part + w * a.nb * (long long)a.pstride;
     for (int i = threadIdx.x; i < a.pstride; i += NA * 32) {
         double acc = 0.0;
-        for (int bd = 0; bd < a.nb; ++bd) acc += pp[(long long)bd * a.pstride + i];
+        int bd = 0;
+        for (; bd + 4 <= a.nb; bd += 4) {          // independent loads, fixed-order sum
+            const double x0 = pp[(long long)bd * a.pstride + i], x1 = pp[(long long)(bd + 1) * a.pstride + i];
+            const double x2 = pp[(long long)(bd + 2) * a.pstride + i], x3 = pp[(long long)(bd + 3) * a.pstride + i];
+            acc += x0; acc += x1; acc += x2; acc += x3;
+        }
+        for (; bd < a.nb; ++bd) acc += pp[(long long)bd * a.pstride + i];
         sp[i] = acc;
     }
     __syncthreads();
@@ -775,7 +782,13 @@ static qvts_status launch_hist(Model &m, const BandSet &bs, const float *beliefs
     a.red_off = 0;
     a.sums_off = ((2 * kRedChunk * (kHistThreads + 1)) + 3) & ~3;
     const int region = std::max(2 * a.tstride, a.sums_off + 2 * 2 * NOUT);
-    a.cluster = bs.nb <= 8 ? 1 : 0;
+    // DSMEM cluster reduction over the bands of a parent pair: off by default (measured slower
+    // than writing one fp64 partial per band); QVTS_HIST_CLUSTER=1 enables it
+    static const int use_cluster = [] {
+        const char *ev = std::getenv("QVTS_HIST_CLUSTER");
+        return ev ? std::atoi(ev) : 0;
+    }();
+    a.cluster = (use_cluster && bs.nb <= 8) ? 1 : 0;
     a.part = m.part.as<double>(); a.pstride = pstride;
     const size_t smem = (size_t)region * sizeof(float);
     QVTS_CUDA(cudaFuncSetAttribute(k_hist<MASK, LEAF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
