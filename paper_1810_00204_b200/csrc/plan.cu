@@ -33,6 +33,254 @@ __device__ __forceinline__ int action_of(int j) {
     return k;
 }
 
+template <uint32_t MASK, bool LEAF>
+__host__ __device__ constexpr int hist_cb() {      // class-binned values per thread
+    return 1 + 8 + (LEAF ? mask_count(MASK) * 9 : 0);
+}
+template <uint32_t MASK, bool LEAF>
+__host__ __device__ constexpr int hist_nv() { return hist_cb<MASK, LEAF>() + 8; }
+constexpr int kRedChunk = 48;                       // values per reduction round
+
+// direction index di (0..7) <-> stencil id k != 4
+__host__ __device__ constexpr int dir_k(int di) { return di < 4 ? di : di + 1; }
+// orthogonal moves: their target's occupancy is the wall-signature bit (PAPER.md:336 sensors)
+__host__ __device__ constexpr bool is_orth(int k) { return k == 1 || k == 3 || k == 5 || k == 7; }
+__host__ __device__ constexpr int orth_bit(int k) { return k == 1 ? 0 : k == 3 ? 1 : k == 5 ? 2 : 3; }
+// occupancy of y + d_k for every cell of signature class s, or 0 when it is not class-constant
+__device__ __forceinline__ double class_blocked(int k, int s) {
+    return (k != 4 && is_orth(k) && ((s >> orth_bit(k)) & 1)) ? 1.0 : 0.0;
+}
+
+// ---- S2 tail + S3 (+ S5 tail + S6 leaf backup) ------------------------------------------------
+struct ReduceArgs {
+    const double *part;
+    int pstride, nb;
+    long long nwork;
+    const int32_t *vmap;
+    const float *beliefs;
+    long long bstride;
+    const uint64_t *vpath;
+    const int32_t *vroot;
+    const uint32_t *root_step, *root_ep;
+    uint32_t seed;
+    int level, n;
+    const double *O64;
+    int ngc;
+    const int32_t *gc_cell, *gc_act;
+    const double *gc_val;
+    int goal;
+    double p_stay, p_int, p_lat, gamma, qbar;
+    double *R, *P;
+    uint16_t *cnt, *umask;
+    int32_t *U;
+    uint8_t *zdraw;
+    double *Q, *leafV;
+    unsigned long long *counters;   // [0] flagged draws, [1] leaf V-nodes
+};
+
+// One CTA per parent V-node, one warp per action (Q-node).  The CTA first sums the parent's band
+// partials into shared memory (coalesced, fixed band order, fp64); then each warp: per-action
+// recombination of the linear fields -> M[s], P(z|b,a) (Eq. 3 normaliser), R(b,a) (PAPER.md:58),
+// n Philox draws (lane j = sample j), counts by ballot; for the leaf level also the Q_MDP value of
+// every sampled child, V(z) = qbar + max_a' [sum_s O[s][z] S[s][a']] / P(z), and the Q-node's
+// backup Q = R + gamma sum_z (f_z/n) V(z) in ascending z (Alg. 6 with gamma, R13).
+template <uint32_t MASK, bool LEAF>
+__host__ __device__ constexpr int reduce_smem_doubles(int pstride) {
+    return pstride + 8 + (LEAF ? mask_count(MASK) * 32 * mask_count(MASK) : 0);
+}
+
+// Executed by a whole CTA of nthreads (a multiple of 32) for parent w; warp j handles actions
+// j, j + nwarps, ...  rsm: reduce_smem_doubles(pstride) doubles of shared memory.
+template <uint32_t MASK, bool LEAF>
+__device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int nthreads) {
+    constexpr int NA = mask_count(MASK);
+    constexpr int CB = hist_cb<MASK, LEAF>();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = nthreads >> 5;
+    double *sp = rsm;                          // [pstride] band-summed partials
+    double *sE = rsm + a.pstride;              // [8] blocked-mass totals
+    const double *pp = a.part + w * a.nb * (long long)a.pstride;
+    for (int i = threadIdx.x; i < a.pstride; i += nthreads) {
+        double acc = 0.0;
+        int bd = 0;
+        for (; bd + 4 <= a.nb; bd += 4) {          // independent loads, fixed-order sum
+            const double x0 = pp[(long long)bd * a.pstride + i], x1 = pp[(long long)(bd + 1) * a.pstride + i];
+            const double x2 = pp[(long long)(bd + 2) * a.pstride + i], x3 = pp[(long long)(bd + 3) * a.pstride + i];
+            acc += x0; acc += x1; acc += x2; acc += x3;
+        }
+        for (; bd < a.nb; ++bd) acc += pp[(long long)bd * a.pstride + i];
+        sp[i] = acc;
+    }
+    __syncthreads();
+    // E[d] = sum_y occ(y + d) b(y); orthogonal directions come from the class masses (signature bit)
+    if (threadIdx.x < 8) {
+        const int d = threadIdx.x, kd = d < 4 ? d : d + 1;
+        double e = sp[16 * CB + d];
+        if (is_orth(kd)) {
+            e = 0.0;
+            for (int s2 = 0; s2 < 16; ++s2) e += class_blocked(kd, s2) * sp[s2 * CB];
+        }
+        sE[d] = e;
+    }
+    __syncthreads();
+    const long long v = a.vmap ? (long long)a.vmap[w] : w;
+    const float *bp = a.beliefs + v * a.bstride;
+    const double mass_s = lane < 16 ? sp[lane * CB] : 0.0;
+    double mass = 0.0;
+#pragma unroll
+    for (int s = 0; s < 16; ++s) mass += __shfl_sync(0xffffffffu, mass_s, s);
+    const uint64_t vpath = a.vpath[v];
+    const int root = a.vroot[v];
+    const uint32_t step = a.root_step[root], ep = a.root_ep[root];
+    int nflag = 0, leaves = 0;
+    for (int j = warp; j < NA; j += nwarps) {
+    double *sS = sE + 8 + warp * 32 * NA;      // [16][NA] S of this warp's action
+    double *sR = sS + 16 * NA;                 // [16][NA] its (z, a') numerators
+    const long long q = w * NA + j;
+    const int k = action_of<MASK>(j);
+    const int da = k == 4 ? 0 : nbit(k), d1 = k == 4 ? 0 : nbit(lat1(k)), d2 = k == 4 ? 0 : nbit(lat2(k));
+    const int k1 = k == 4 ? 4 : lat1(k), k2 = k == 4 ? 4 : lat2(k);
+    // M[s]: bbar_a summed over signature class s
+    double Ms = 0.0;
+    if (lane < 16) {
+        const double *c = sp + lane * CB;
+        const double hma = c[1 + da] + class_blocked(k, lane) * c[0];
+        const double hm1 = c[1 + d1] + class_blocked(k1, lane) * c[0];
+        const double hm2 = c[1 + d2] + class_blocked(k2, lane) * c[0];
+        Ms = (k == 4) ? c[0] : a.p_stay * c[0] + a.p_int * hma + a.p_lat * (hm1 + hm2);
+    }
+    // R(b,a) = (p_stay - 1) sum b - sum c_a b + goal terms, sum c_a b = p_stay mass + p_int E_a + p_lat (E_l1 + E_l2)
+    double R = 0.0;
+    if (lane == 0) {
+        if (k == 4) {
+            R = -2.0 * mass + 2.0 * (double)bp[a.goal];
+        } else {
+            const double Rp = a.p_stay * mass + a.p_int * sE[da] + a.p_lat * (sE[d1] + sE[d2]);
+            R = (a.p_stay - 1.0) * mass - Rp;
+            for (int g = 0; g < a.ngc; ++g)
+                if (a.gc_act[g] == j) R += a.gc_val[g] * (double)bp[a.gc_cell[g]];
+        }
+    }
+    // P(z|b,a) = sum_s O[s][z] M[s]  (fixed s order)
+    double Pz = 0.0;
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+        const double m = __shfl_sync(0xffffffffu, Ms, s);
+        if (lane < 16) Pz += a.O64[s * 16 + lane] * m;
+    }
+    double C[16];
+    double acc = 0.0;
+#pragma unroll
+    for (int z = 0; z < 16; ++z) {
+        acc += __shfl_sync(0xffffffffu, Pz, z);
+        C[z] = acc;
+    }
+    // S3: n draws keyed by the tree path (Appendix A.2-A.5)
+    const uint64_t qpath = vpath | ((uint64_t)(k + 1) << (8 * a.level));
+    int cntk = 0;
+    for (int j0 = 0; j0 < a.n; j0 += 32) {
+        const int jj = j0 + lane;
+        int z = -1;
+        if (jj < a.n) {
+            const uint4 r = philox4x32_10(make_uint4((uint32_t)jj, (uint32_t)qpath, (uint32_t)(qpath >> 32), step),
+                                          make_uint2(a.seed, ep));
+            const double u = philox_uniform(r.x);
+            const double tt = u * C[15];
+            z = 0;
+            double gap = INFINITY;
+#pragma unroll
+            for (int kk = 0; kk < 16; ++kk) {
+                z += (C[kk] <= tt) ? 1 : 0;
+                if (kk < 15) gap = fmin(gap, fabs(tt - C[kk]));
+            }
+            z = min(z, 15);
+            nflag += gap < 1e-6 ? 1 : 0;
+            if (a.zdraw) a.zdraw[q * a.n + jj] = (uint8_t)z;
+        }
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) {
+            const unsigned bal = __ballot_sync(0xffffffffu, z == kk);
+            if (lane == kk) cntk += __popc(bal);
+        }
+    }
+    const unsigned um = __ballot_sync(0xffffffffu, lane < 16 && cntk > 0) & 0xFFFFu;
+    const int U = __popc(um);
+    leaves += U;
+    if (lane < 16) {
+        a.P[q * 16 + lane] = Pz;
+        a.cnt[q * 16 + lane] = (uint16_t)cntk;
+    }
+    if (lane == 0) {
+        a.R[q] = R;
+        a.umask[q] = (uint16_t)um;
+        a.U[q] = U;
+    }
+    if (LEAF) {
+        // S[s][a'] of this action from the linear fields, staged for the (z, a') dot products
+        if (lane < 16) {
+            const double *c = sp + lane * CB;
+            const double oa = class_blocked(k, lane), o1 = class_blocked(k1, lane), o2 = class_blocked(k2, lane);
+#pragma unroll
+            for (int j2 = 0; j2 < NA; ++j2) {
+                const double zb = c[9 + j2];
+                const double ha = c[9 + NA + da * NA + j2] + oa * zb;
+                const double h1 = c[9 + NA + d1 * NA + j2] + o1 * zb;
+                const double h2 = c[9 + NA + d2 * NA + j2] + o2 * zb;
+                sS[lane * NA + j2] = (k == 4) ? zb : a.p_stay * zb + a.p_int * ha + a.p_lat * (h1 + h2);
+            }
+        }
+        __syncwarp();
+        // lane -> (u, a'): numerator sum_s O[s][z_u] S[s][a']
+        for (int idx = lane; idx < U * NA; idx += 32) {
+            const int u = idx / NA, j2 = idx % NA;
+            unsigned rem = um;
+            for (int i = 0; i < u; ++i) rem &= rem - 1;
+            const int z = __ffs(rem) - 1;
+            double num = 0.0;
+#pragma unroll
+            for (int s = 0; s < 16; ++s) num += a.O64[s * 16 + z] * sS[s * NA + j2];
+            sR[u * NA + j2] = num;
+        }
+        __syncwarp();
+        // lane u < U: V(z_u) = qbar + max_a' num / P(z_u); then the backup in ascending z on lane 0
+        double Vz = 0.0, wz = 0.0;
+        int zu = 0;
+        if (lane < U) {
+            unsigned rem = um;
+            for (int i = 0; i < lane; ++i) rem &= rem - 1;
+            zu = __ffs(rem) - 1;
+            double best = -INFINITY;
+            for (int j2 = 0; j2 < NA; ++j2) best = fmax(best, sR[lane * NA + j2]);
+            Vz = best;   // divided below by P(z), held by lane z
+        }
+        const int zsrc = lane < U ? zu : 0;
+        const double Pexact = __shfl_sync(0xffffffffu, Pz, zsrc);
+        const int f = __shfl_sync(0xffffffffu, cntk, zsrc);
+        if (lane < U) {
+            Vz = a.qbar + Vz / Pexact;
+            wz = (double)f / (double)a.n;
+            if (a.leafV) a.leafV[q * 16 + zu] = Vz;
+        }
+        double accq = 0.0;
+        for (int u = 0; u < U; ++u) accq += __shfl_sync(0xffffffffu, wz, u) * __shfl_sync(0xffffffffu, Vz, u);
+        if (lane == 0) a.Q[q] = R + a.gamma * accq;
+        __syncwarp();
+    }
+    }   // actions of this warp
+    // flagged-draw and leaf counts: per warp, one global atomic each (counts are integers)
+    for (int o = 16; o > 0; o >>= 1) nflag += __shfl_xor_sync(0xffffffffu, nflag, o);
+    if (lane == 0 && a.counters) {
+        if (nflag) atomicAdd(&a.counters[0], (unsigned long long)nflag);
+        if (LEAF && leaves) atomicAdd(&a.counters[1], (unsigned long long)leaves);
+    }
+    __syncthreads();   // rsm may be reused by the caller
+}
+
+template <uint32_t MASK, bool LEAF>
+__global__ void __launch_bounds__(mask_count(MASK) * 32) k_reduce(ReduceArgs a) {
+    extern __shared__ double rsm[];
+    reduce_parent<MASK, LEAF>(a, blockIdx.x, rsm, mask_count(MASK) * 32);
+}
+
 // ---- S1 + S2 (+ S5): signature-binned histograms ----------------------------------------------
 // Linear form of the clamped predict: with the 8 clamped source fields
 //   h_k(y) = b(y - d_k) + occ(y + d_k) b(y)          (k = the 8 moving stencil directions)
@@ -60,25 +308,10 @@ struct HistArgs {
     int cluster;          // 1: bands of a pair form one cluster and reduce through DSMEM
     double *part;
     int pstride;
+    int fused;            // 1: the last band CTA of a pair runs reduce_parent (tickets[pair])
+    int *tickets;
+    ReduceArgs red;
 };
-
-template <uint32_t MASK, bool LEAF>
-__host__ __device__ constexpr int hist_cb() {      // class-binned values per thread
-    return 1 + 8 + (LEAF ? mask_count(MASK) * 9 : 0);
-}
-template <uint32_t MASK, bool LEAF>
-__host__ __device__ constexpr int hist_nv() { return hist_cb<MASK, LEAF>() + 8; }
-constexpr int kRedChunk = 48;                       // values per reduction round
-
-// direction index di (0..7) <-> stencil id k != 4
-__host__ __device__ constexpr int dir_k(int di) { return di < 4 ? di : di + 1; }
-// orthogonal moves: their target's occupancy is the wall-signature bit (PAPER.md:336 sensors)
-__host__ __device__ constexpr bool is_orth(int k) { return k == 1 || k == 3 || k == 5 || k == 7; }
-__host__ __device__ constexpr int orth_bit(int k) { return k == 1 ? 0 : k == 3 ? 1 : k == 5 ? 2 : 3; }
-// occupancy of y + d_k for every cell of signature class s, or 0 when it is not class-constant
-__device__ __forceinline__ double class_blocked(int k, int s) {
-    return (k != 4 && is_orth(k) && ((s >> orth_bit(k)) & 1)) ? 1.0 : 0.0;
-}
 
 template <uint32_t MASK, bool LEAF>
 __global__ void __launch_bounds__(kPairThreads, 2) k_hist(HistArgs a) {
@@ -287,233 +520,22 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_hist(HistArgs a) {
             const long long wp = 2 * pair + pp;
             if (wp < a.nwork) a.part[(wp * a.nb + band) * (long long)a.pstride + oo] = sums[o];
         }
-    }
-}
-
-// ---- S2 tail + S3 (+ S5 tail + S6 leaf backup): one warp per parent V-node ---------------------
-struct ReduceArgs {
-    const double *part;
-    int pstride, nb;
-    long long nwork;
-    const int32_t *vmap;
-    const float *beliefs;
-    long long bstride;
-    const uint64_t *vpath;
-    const int32_t *vroot;
-    const uint32_t *root_step, *root_ep;
-    uint32_t seed;
-    int level, n;
-    const double *O64;
-    int ngc;
-    const int32_t *gc_cell, *gc_act;
-    const double *gc_val;
-    int goal;
-    double p_stay, p_int, p_lat, gamma, qbar;
-    double *R, *P;
-    uint16_t *cnt, *umask;
-    int32_t *U;
-    uint8_t *zdraw;
-    double *Q, *leafV;
-    unsigned long long *counters;   // [0] flagged draws, [1] leaf V-nodes
-};
-
-// One CTA per parent V-node, one warp per action (Q-node).  The CTA first sums the parent's band
-// partials into shared memory (coalesced, fixed band order, fp64); then each warp: per-action
-// recombination of the linear fields -> M[s], P(z|b,a) (Eq. 3 normaliser), R(b,a) (PAPER.md:58),
-// n Philox draws (lane j = sample j), counts by ballot; for the leaf level also the Q_MDP value of
-// every sampled child, V(z) = qbar + max_a' [sum_s O[s][z] S[s][a']] / P(z), and the Q-node's
-// backup Q = R + gamma sum_z (f_z/n) V(z) in ascending z (Alg. 6 with gamma, R13).
-template <uint32_t MASK, bool LEAF>
-__host__ __device__ constexpr int reduce_smem_doubles(int pstride) {
-    return pstride + 8 + (LEAF ? mask_count(MASK) * 32 * mask_count(MASK) : 0);
-}
-
-template <uint32_t MASK, bool LEAF>
-__global__ void __launch_bounds__(mask_count(MASK) * 32) k_reduce(ReduceArgs a) {
-    constexpr int NA = mask_count(MASK);
-    constexpr int CB = hist_cb<MASK, LEAF>();
-    extern __shared__ double rsm[];
-    const int lane = threadIdx.x & 31, j = threadIdx.x >> 5;   // warp j = action j
-    const long long w = blockIdx.x;
-    double *sp = rsm;                          // [pstride] band-summed partials
-    double *sE = rsm + a.pstride;              // [8] blocked-mass totals
-    double *sS = sE + 8 + j * 32 * NA;         // [16][NA] S of this warp's action
-    double *sR = sS + 16 * NA;                 // [16][NA] its (z, a') numerators
-    const double *pp = a.part + w * a.nb * (long long)a.pstride;
-    for (int i = threadIdx.x; i < a.pstride; i += NA * 32) {
-        double acc = 0.0;
-        int bd = 0;
-        for (; bd + 4 <= a.nb; bd += 4) {          // independent loads, fixed-order sum
-            const double x0 = pp[(long long)bd * a.pstride + i], x1 = pp[(long long)(bd + 1) * a.pstride + i];
-            const double x2 = pp[(long long)(bd + 2) * a.pstride + i], x3 = pp[(long long)(bd + 3) * a.pstride + i];
-            acc += x0; acc += x1; acc += x2; acc += x3;
-        }
-        for (; bd < a.nb; ++bd) acc += pp[(long long)bd * a.pstride + i];
-        sp[i] = acc;
-    }
-    __syncthreads();
-    // E[d] = sum_y occ(y + d) b(y); orthogonal directions come from the class masses (signature bit)
-    if (threadIdx.x < 8) {
-        const int d = threadIdx.x, kd = d < 4 ? d : d + 1;
-        double e = sp[16 * CB + d];
-        if (is_orth(kd)) {
-            e = 0.0;
-            for (int s2 = 0; s2 < 16; ++s2) e += class_blocked(kd, s2) * sp[s2 * CB];
-        }
-        sE[d] = e;
-    }
-    __syncthreads();
-    const long long v = a.vmap ? (long long)a.vmap[w] : w;
-    const float *bp = a.beliefs + v * a.bstride;
-    const double mass_s = lane < 16 ? sp[lane * CB] : 0.0;
-    double mass = 0.0;
-#pragma unroll
-    for (int s = 0; s < 16; ++s) mass += __shfl_sync(0xffffffffu, mass_s, s);
-    const uint64_t vpath = a.vpath[v];
-    const int root = a.vroot[v];
-    const uint32_t step = a.root_step[root], ep = a.root_ep[root];
-
-    const long long q = w * NA + j;
-    const int k = action_of<MASK>(j);
-    const int da = k == 4 ? 0 : nbit(k), d1 = k == 4 ? 0 : nbit(lat1(k)), d2 = k == 4 ? 0 : nbit(lat2(k));
-    const int k1 = k == 4 ? 4 : lat1(k), k2 = k == 4 ? 4 : lat2(k);
-    // M[s]: bbar_a summed over signature class s
-    double Ms = 0.0;
-    if (lane < 16) {
-        const double *c = sp + lane * CB;
-        const double hma = c[1 + da] + class_blocked(k, lane) * c[0];
-        const double hm1 = c[1 + d1] + class_blocked(k1, lane) * c[0];
-        const double hm2 = c[1 + d2] + class_blocked(k2, lane) * c[0];
-        Ms = (k == 4) ? c[0] : a.p_stay * c[0] + a.p_int * hma + a.p_lat * (hm1 + hm2);
-    }
-    // R(b,a) = (p_stay - 1) sum b - sum c_a b + goal terms, sum c_a b = p_stay mass + p_int E_a + p_lat (E_l1 + E_l2)
-    double R = 0.0;
-    if (lane == 0) {
-        if (k == 4) {
-            R = -2.0 * mass + 2.0 * (double)bp[a.goal];
-        } else {
-            const double Rp = a.p_stay * mass + a.p_int * sE[da] + a.p_lat * (sE[d1] + sE[d2]);
-            R = (a.p_stay - 1.0) * mass - Rp;
-            for (int g = 0; g < a.ngc; ++g)
-                if (a.gc_act[g] == j) R += a.gc_val[g] * (double)bp[a.gc_cell[g]];
-        }
-    }
-    // P(z|b,a) = sum_s O[s][z] M[s]  (fixed s order)
-    double Pz = 0.0;
-#pragma unroll
-    for (int s = 0; s < 16; ++s) {
-        const double m = __shfl_sync(0xffffffffu, Ms, s);
-        if (lane < 16) Pz += a.O64[s * 16 + lane] * m;
-    }
-    double C[16];
-    double acc = 0.0;
-#pragma unroll
-    for (int z = 0; z < 16; ++z) {
-        acc += __shfl_sync(0xffffffffu, Pz, z);
-        C[z] = acc;
-    }
-    // S3: n draws keyed by the tree path (Appendix A.2-A.5)
-    const uint64_t qpath = vpath | ((uint64_t)(k + 1) << (8 * a.level));
-    int cntk = 0, nflag = 0;
-    for (int j0 = 0; j0 < a.n; j0 += 32) {
-        const int jj = j0 + lane;
-        int z = -1;
-        if (jj < a.n) {
-            const uint4 r = philox4x32_10(make_uint4((uint32_t)jj, (uint32_t)qpath, (uint32_t)(qpath >> 32), step),
-                                          make_uint2(a.seed, ep));
-            const double u = philox_uniform(r.x);
-            const double tt = u * C[15];
-            z = 0;
-            double gap = INFINITY;
-#pragma unroll
-            for (int kk = 0; kk < 16; ++kk) {
-                z += (C[kk] <= tt) ? 1 : 0;
-                if (kk < 15) gap = fmin(gap, fabs(tt - C[kk]));
-            }
-            z = min(z, 15);
-            nflag += gap < 1e-6 ? 1 : 0;
-            if (a.zdraw) a.zdraw[q * a.n + jj] = (uint8_t)z;
-        }
-#pragma unroll
-        for (int kk = 0; kk < 16; ++kk) {
-            const unsigned bal = __ballot_sync(0xffffffffu, z == kk);
-            if (lane == kk) cntk += __popc(bal);
-        }
-    }
-    const unsigned um = __ballot_sync(0xffffffffu, lane < 16 && cntk > 0) & 0xFFFFu;
-    const int U = __popc(um);
-    if (lane < 16) {
-        a.P[q * 16 + lane] = Pz;
-        a.cnt[q * 16 + lane] = (uint16_t)cntk;
-    }
-    if (lane == 0) {
-        a.R[q] = R;
-        a.umask[q] = (uint16_t)um;
-        a.U[q] = U;
-    }
-    if (LEAF) {
-        // S[s][a'] of this action from the linear fields, staged for the (z, a') dot products
-        if (lane < 16) {
-            const double *c = sp + lane * CB;
-            const double oa = class_blocked(k, lane), o1 = class_blocked(k1, lane), o2 = class_blocked(k2, lane);
-#pragma unroll
-            for (int j2 = 0; j2 < NA; ++j2) {
-                const double zb = c[9 + j2];
-                const double ha = c[9 + NA + da * NA + j2] + oa * zb;
-                const double h1 = c[9 + NA + d1 * NA + j2] + o1 * zb;
-                const double h2 = c[9 + NA + d2 * NA + j2] + o2 * zb;
-                sS[lane * NA + j2] = (k == 4) ? zb : a.p_stay * zb + a.p_int * ha + a.p_lat * (h1 + h2);
+        if (a.fused) {
+            // the last band CTA of this parent pair runs the pair's reduce/sample (k_reduce's
+            // work) while the band partials are still in L2; the ticket only picks who, the sum
+            // order over bands is fixed
+            __shared__ int s_last;
+            __threadfence();
+            __syncthreads();
+            if (t == 0) s_last = (atomicAdd(a.tickets + pair, 1) == a.nb - 1);
+            __syncthreads();
+            if (s_last) {
+                __threadfence();
+                double *rsm = reinterpret_cast<double *>(smem);
+                for (int pp = 0; pp < 2; ++pp)
+                    if (2 * pair + pp < a.nwork) reduce_parent<MASK, LEAF>(a.red, 2 * pair + pp, rsm, kPairThreads);
             }
         }
-        __syncwarp();
-        // lane -> (u, a'): numerator sum_s O[s][z_u] S[s][a']
-        for (int idx = lane; idx < U * NA; idx += 32) {
-            const int u = idx / NA, j2 = idx % NA;
-            unsigned rem = um;
-            for (int i = 0; i < u; ++i) rem &= rem - 1;
-            const int z = __ffs(rem) - 1;
-            double num = 0.0;
-#pragma unroll
-            for (int s = 0; s < 16; ++s) num += a.O64[s * 16 + z] * sS[s * NA + j2];
-            sR[u * NA + j2] = num;
-        }
-        __syncwarp();
-        // lane u < U: V(z_u) = qbar + max_a' num / P(z_u); then the backup in ascending z on lane 0
-        double Vz = 0.0, wz = 0.0;
-        int zu = 0;
-        if (lane < U) {
-            unsigned rem = um;
-            for (int i = 0; i < lane; ++i) rem &= rem - 1;
-            zu = __ffs(rem) - 1;
-            double best = -INFINITY;
-            for (int j2 = 0; j2 < NA; ++j2) best = fmax(best, sR[lane * NA + j2]);
-            Vz = best;   // divided below by P(z), held by lane z
-        }
-        const int zsrc = lane < U ? zu : 0;
-        const double Pexact = __shfl_sync(0xffffffffu, Pz, zsrc);
-        const int f = __shfl_sync(0xffffffffu, cntk, zsrc);
-        if (lane < U) {
-            Vz = a.qbar + Vz / Pexact;
-            wz = (double)f / (double)a.n;
-            if (a.leafV) a.leafV[q * 16 + zu] = Vz;
-        }
-        double accq = 0.0;
-        for (int u = 0; u < U; ++u) accq += __shfl_sync(0xffffffffu, wz, u) * __shfl_sync(0xffffffffu, Vz, u);
-        if (lane == 0) a.Q[q] = R + a.gamma * accq;
-    }
-    // flagged-draw and leaf counts: per CTA in shared memory, one global atomic each
-    __shared__ unsigned int s_cnt[2];
-    if (threadIdx.x < 2) s_cnt[threadIdx.x] = 0;
-    __syncthreads();
-    for (int o = 16; o > 0; o >>= 1) nflag += __shfl_xor_sync(0xffffffffu, nflag, o);
-    if (lane == 0) {
-        if (nflag) atomicAdd(&s_cnt[0], (unsigned)nflag);
-        if (LEAF) atomicAdd(&s_cnt[1], (unsigned)U);
-    }
-    __syncthreads();
-    if (threadIdx.x == 0 && a.counters) {
-        if (s_cnt[0]) atomicAdd(&a.counters[0], (unsigned long long)s_cnt[0]);
-        if (LEAF) atomicAdd(&a.counters[1], (unsigned long long)s_cnt[1]);
     }
 }
 
@@ -768,7 +790,8 @@ static inline int correct_rows_per_cta(int H, int G) {
 
 template <uint32_t MASK, bool LEAF>
 static qvts_status launch_hist(Model &m, const BandSet &bs, const float *beliefs, long long bstride,
-                               const int32_t *vmap, long long nwork, int pstride, cudaStream_t st, int *nb_eff) {
+                               const int32_t *vmap, long long nwork, int pstride, cudaStream_t st, int *nb_eff,
+                               const ReduceArgs *red = nullptr, bool *fused_out = nullptr) {
     constexpr int NOUT = 16 * hist_cb<MASK, LEAF>() + 8;
     HistArgs a;
     a.beliefs = beliefs; a.bstride = bstride; a.vmap = vmap; a.nwork = nwork;
@@ -790,7 +813,25 @@ static qvts_status launch_hist(Model &m, const BandSet &bs, const float *beliefs
     }();
     a.cluster = (use_cluster && bs.nb <= 8) ? 1 : 0;
     a.part = m.part.as<double>(); a.pstride = pstride;
-    const size_t smem = (size_t)region * sizeof(float);
+    // fused reduce (the last band CTA of each pair runs reduce_parent): measured slower than a
+    // separate k_reduce launch, so off unless QVTS_FUSED_REDUCE=1
+    static const int use_fused = [] {
+        const char *ev = std::getenv("QVTS_FUSED_REDUCE");
+        return ev ? std::atoi(ev) : 0;
+    }();
+    a.fused = (use_fused && red && !a.cluster) ? 1 : 0;
+    a.tickets = nullptr;
+    if (a.fused) {
+        const long long npairs = (nwork + 1) / 2;
+        QVTS_TRY(m.tickets.ensure(sizeof(int) * npairs));
+        QVTS_CUDA(cudaMemsetAsync(m.tickets.p, 0, sizeof(int) * npairs, st));
+        a.tickets = m.tickets.as<int>();
+        a.red = *red;
+        a.red.nb = bs.nb;
+    }
+    if (fused_out) *fused_out = a.fused != 0;
+    const size_t smem = (size_t)std::max<size_t>((size_t)region * sizeof(float),
+                                                 a.fused ? sizeof(double) * reduce_smem_doubles<MASK, LEAF>(pstride) : 0);
     QVTS_CUDA(cudaFuncSetAttribute(k_hist<MASK, LEAF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const long long nblocks = ((nwork + 1) / 2) * bs.nb;
     if (nblocks > 0x7FFFFFFFLL) { set_error("too many hist blocks"); return QVTS_ERR_INVALID_ARG; }
@@ -896,10 +937,8 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
             const int pstride = pstride_of<MASK>(leaf);
             QVTS_TRY(m.part.ensure(sizeof(double) * (size_t)(nwork + 1) * bs.nb * pstride));
             int nb_eff = bs.nb;
-            if (leaf) QVTS_TRY((launch_hist<MASK, true>(m, bs, bel, bstride, vmap, nwork, pstride, st, &nb_eff)));
-            else QVTS_TRY((launch_hist<MASK, false>(m, bs, bel, bstride, vmap, nwork, pstride, st, &nb_eff)));
             ReduceArgs r;
-            r.part = m.part.as<double>(); r.pstride = pstride; r.nb = nb_eff; r.nwork = nwork; r.vmap = vmap;
+            r.part = m.part.as<double>(); r.pstride = pstride; r.nb = bs.nb; r.nwork = nwork; r.vmap = vmap;
             r.beliefs = bel; r.bstride = bstride; r.vpath = vl.path.as<uint64_t>(); r.vroot = vl.root.as<int32_t>();
             r.root_step = roots.step_dev; r.root_ep = roots.episode_dev; r.seed = cfg.seed;
             r.level = d; r.n = n; r.O64 = m.d_O64.as<double>();
@@ -911,8 +950,14 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
             r.zdraw = trace ? ql.zdraw.as<uint8_t>() : nullptr;
             r.Q = ql.Q.as<double>(); r.leafV = (trace && leaf) ? ql.leafV.as<double>() : nullptr;
             r.counters = m.counters.as<unsigned long long>();
+            bool fused = false;
+            if (leaf) QVTS_TRY((launch_hist<MASK, true>(m, bs, bel, bstride, vmap, nwork, pstride, st, &nb_eff, &r, &fused)));
+            else QVTS_TRY((launch_hist<MASK, false>(m, bs, bel, bstride, vmap, nwork, pstride, st, &nb_eff, &r, &fused)));
+            r.nb = nb_eff;
+            if (!fused) {
             if (leaf) QVTS_TRY((launch_reduce<MASK, true>(m, r, st)));
             else QVTS_TRY((launch_reduce<MASK, false>(m, r, st)));
+            }
             QVTS_CUDA(cudaGetLastError());
         }
         if (leaf) break;
