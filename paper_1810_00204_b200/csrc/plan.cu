@@ -99,16 +99,28 @@ __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int
     double *sp = rsm;                          // [pstride] band-summed partials
     double *sE = rsm + a.pstride;              // [8] blocked-mass totals
     const double *pp = a.part + w * a.nb * (long long)a.pstride;
-    for (int i = threadIdx.x; i < a.pstride; i += nthreads) {
-        double acc = 0.0;
+    // band sum, fixed band order; two elements per pass with all their band loads in flight
+    for (int i0 = threadIdx.x; i0 < a.pstride; i0 += 2 * nthreads) {
+        const int i1 = i0 + nthreads;
+        const bool has1 = i1 < a.pstride;
+        double acc0 = 0.0, acc1 = 0.0;
         int bd = 0;
-        for (; bd + 4 <= a.nb; bd += 4) {          // independent loads, fixed-order sum
-            const double x0 = pp[(long long)bd * a.pstride + i], x1 = pp[(long long)(bd + 1) * a.pstride + i];
-            const double x2 = pp[(long long)(bd + 2) * a.pstride + i], x3 = pp[(long long)(bd + 3) * a.pstride + i];
-            acc += x0; acc += x1; acc += x2; acc += x3;
+        for (; bd + 4 <= a.nb; bd += 4) {
+            double x[4], y[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                x[u] = pp[(long long)(bd + u) * a.pstride + i0];
+                y[u] = has1 ? pp[(long long)(bd + u) * a.pstride + i1] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) { acc0 += x[u]; acc1 += y[u]; }
         }
-        for (; bd < a.nb; ++bd) acc += pp[(long long)bd * a.pstride + i];
-        sp[i] = acc;
+        for (; bd < a.nb; ++bd) {
+            acc0 += pp[(long long)bd * a.pstride + i0];
+            if (has1) acc1 += pp[(long long)bd * a.pstride + i1];
+        }
+        sp[i0] = acc0;
+        if (has1) sp[i1] = acc1;
     }
     __syncthreads();
     // E[d] = sum_y occ(y + d) b(y); orthogonal directions come from the class masses (signature bit)
