@@ -621,20 +621,29 @@ template <int K>
 __device__ __forceinline__ void correct_predict(const CorrectArgs &a, int r, int c0, const float (&nbh)[3][6],
                                                 float (&bb)[4], int (&sg)[4]) {
 #pragma unroll
+    // cell info of the 4 cells in one 32-bit load each when the row is 4-aligned
+    const int x0 = r * a.W + c0;
+    uint32_t info4 = 0, m84 = 0;
+    const bool al = ((a.W & 3) == 0) && (c0 + 3 < a.W);
+    if (al) {
+        info4 = __ldg(reinterpret_cast<const unsigned int *>(a.cell + x0));
+        if (K != 4) m84 = __ldg(reinterpret_cast<const unsigned int *>(a.m8 + x0));
+    }
+#pragma unroll
     for (int i = 0; i < 4; ++i) {
         const int c = c0 + i;
         bb[i] = 0.f;
         sg[i] = 0;
         if (c >= a.W) continue;
-        const int x = r * a.W + c;
-        const int info = __ldg(a.cell + x);
+        const int x = x0 + i;
+        const int info = al ? (int)((info4 >> (8 * i)) & 0xFFu) : (int)__ldg(a.cell + x);
         sg[i] = info & 15;
         if (info & 16) continue;                      // occupied: no mass
         const float b0 = nbh[1][1 + i];
         if (K == 4) {
             bb[i] = b0;
         } else {
-            const int m8 = __ldg(a.m8 + x);
+            const int m8 = al ? (int)((m84 >> (8 * i)) & 0xFFu) : (int)__ldg(a.m8 + x);
             constexpr int L1 = lat1(K), L2 = lat2(K);
             const float sa = nbh[1 - st_dr(K)][1 + i - st_dc(K)];
             const float s1 = nbh[1 - st_dr(L1)][1 + i - st_dc(L1)];
