@@ -98,6 +98,7 @@ def _declare(L):
     L.or_belief_update.argtypes = [vp, _dp, C.c_int, C.c_int, _dp, C.POINTER(C.c_double)]
     L.or_value_iteration.argtypes = [vp, C.c_double, C.c_int, _dp, _dp, C.POINTER(C.c_int),
                                      C.POINTER(C.c_double)]
+    L.or_fib.argtypes = [vp, C.c_double, C.c_int, _dp, C.POINTER(C.c_int), C.POINTER(C.c_double)]
     L.or_qmdp_value.restype = C.c_double
     L.or_qmdp_value.argtypes = [vp, _dp, _dp, C.POINTER(C.c_int)]
     L.or_trace_new.restype = vp
@@ -270,6 +271,12 @@ class Model:
         sw, res = C.c_int(0), C.c_double(0)
         st = lib().or_value_iteration(self._h, eps, max_sweeps, V, Q, C.byref(sw), C.byref(res))
         return st, V, Q.reshape(self.na, self.nx), sw.value, res.value
+
+    def fib(self, eps=1e-9, max_iter=100000):
+        alpha = np.zeros(self.na * self.nx)
+        it, res = C.c_int(0), C.c_double(0)
+        st = lib().or_fib(self._h, eps, max_iter, alpha, C.byref(it), C.byref(res))
+        return st, alpha.reshape(self.na, self.nx), it.value, res.value
 
     def qmdp_value(self, Q, b):
         arg = C.c_int(0)

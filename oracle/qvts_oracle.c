@@ -342,6 +342,54 @@ int or_value_iteration(const or_model *m, double eps, int max_sweeps, double *V,
     return st;
 }
 
+/* Fast Informed Bound, Eq. 7:
+ *   alpha^a(x) = R(x,a) + gamma sum_z max_a' sum_x' O(x',z) T(x,a,x') alpha^a'(x'),
+ * a monotone contraction; synchronous iteration from alpha = R_max/(1-gamma). */
+int or_fib(const or_model *m, double eps, int max_iter, double *alpha, int *iters, double *resid) {
+    int nx = m->nx, na = m->na, nz = m->nz;
+    double rmax = -INFINITY;
+    for (int i = 0; i < nx * na; ++i) if (m->R[i] > rmax) rmax = m->R[i];
+    double *an = (double *)malloc(sizeof(double) * (size_t)na * nx);
+    for (int a = 0; a < na; ++a)
+        for (int x = 0; x < nx; ++x)
+            alpha[(size_t)a * nx + x] = (m->is_grid && m->occ[x]) ? 0.0 : rmax / (1.0 - m->gamma);
+    int k = 0, st = OR_ERR_NOT_CONVERGED;
+    double res = INFINITY;
+    while (k < max_iter) {
+        res = 0.0;
+        for (int x = 0; x < nx; ++x)
+            for (int a = 0; a < na; ++a) {
+                double v = 0.0;
+                if (!(m->is_grid && m->occ[x])) {
+                    double s = 0.0;
+                    for (int z = 0; z < nz; ++z) {
+                        double best = -INFINITY;
+                        for (int a2 = 0; a2 < na; ++a2) {
+                            double d = 0.0;
+                            for (int e = m->t_start[x * na + a]; e < m->t_start[x * na + a + 1]; ++e) {
+                                int y = m->t_y[e];
+                                d += m->O[y * nz + z] * m->t_p[e] * alpha[(size_t)a2 * nx + y];
+                            }
+                            if (d > best) best = d;
+                        }
+                        s += best;
+                    }
+                    v = m->R[x * na + a] + m->gamma * s;
+                }
+                an[(size_t)a * nx + x] = v;
+                double dd = fabs(v - alpha[(size_t)a * nx + x]);
+                if (dd > res) res = dd;
+            }
+        memcpy(alpha, an, sizeof(double) * (size_t)na * nx);
+        ++k;
+        if (res < eps) { st = OR_OK; break; }
+    }
+    if (iters) *iters = k;
+    if (resid) *resid = res;
+    free(an);
+    return st;
+}
+
 /* Eq. 4 with one alpha-vector per action, alpha_a = Q(.,a) (north star Q_MDP leaf; R14). */
 double or_qmdp_value(const or_model *m, const double *Q, const double *b, int *argmax) {
     double best = -INFINITY;

@@ -56,6 +56,10 @@ int or_belief_update(const or_model *m, const double *b, int a, int z, double *o
 /* ---- MDP value iteration, Q layout [na][nx] ---- */
 int or_value_iteration(const or_model *m, double eps, int max_sweeps, double *V, double *Q,
                        int *sweeps, double *resid);
+/* Fast Informed Bound (Eq. 7): one alpha-vector per action, iterated from
+ * alpha = R_max/(1-gamma) until max|alpha' - alpha| < eps; layout [na][nx].
+ * Occupied grid cells: alpha = 0 (unreachable, as for Q). */
+int or_fib(const or_model *m, double eps, int max_iter, double *alpha, int *iters, double *resid);
 /* Eq. 4 with alpha_a = Q(.,a): max_a sum_x b(x) Q(x,a); argmax lowest index. */
 double or_qmdp_value(const or_model *m, const double *Q, const double *b, int *argmax);
 

@@ -409,3 +409,58 @@ def test_episode_bookkeeping_replay():
         x = int(lx[s])
     assert ret == pytest.approx(rec.disc_return, abs=1e-12)
     assert x == rec.x_final
+
+
+# ---- FIB (Eq. 6-7, NEXT-1) ----------------------------------------------------------------------
+def test_fib_identity_observation_equals_mdp():
+    """O = identity (|Z| = |X|): FIB is the MDP Q-function."""
+    rng = np.random.default_rng(3)
+    nx, na = 6, 3
+    T = rng.random((nx, na, nx)) ** 3
+    T /= T.sum(axis=2, keepdims=True)
+    R = -rng.random((nx, na))
+    m = O.Model.dense(T, np.eye(nx), R, 0.9)
+    st, alpha, it, res = m.fib(1e-11)
+    st2, V, Q, _, _ = m.value_iteration(1e-11)
+    assert st == O.OK and st2 == O.OK
+    assert np.allclose(alpha, Q, atol=1e-9)
+
+
+def test_fib_uninformative_observation_closed_form():
+    """Uniform O: the z-sum collapses, alpha^a = R(.,a) + gamma max_a' T_a alpha^a' (one a' per
+    (x,a)) — iterated here with dense matrices."""
+    rng = np.random.default_rng(5)
+    nx, na, nz = 5, 3, 4
+    T = rng.random((nx, na, nx))
+    T /= T.sum(axis=2, keepdims=True)
+    R = -rng.random((nx, na))
+    m = O.Model.dense(T, np.full((nx, nz), 1.0 / nz), R, 0.85)
+    st, alpha, _, _ = m.fib(1e-12)
+    a = np.full((na, nx), R.max() / (1 - 0.85))
+    for _ in range(2000):
+        nxt = np.stack([R[:, k] + 0.85 * np.max(np.stack([T[:, k, :] @ a[k2] for k2 in range(na)]), axis=0)
+                        for k in range(na)])
+        if np.max(np.abs(nxt - a)) < 1e-13:
+            a = nxt
+            break
+        a = nxt
+    assert np.allclose(alpha, a, atol=1e-10)
+
+
+def test_fib_constant_reward_and_bounds_on_grid():
+    T = np.zeros((3, 2, 3))
+    for i in range(3):
+        T[i, 0, i] = 1
+        T[i, 1, (i + 1) % 3] = 1
+    m = O.Model.dense(T, np.array([[0.7, 0.3], [0.2, 0.8], [0.5, 0.5]]), np.full((3, 2), -2.0), 0.8)
+    st, alpha, _, _ = m.fib(1e-12)
+    assert np.allclose(alpha, -2.0 / 0.2, atol=1e-9)
+    gm = W.random_map(9, 10, 0.2, seed=13)
+    g = O.Model.grid(gm, action_mask=W.A8, acc=0.9)
+    st, alpha, it, res = g.fib(1e-9)
+    _, V, Q, _, _ = g.value_iteration(1e-9)
+    free = gm.occupancy == 0
+    assert st == O.OK and res < 1e-9
+    # FIB is an upper bound no looser than Q_MDP (the max over a' moved inside the z-sum)
+    assert np.all(alpha[:, free] <= Q[:, free] + 1e-9)
+    assert np.any(alpha[:, free] < Q[:, free] - 1e-3)
