@@ -95,6 +95,16 @@ QVTS_API qvts_status qvts_value_iteration(qvts_model *model, double eps, int32_t
 /* Host copy of Q in fp64, layout [|A|][H*W]; QVTS_ERR_STATE before value iteration. */
 QVTS_API qvts_status qvts_get_q(const qvts_model *model, double *q_host);
 
+/* ---- (2b) Fast Informed Bound (Eq. 6-7) ------------
+ * alpha^a(x) = R(x,a) + gamma sum_z max_a' sum_x' O(x',z) T(x,a,x') alpha^a'(x'), synchronous
+ * fp64 iteration from alpha = max R / (1 - gamma) to max|delta| < eps.  The result
+ * is one alpha-vector per action, an upper bound on V* no looser than Q_MDP; plan steps with
+ * cfg.leaf_bound = QVTS_LEAF_FIB score leaves with it (Eq. 4).  Occupied cells: alpha = 0. */
+QVTS_API qvts_status qvts_fib_iteration(qvts_model *model, double eps, int32_t max_sweeps,
+                                        int32_t *sweeps_out, double *residual_out, void *stream);
+/* Host copy of alpha_FIB in fp64, [|A|][H*W]; QVTS_ERR_STATE before qvts_fib_iteration. */
+QVTS_API qvts_status qvts_get_alpha(const qvts_model *model, double *alpha_host);
+
 /* ---- (3) Bayes belief update, Eq. 3 ----------------------------------
  * out(x') = O(x',z) sum_x T(x,a,x') b(x) / P(z|b,a); *p_obs_out = P(z|b,a) (fp64).
  * b_dev and out_dev: device fp32 [H*W] (may not alias).  QVTS_ERR_ZERO_LIKELIHOOD when
@@ -109,11 +119,13 @@ QVTS_API qvts_status qvts_belief_update(qvts_model *model, const float *b_dev, i
  * readings R9/R10), one child per unique z weighted by its frequency f/n,
  * Q_MDP leaves (Eq. 4, R14), backup Q = R + gamma sum (f/n) V, V = max_a Q (Alg. 6-7, R13),
  * action = argmax_a Q(root, a), ties to the lowest stencil id (R16/R18). */
+typedef enum { QVTS_LEAF_QMDP = 0, QVTS_LEAF_FIB = 1 } qvts_leaf_bound;
 typedef struct {
     int32_t depth;        /* number of action levels D, 1..8 (reading R15)                       */
     int32_t n_samples;    /* observations drawn per Q-node, 1..4096                               */
     uint32_t seed, step, episode;
     int32_t want_trace;   /* 1: keep per-node draws for qvts_trace_* (costs memory)               */
+    int32_t leaf_bound;   /* qvts_leaf_bound: Q_MDP (north star, R14) or FIB (needs qvts_fib_iteration) */
 } qvts_plan_cfg;
 
 typedef struct {

@@ -347,8 +347,9 @@ int or_value_iteration(const or_model *m, double eps, int max_sweeps, double *V,
  * a monotone contraction; synchronous iteration from alpha = R_max/(1-gamma). */
 int or_fib(const or_model *m, double eps, int max_iter, double *alpha, int *iters, double *resid) {
     int nx = m->nx, na = m->na, nz = m->nz;
-    double rmax = -INFINITY;
-    for (int i = 0; i < nx * na; ++i) if (m->R[i] > rmax) rmax = m->R[i];
+    double rmax = -INFINITY;   /* over reachable states: occupied grid rows carry R := 0 (R5) */
+    for (int i = 0; i < nx * na; ++i)
+        if (!(m->is_grid && m->occ[i / na]) && m->R[i] > rmax) rmax = m->R[i];
     double *an = (double *)malloc(sizeof(double) * (size_t)na * nx);
     for (int a = 0; a < na; ++a)
         for (int x = 0; x < nx; ++x)

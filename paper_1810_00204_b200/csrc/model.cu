@@ -210,15 +210,93 @@ __global__ void k_qlist(const double *__restrict__ Q64, const int32_t *__restric
     }
 }
 
-qvts_status build_qlists(Model &m, cudaStream_t st) {
+qvts_status build_qlists(Model &m, const double *src64, double qbar, bool fib, cudaStream_t st) {
     for (BandSet *bs : {&m.band_big, &m.band_small}) {
-        QVTS_TRY(bs->qlist.ensure(sizeof(float) * bs->total_slots * m.NAP));
+        DevBuf &dst = fib ? bs->qlist_fib : bs->qlist;
+        QVTS_TRY(dst.ensure(sizeof(float) * bs->total_slots * m.NAP));
         long long n = bs->total_slots;
-        k_qlist<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(m.d_Q64.as<double>(), bs->slot_cell.as<int32_t>(), n,
-                                                            m.NA, m.NAP, m.HW, m.qbar, bs->qlist.as<float>());
+        k_qlist<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(src64, bs->slot_cell.as<int32_t>(), n, m.NA, m.NAP, m.HW,
+                                                            qbar, dst.as<float>());
         QVTS_CUDA(cudaGetLastError());
     }
     return QVTS_OK;
+}
+
+// ---- Fast Informed Bound (Eq. 7), fp64 -----------------------------------------
+// One sweep, one thread per cell: for every action a, the clamped successor taps y_t with
+// probabilities p_t (as in VI), then alpha'(x,a) = R(x,a) + gamma sum_z max_a' sum_t
+// O[sig(y_t)][z] p_t alpha(y_t, a').  Occupied cells keep 0.  No-op once converged (as VI).
+template <uint32_t MASK>
+__global__ void __launch_bounds__(128) k_fib_sweep(const double *__restrict__ Ain, double *__restrict__ Aout,
+                                                   const double *__restrict__ R64, const uint8_t *__restrict__ m8v,
+                                                   const uint8_t *__restrict__ freev, const uint8_t *__restrict__ sigv,
+                                                   const double *__restrict__ O64g, int HW, int W, double p_int,
+                                                   double p_stay, double p_lat, double gamma,
+                                                   unsigned long long *resid, int k, double eps) {
+    if (k > 0 && __longlong_as_double((long long)resid[k - 1]) < eps) return;   // converged
+    constexpr int NA = mask_count(MASK);
+    __shared__ double sO[256];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) sO[i] = O64g[i];
+    __syncthreads();
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    double diff = 0.0;
+    if (x < HW) {
+        const bool fr = freev[x] != 0;
+        const int m8 = m8v[x];
+#pragma unroll 1
+        for (int j = 0; j < NA; ++j) {
+            double out = 0.0;
+            if (fr) {
+                int kk = 0;
+#pragma unroll
+                for (int i = 0; i < NA; ++i) if (i == j) kk = mask_action(MASK, i);
+                int ty[4], ts[4];
+                double tp[4];
+                int nt;
+                auto tgt = [&](int kd) -> int {
+                    if ((m8 >> nbit(kd)) & 1) return x;
+                    return x + st_dr(kd) * W + st_dc(kd);
+                };
+                if (kk == 4) {
+                    ty[0] = x; tp[0] = 1.0; nt = 1;
+                } else {
+                    ty[0] = tgt(kk); tp[0] = p_int;
+                    ty[1] = x; tp[1] = p_stay;
+                    ty[2] = tgt(lat1(kk)); tp[2] = p_lat;
+                    ty[3] = tgt(lat2(kk)); tp[3] = p_lat;
+                    nt = 4;
+                }
+                double v[NA][4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    ts[t] = t < nt ? sigv[ty[t]] : 0;
+#pragma unroll
+                    for (int a2 = 0; a2 < NA; ++a2) v[a2][t] = t < nt ? tp[t] * Ain[(size_t)a2 * HW + ty[t]] : 0.0;
+                }
+                double s = 0.0;
+                for (int z = 0; z < 16; ++z) {
+                    const double o0 = sO[ts[0] * 16 + z], o1 = sO[ts[1] * 16 + z], o2 = sO[ts[2] * 16 + z],
+                                 o3 = sO[ts[3] * 16 + z];
+                    double best = -INFINITY;
+#pragma unroll
+                    for (int a2 = 0; a2 < NA; ++a2)
+                        best = fmax(best, o0 * v[a2][0] + o1 * v[a2][1] + o2 * v[a2][2] + o3 * v[a2][3]);
+                    s += best;
+                }
+                out = R64[(size_t)j * HW + x] + gamma * s;
+            }
+            Aout[(size_t)j * HW + x] = out;
+            diff = fmax(diff, fabs(out - Ain[(size_t)j * HW + x]));
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) diff = fmax(diff, __shfl_xor_sync(0xffffffffu, diff, o));
+    if ((threadIdx.x & 31) == 0 && diff > 0.0)
+        atomicMax(&resid[k], (unsigned long long)__double_as_longlong(diff));
+}
+
+__global__ void k_fib_init(double *A, const uint8_t *__restrict__ freev, int HW, int NA, double v0) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i < (long long)HW * NA) A[i] = freev[i % HW] ? v0 : 0.0;
 }
 
 // ---- value iteration (fp64 Jacobi, reading R24) -----------------------------------------------
@@ -453,12 +531,12 @@ extern "C" void qvts_model_destroy(qvts_model *m) {
     cudaSetDevice(m->device);
     DevBuf *bufs[] = {&m->d_m8, &m->d_sig, &m->d_cell, &m->bu_R, &m->bu_P, &m->bu_cnt, &m->bu_umask,
                       &m->bu_U, &m->bu_off, &m->bu_path, &m->bu_root, &m->bu_key, &m->d_ctab, &m->d_R64, &m->d_O64, &m->d_O32, &m->d_gc_cell,
-                      &m->d_gc_act, &m->d_gc_val, &m->d_free, &m->d_V[0], &m->d_V[1], &m->d_resid,
+                      &m->d_gc_act, &m->d_gc_val, &m->d_free, &m->d_V[0], &m->d_V[1], &m->d_A[0], &m->d_A[1], &m->d_alpha64, &m->d_resid,
                       &m->d_Q64, &m->part, &m->tickets, &m->scan_tmp, &m->total, &m->counters, &m->vshard,
                       &m->ep_b[0], &m->ep_b[1], &m->ep_state, &m->ep_root_step, &m->ep_root_ep};
     for (DevBuf *b : bufs) b->release();
     for (BandSet *bs : {&m->band_big, &m->band_small}) {
-        bs->bands.release(); bs->entries.release(); bs->slot_cell.release(); bs->qlist.release();
+        bs->bands.release(); bs->entries.release(); bs->slot_cell.release(); bs->qlist.release(); bs->qlist_fib.release();
     }
     for (cudaEvent_t e : m->evpool) cudaEventDestroy(e);
     for (auto &v : m->vl) { v.path.release(); v.parent_q.release(); v.z.release(); v.f.release(); v.root.release(); v.V.release(); v.belief.release(); }
@@ -556,12 +634,83 @@ extern "C" qvts_status qvts_value_iteration(qvts_model *m, double eps, int32_t m
     for (int x = 0; x < HW; ++x)
         if (!m->occ[x]) { lo = std::min(lo, V[x]); hi = std::max(hi, V[x]); }
     m->qbar = std::isfinite(lo) ? 0.5 * (lo + hi) : 0.0;
-    QVTS_TRY(build_qlists(*m, st));
+    QVTS_TRY(build_qlists(*m, m->d_Q64.as<double>(), m->qbar, false, st));
     QVTS_CUDA(cudaStreamSynchronize(st));
     m->have_q = true;
     if (sweeps_out) *sweeps_out = last + 1;
     if (residual_out) *residual_out = resid;
     if (done < 0) { set_error("value iteration did not converge"); return QVTS_ERR_NOT_CONVERGED; }
+    return QVTS_OK;
+}
+
+extern "C" qvts_status qvts_fib_iteration(qvts_model *m, double eps, int32_t max_sweeps, int32_t *sweeps_out,
+                                          double *residual_out, void *stream) {
+    if (!m || !(eps > 0) || max_sweeps <= 0) { set_error("bad fib_iteration arguments"); return QVTS_ERR_INVALID_ARG; }
+    QVTS_CUDA(cudaSetDevice(m->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const int HW = m->HW, NA = m->NA;
+    const size_t nA = (size_t)NA * HW;
+    QVTS_TRY(m->d_A[0].ensure(sizeof(double) * nA));
+    QVTS_TRY(m->d_A[1].ensure(sizeof(double) * nA));
+    QVTS_TRY(m->d_alpha64.ensure(sizeof(double) * nA));
+    QVTS_TRY(m->d_resid.ensure(sizeof(unsigned long long) * (size_t)max_sweeps));
+    QVTS_CUDA(cudaMemsetAsync(m->d_resid.p, 0, sizeof(unsigned long long) * (size_t)max_sweeps, st));
+    double rmax = -INFINITY;
+    for (size_t i = 0; i < m->R64.size(); ++i)
+        if (!m->occ[i % HW]) rmax = std::max(rmax, m->R64[i]);
+    k_fib_init<<<(unsigned)((nA + 255) / 256), 256, 0, st>>>(m->d_A[0].as<double>(), m->d_free.as<uint8_t>(), HW, NA,
+                                                            rmax / (1.0 - m->gamma));
+    QVTS_CUDA(cudaGetLastError());
+    const int blk = 128, grid = (HW + blk - 1) / blk;
+    std::vector<unsigned long long> res(max_sweeps);
+    int done = -1, k = 0;
+    while (k < max_sweeps && done < 0) {
+        const int k1 = std::min(max_sweeps, k + 32);
+        for (int kk = k; kk < k1; ++kk) {
+#define QVTS_FIB_LAUNCH(MASK)                                                                                    \
+    k_fib_sweep<MASK><<<grid, blk, 0, st>>>(m->d_A[kk & 1].as<double>(), m->d_A[(kk + 1) & 1].as<double>(),       \
+                                            m->d_R64.as<double>(), m->d_m8.as<uint8_t>(), m->d_free.as<uint8_t>(), \
+                                            m->d_sig.as<uint8_t>(), m->d_O64.as<double>(), HW, m->W, m->p_int,     \
+                                            m->p_stay, m->p_lat, m->gamma, m->d_resid.as<unsigned long long>(), kk, eps)
+            QVTS_DISPATCH_MASK(m->mask, QVTS_FIB_LAUNCH);
+#undef QVTS_FIB_LAUNCH
+        }
+        QVTS_CUDA(cudaGetLastError());
+        QVTS_CUDA(cudaMemcpyAsync(res.data() + k, m->d_resid.as<unsigned long long>() + k,
+                                  sizeof(unsigned long long) * (k1 - k), cudaMemcpyDeviceToHost, st));
+        QVTS_CUDA(cudaStreamSynchronize(st));
+        for (int kk = k; kk < k1; ++kk) {
+            double r;
+            std::memcpy(&r, &res[kk], sizeof(double));
+            if (r < eps) { done = kk; break; }
+        }
+        k = k1;
+    }
+    const int last = done >= 0 ? done : max_sweeps - 1;
+    double resid;
+    std::memcpy(&resid, &res[last], sizeof(double));
+    QVTS_CUDA(cudaMemcpyAsync(m->d_alpha64.p, m->d_A[(last + 1) & 1].p, sizeof(double) * nA, cudaMemcpyDeviceToDevice, st));
+    std::vector<double> A(nA);
+    QVTS_CUDA(cudaMemcpyAsync(A.data(), m->d_alpha64.p, sizeof(double) * nA, cudaMemcpyDeviceToHost, st));
+    QVTS_CUDA(cudaStreamSynchronize(st));
+    double lo = INFINITY, hi = -INFINITY;
+    for (size_t i = 0; i < nA; ++i)
+        if (!m->occ[i % HW]) { lo = std::min(lo, A[i]); hi = std::max(hi, A[i]); }
+    m->qbar_fib = std::isfinite(lo) ? 0.5 * (lo + hi) : 0.0;
+    QVTS_TRY(build_qlists(*m, m->d_alpha64.as<double>(), m->qbar_fib, true, st));
+    QVTS_CUDA(cudaStreamSynchronize(st));
+    m->have_fib = true;
+    if (sweeps_out) *sweeps_out = last + 1;
+    if (residual_out) *residual_out = resid;
+    if (done < 0) { set_error("FIB iteration did not converge"); return QVTS_ERR_NOT_CONVERGED; }
+    return QVTS_OK;
+}
+
+extern "C" qvts_status qvts_get_alpha(const qvts_model *m, double *alpha_host) {
+    if (!m || !alpha_host) { set_error("NULL argument"); return QVTS_ERR_INVALID_ARG; }
+    if (!m->have_fib) { set_error("FIB iteration has not run"); return QVTS_ERR_STATE; }
+    QVTS_CUDA(cudaSetDevice(m->device));
+    QVTS_CUDA(cudaMemcpy(alpha_host, m->d_alpha64.p, sizeof(double) * (size_t)m->NA * m->HW, cudaMemcpyDeviceToHost));
     return QVTS_OK;
 }
 

@@ -818,7 +818,7 @@ static qvts_status launch_hist(Model &m, const BandSet &bs, const float *beliefs
     a.beliefs = beliefs; a.bstride = bstride; a.vmap = vmap; a.nwork = nwork;
     a.bands = bs.bands.as<BandInfo>(); a.nb = bs.nb;
     a.entries = bs.entries.as<uint32_t>();
-    a.qlist = bs.qlist.as<float4>();
+    a.qlist = (m.cur_leaf == QVTS_LEAF_FIB ? bs.qlist_fib : bs.qlist).as<float4>();
     a.H = m.H; a.W = m.W; a.TW = bs.tile_pitch;
     a.vec16 = ((m.W & 3) == 0 && (bstride & 3) == 0 && (reinterpret_cast<uintptr_t>(beliefs) & 15) == 0) ? 1 : 0;
     // second tile offset = 16 banks modulo 32, so the two half-warps never share a bank
@@ -896,6 +896,7 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
     constexpr int NA = mask_count(MASK);
     const int D = cfg.depth, n = cfg.n_samples;
     const bool trace = cfg.want_trace != 0;
+    m.cur_leaf = cfg.leaf_bound;
     const int G = (comm && comm->nranks > 1) ? comm->nranks : 1;
     const int rank = comm ? comm->rank : 0;
     const long long shard_min = (long long)std::max(1, comm ? comm->min_nodes_per_rank : 16) * G;
@@ -965,7 +966,8 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
             r.level = d; r.n = n; r.O64 = m.d_O64.as<double>();
             r.ngc = m.ngc; r.gc_cell = m.d_gc_cell.as<int32_t>(); r.gc_act = m.d_gc_act.as<int32_t>();
             r.gc_val = m.d_gc_val.as<double>(); r.goal = m.goal;
-            r.p_stay = m.p_stay; r.p_int = m.p_int; r.p_lat = m.p_lat; r.gamma = m.gamma; r.qbar = m.qbar;
+            r.p_stay = m.p_stay; r.p_int = m.p_int; r.p_lat = m.p_lat; r.gamma = m.gamma;
+            r.qbar = m.cur_leaf == QVTS_LEAF_FIB ? m.qbar_fib : m.qbar;
             r.R = ql.R.as<double>(); r.P = ql.P.as<double>(); r.cnt = ql.cnt.as<uint16_t>();
             r.umask = ql.umask.as<uint16_t>(); r.U = ql.U.as<int32_t>();
             r.zdraw = trace ? ql.zdraw.as<uint8_t>() : nullptr;
@@ -1160,6 +1162,8 @@ extern "C" qvts_status qvts_plan_step(qvts_model *m, const float *root_dev, cons
         set_error("bad comm"); return QVTS_ERR_INVALID_ARG;
     }
     if (!m->have_q) { set_error("run qvts_value_iteration before planning"); return QVTS_ERR_STATE; }
+    if (cfg->leaf_bound != QVTS_LEAF_QMDP && cfg->leaf_bound != QVTS_LEAF_FIB) { set_error("bad leaf_bound"); return QVTS_ERR_INVALID_ARG; }
+    if (cfg->leaf_bound == QVTS_LEAF_FIB && !m->have_fib) { set_error("run qvts_fib_iteration before FIB leaves"); return QVTS_ERR_STATE; }
     QVTS_CUDA(cudaSetDevice(m->device));
     cudaStream_t st = (cudaStream_t)stream;
     QVTS_TRY(m->ep_root_step.ensure(sizeof(uint32_t) * 2));

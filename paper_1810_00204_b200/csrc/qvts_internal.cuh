@@ -55,7 +55,7 @@ struct BandSet {
     long long total_slots = 0;
     std::vector<BandInfo> h_bands;
     std::vector<int32_t> h_slot_cell;
-    DevBuf bands, entries, slot_cell, qlist;
+    DevBuf bands, entries, slot_cell, qlist, qlist_fib;
 };
 
 // Per-level node arrays of the level-batched tree (SoA).
@@ -87,6 +87,11 @@ struct Model {
     bool have_q = false;
     double qbar = 0.0;
     DevBuf d_V[2], d_resid, d_Q64;
+    // Fast Informed Bound (NEXT-1)
+    bool have_fib = false;
+    double qbar_fib = 0.0;
+    DevBuf d_A[2], d_alpha64;
+    int cur_leaf = 0;                 // leaf alpha-set of the plan being built (qvts_leaf_bound)
     // plan workspace
     VLevel vl[kMaxLevels + 1];
     QLevel ql[kMaxLevels];
@@ -116,7 +121,7 @@ void prof_collect(Model &m);   // after a stream sync: fold recorded event pairs
 
 // model.cu
 qvts_status build_bands(Model &m, BandSet &bs, int rows);
-qvts_status build_qlists(Model &m, cudaStream_t st);
+qvts_status build_qlists(Model &m, const double *src64, double qbar, bool fib, cudaStream_t st);
 
 // plan.cu
 struct RootBatch {

@@ -23,8 +23,9 @@ EXPORTS = [
     "qvts_model_create", "qvts_model_destroy", "qvts_last_error", "qvts_model_info", "qvts_model_tables",
     "qvts_value_iteration", "qvts_get_q", "qvts_belief_update", "qvts_plan_step", "qvts_trace_qnodes",
     "qvts_trace_vnodes", "qvts_trace_leaf_values", "qvts_trace_belief", "qvts_run_episodes",
-    "qvts_trace_counts", "qvts_set_profiling", "qvts_get_profile",
+    "qvts_trace_counts", "qvts_set_profiling", "qvts_get_profile", "qvts_fib_iteration", "qvts_get_alpha",
 ]
+QVTS_LEAF_QMDP, QVTS_LEAF_FIB = 0, 1
 
 
 class QvtsError(RuntimeError):
@@ -42,7 +43,7 @@ class qvts_model_desc(C.Structure):
 
 class qvts_plan_cfg(C.Structure):
     _fields_ = [("depth", C.c_int32), ("n_samples", C.c_int32), ("seed", C.c_uint32), ("step", C.c_uint32),
-                ("episode", C.c_uint32), ("want_trace", C.c_int32)]
+                ("episode", C.c_uint32), ("want_trace", C.c_int32), ("leaf_bound", C.c_int32)]
 
 
 class qvts_plan_result(C.Structure):
@@ -100,6 +101,8 @@ def lib() -> C.CDLL:
         L.qvts_value_iteration.argtypes = [vp, C.c_double, C.c_int32, C.POINTER(C.c_int32),
                                            C.POINTER(C.c_double), vp]
         L.qvts_get_q.argtypes = [vp, vp]
+        L.qvts_fib_iteration.argtypes = [vp, C.c_double, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_double), vp]
+        L.qvts_get_alpha.argtypes = [vp, vp]
         L.qvts_belief_update.argtypes = [vp, vp, C.c_int32, C.c_int32, vp, C.POINTER(C.c_double), vp]
         L.qvts_plan_step.argtypes = [vp, vp, C.POINTER(qvts_plan_cfg), C.POINTER(qvts_comm),
                                      C.POINTER(qvts_plan_result), vp]
@@ -188,6 +191,20 @@ def qvts_get_q(h, n_actions, n_cells):
     return q
 
 
+def qvts_fib_iteration(h, eps=1e-9, max_sweeps=100000, stream=None):
+    sw, res = C.c_int32(), C.c_double()
+    code = lib().qvts_fib_iteration(h, eps, max_sweeps, C.byref(sw), C.byref(res), _stream(stream))
+    if code not in (QVTS_OK, 4):
+        _check(code, "qvts_fib_iteration")
+    return code, sw.value, res.value
+
+
+def qvts_get_alpha(h, n_actions, n_cells):
+    a = np.zeros((n_actions, n_cells), np.float64)
+    _check(lib().qvts_get_alpha(h, a.ctypes.data), "qvts_get_alpha")
+    return a
+
+
 def qvts_belief_update(h, b_dev, action, z, out_dev, stream=None):
     p = C.c_double()
     _check(lib().qvts_belief_update(h, _ptr(b_dev), int(action), int(z), _ptr(out_dev), C.byref(p),
@@ -196,8 +213,9 @@ def qvts_belief_update(h, b_dev, action, z, out_dev, stream=None):
 
 
 def qvts_plan_step(h, root_dev, depth, n_samples, seed=1, step=0, episode=0, want_trace=False, comm=None,
-                   stream=None) -> qvts_plan_result:
-    cfg = qvts_plan_cfg(int(depth), int(n_samples), int(seed), int(step), int(episode), 1 if want_trace else 0)
+                   stream=None, leaf_bound=QVTS_LEAF_QMDP) -> qvts_plan_result:
+    cfg = qvts_plan_cfg(int(depth), int(n_samples), int(seed), int(step), int(episode), 1 if want_trace else 0,
+                        int(leaf_bound))
     res = qvts_plan_result()
     _check(lib().qvts_plan_step(h, _ptr(root_dev), C.byref(cfg), C.byref(comm) if comm is not None else None,
                                 C.byref(res), _stream(stream)), "qvts_plan_step")
@@ -340,6 +358,12 @@ class Model:
 
     def q(self):
         return qvts_get_q(self.h, self.n_actions, self.n_cells)
+
+    def fib_iteration(self, eps=1e-9, max_sweeps=100000):
+        return qvts_fib_iteration(self.h, eps, max_sweeps)
+
+    def alpha(self):
+        return qvts_get_alpha(self.h, self.n_actions, self.n_cells)
 
     def tables(self):
         return qvts_model_tables(self.h, self.n_actions, self.n_cells)

@@ -247,3 +247,30 @@ def test_C4_full_size_sampled_parity(Q):
             s = sum((lc["f"][c] / n) * lc["V"][c] for c in range(off[qi], off[qi + 1]))
             assert abs(lq["R"][qi] + 0.95 * s - lq["Q"][qi]) <= 1e-9
     assert np.max(np.abs(np.array(res.q_root[:na]) - qlev[0]["Q"])) == 0.0
+
+
+@pytest.mark.parametrize("name", ["ragged", "paper"])
+def test_fib_alpha_and_fib_leaf_plan(Q, name):
+    """NEXT-1: FIB alpha-vectors (Eq. 7) against the oracle, then a plan step whose leaves use them."""
+    gm, mask = MAPS[name][0](), MAPS[name][1]
+    g, o, Qo, _, _ = pair(Q, gm, mask)
+    code, sweeps, res = g.fib_iteration(1e-9)
+    assert code == 0 and res < 1e-9
+    st, Ao, osw, ores = o.fib(1e-9)
+    assert st == O.OK and abs(sweeps - osw) <= 1
+    A = g.alpha()
+    assert np.max(np.abs(A - Ao)) <= 1e-7
+    free = gm.occupancy == 0
+    assert np.all(A[:, free] <= g.q()[:, free] + 1e-7)          # FIB no looser than Q_MDP
+    b32 = np.asarray(W.uniform_belief(gm), np.float32)
+    res = g.plan_step(dev(b32), 2, 8, seed=4, want_trace=True, leaf_bound=Q.QVTS_LEAF_FIB)
+    gq, gv, _, _ = PT.gpu_tree(g, 8)
+    ro = o.plan(Ao, b32.astype(np.float64), 2, 8, seed=4, trace=True)
+    oq, ov, _ = PT.oracle_tree(ro)
+    replay, _ = PT.draw_mismatches(gq, oq)
+    if replay:
+        ro = o.plan(Ao, b32.astype(np.float64), 2, 8, seed=4, trace=True, replay=replay)
+        oq, ov, _ = PT.oracle_tree(ro)
+    PT.compare_trees(gq, gv, oq, ov)
+    assert np.max(np.abs(np.array(res.q_root[:g.n_actions]) - ro.qroot)) <= PT.TOL
+    PT.check_action(res.action, ro.action, ro.qroot, g.action_ids)
