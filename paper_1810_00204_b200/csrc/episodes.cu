@@ -496,6 +496,7 @@ extern "C" qvts_status qvts_run_episodes(qvts_model *m, const qvts_episode_cfg *
         EP_CUDA(cudaGetLastError());
         EP_CUDA(cudaMemcpyAsync(&n_act, cnt.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
         EP_CUDA(cudaStreamSynchronize(st));
+        prof_collect(*m);               // fold this step's instrumentation events (if enabled)
     }
     EP_CUDA(cudaMemsetAsync(recbuf.p, 0, sizeof(double) * 6 * std::max(1, E), st));
     if (no > 0) k_records<<<(no + 127) / 128, 128, 0, st>>>(ea, recbuf.as<double>(), E);
