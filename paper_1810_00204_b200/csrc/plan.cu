@@ -385,6 +385,27 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_hist(HistArgs a) {
     }
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();
+    // Active-tile skipping: when both parents' bands (with halo) hold no
+    // belief mass, every accumulated value is exactly zero -- write zero partials, skip the work.
+    {
+        int any = 0;
+        for (int pp = 0; pp < 2; ++pp) {
+            const float4 *t4 = reinterpret_cast<const float4 *>(smem + pp * a.tstride);
+            for (int i = t; i < (TH * TP) / 4; i += kPairThreads) {
+                const float4 v = t4[i];
+                any |= (v.x != 0.f) | (v.y != 0.f) | (v.z != 0.f) | (v.w != 0.f);
+            }
+        }
+        if (!__syncthreads_or(any)) {
+            constexpr int NOUT0 = 16 * CB + 8;
+            for (int o = t; o < 2 * NOUT0; o += kPairThreads) {
+                const int pp = o / NOUT0, oo = o % NOUT0;
+                const long long wp = 2 * pair + pp;
+                if (wp < a.nwork) a.part[(wp * a.nb + band) * (long long)a.pstride + oo] = 0.0;
+            }
+            if (!a.cluster) return;
+        }
+    }
     const float *tile = smem + p * a.tstride;
 
     float acc[NV];
@@ -955,7 +976,7 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
             // summation order -- and every value -- is identical for any number of ranks
             double expect = 1.0;    // per root: the choice must not depend on batch or wave size either
             for (int i = 0; i < d; ++i) expect *= 10.0;
-            const BandSet &bs = expect < 1000.0 ? m.band_small : m.band_big;
+            const BandSet &bs = expect < 100.0 ? m.band_small : m.band_big;
             const int pstride = pstride_of<MASK>(leaf);
             QVTS_TRY(m.part.ensure(sizeof(double) * (size_t)(nwork + 1) * bs.nb * pstride));
             int nb_eff = bs.nb;
