@@ -185,9 +185,16 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one rank per GPU; QVTS_BENCH_BACKEND=gloo lets several ranks share a GPU to exercise the
+    # multi-rank path (the exchange is a host-side all-reduce, no kernel waits on another rank)
+    backend = os.environ.get("QVTS_BENCH_BACKEND", "nccl")
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     cpu_base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -237,10 +244,11 @@ def main():
     prof = Q.qvts_get_profile(model.h)
     Q.qvts_set_profiling(model.h, False)
     if world > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        tdev = "cuda" if backend == "nccl" else "cpu"
+        t = torch.tensor([ms], device=tdev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-        u = torch.tensor([float(local_tot)], device="cuda", dtype=torch.float64)
+        u = torch.tensor([float(local_tot)], device=tdev, dtype=torch.float64)
         dist.all_reduce(u, op=dist.ReduceOp.SUM)
         local_tot = u.item()
     total_updates = repl_tot + local_tot
@@ -261,10 +269,11 @@ def main():
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1)
     if world > 1:
-        t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+        tdev = "cuda" if backend == "nccl" else "cpu"
+        t = torch.tensor([e2e_ms], device=tdev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-        u = torch.tensor([float(e2e_loc)], device="cuda", dtype=torch.float64)
+        u = torch.tensor([float(e2e_loc)], device=tdev, dtype=torch.float64)
         dist.all_reduce(u, op=dist.ReduceOp.SUM)
         e2e_loc = u.item()
     e2e_value = (e2e_repl + e2e_loc) / (e2e_ms / 1e3)

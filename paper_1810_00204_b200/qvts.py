@@ -307,7 +307,12 @@ def make_torch_comm(min_nodes_per_rank=16):
             s = torch.cuda.ExternalStream(int(stream)) if stream else torch.cuda.current_stream()
             with torch.cuda.stream(s):
                 t = torch.as_tensor(_CudaArray(buf, count), device="cuda")
-                dist.all_reduce(t, op=dist.ReduceOp.SUM)
+                if dist.get_backend() == "nccl":
+                    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+                else:                                   # host backends (gloo): stage through host
+                    h = t.cpu()
+                    dist.all_reduce(h, op=dist.ReduceOp.SUM)
+                    t.copy_(h)
             return 0
         except Exception:  # noqa: BLE001 - surfaced as QVTS_ERR_COMM
             return 1
