@@ -120,12 +120,18 @@ QVTS_API qvts_status qvts_belief_update(qvts_model *model, const float *b_dev, i
  * Q_MDP leaves (Eq. 4, R14), backup Q = R + gamma sum (f/n) V, V = max_a Q (Alg. 6-7, R13),
  * action = argmax_a Q(root, a), ties to the lowest stencil id (R16/R18). */
 typedef enum { QVTS_LEAF_QMDP = 0, QVTS_LEAF_FIB = 1 } qvts_leaf_bound;
+/* Observation sampler: the marginal draw z ~ P(z|b,a) on Philox word 0 (reading R9, default), or
+ * Alg. 4 literally: x ~ b on word 1 (fp64 prefix sums over the grid),
+ * x' ~ T(x,a,.) on word 2 (clamped row in stencil order, blocked targets merged into the stay
+ * entry at first occurrence), z ~ O(x',.) on word 3. */
+typedef enum { QVTS_SAMPLER_MARGINAL = 0, QVTS_SAMPLER_ANCESTRAL = 1 } qvts_sampler;
 typedef struct {
     int32_t depth;        /* number of action levels D, 1..8 (reading R15)                       */
     int32_t n_samples;    /* observations drawn per Q-node, 1..4096                               */
     uint32_t seed, step, episode;
     int32_t want_trace;   /* 1: keep per-node draws for qvts_trace_* (costs memory)               */
     int32_t leaf_bound;   /* qvts_leaf_bound: Q_MDP (north star, R14) or FIB (needs qvts_fib_iteration) */
+    int32_t sampler;      /* qvts_sampler                                                          */
 } qvts_plan_cfg;
 
 typedef struct {

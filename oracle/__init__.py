@@ -18,6 +18,7 @@ _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 OK, ERR_INVALID_ARG, ERR_INVALID_MODEL, ERR_NOT_CONVERGED, ERR_ZERO_LIKELIHOOD = 0, 1, 2, 4, 5
 MODE_FREQ, MODE_EXACT, MODE_BRUTE = 0, 1, 2
 PLANNER_QVTS, PLANNER_MDP, PLANNER_ASTAR = 0, 1, 2
+SAMPLER_MARGINAL, SAMPLER_ANCESTRAL = 0, 1
 
 
 def build() -> str:
@@ -50,8 +51,8 @@ _u32p = np.ctypeslib.ndpointer(dtype=np.uint32, flags="C_CONTIGUOUS")
 class PlanCfg(C.Structure):
     _fields_ = [("depth", C.c_int), ("n_samples", C.c_int), ("mode", C.c_int), ("threads", C.c_int),
                 ("seed", C.c_uint32), ("step", C.c_uint32), ("episode", C.c_uint32),
-                ("n_replay", C.c_int), ("replay_path", C.c_void_p), ("replay_j", C.c_void_p),
-                ("replay_z", C.c_void_p)]
+                ("sampler", C.c_int), ("n_replay", C.c_int), ("replay_path", C.c_void_p),
+                ("replay_j", C.c_void_p), ("replay_z", C.c_void_p)]
 
 
 class EpisodeCfg(C.Structure):
@@ -286,8 +287,8 @@ class Model:
 
     # -- plan step --
     @staticmethod
-    def _cfg(depth, n, seed, step, episode, mode, threads, replay):
-        cfg = PlanCfg(depth, n, mode, threads, seed, step, episode, 0, None, None, None)
+    def _cfg(depth, n, seed, step, episode, mode, threads, replay, sampler=0):
+        cfg = PlanCfg(depth, n, mode, threads, seed, step, episode, sampler, 0, None, None, None)
         keep = None
         if replay:
             rp = np.array([r[0] for r in replay], dtype=np.uint64)
@@ -301,9 +302,9 @@ class Model:
         return cfg, keep
 
     def plan(self, Q, b0, depth, n, seed=1, step=0, episode=0, mode=MODE_FREQ, trace=False,
-             capture_beliefs=False, threads=0, replay=None) -> PlanResult:
+             capture_beliefs=False, threads=0, replay=None, sampler=0) -> PlanResult:
         L = lib()
-        cfg, _keep = self._cfg(depth, n, seed, step, episode, mode, threads, replay)
+        cfg, _keep = self._cfg(depth, n, seed, step, episode, mode, threads, replay, sampler)
         tr = L.or_trace_new(1 if capture_beliefs else 0) if trace else None
         act = C.c_int(0)
         qroot = np.zeros(self.na)
@@ -341,8 +342,8 @@ class Model:
                      qz[:nq * ns].reshape(nq, ns), qf[:nq * ns].reshape(nq, ns),
                      vp, vl, vV, vz, vf, bel)
 
-    def qnode_sample(self, b, a, qpath, n, seed=1, step=0, episode=0):
-        cfg, _ = self._cfg(0, n, seed, step, episode, MODE_FREQ, 1, None)
+    def qnode_sample(self, b, a, qpath, n, seed=1, step=0, episode=0, sampler=0):
+        cfg, _ = self._cfg(0, n, seed, step, episode, MODE_FREQ, 1, None, sampler)
         P = np.zeros(16); R = C.c_double(0)
         z = np.zeros(n, np.uint8); f = np.zeros(n, np.uint8); cnt = np.zeros(16, np.uint16)
         lib().or_qnode_sample(self._h, np.ascontiguousarray(b, dtype=np.float64), a, int(qpath),

@@ -505,8 +505,20 @@ static int replay_lookup(const or_plan_cfg *cfg, uint64_t qpath, int j, int *z) 
 }
 
 /* Draws of one Q-node (Appendix A.2-A.6); returns the draws, flags and counts. */
-static void qnode_draws(const or_plan_cfg *cfg, int nz, const double *P, uint64_t qpath,
-                        uint8_t *zs, uint8_t *flags, uint16_t *cnt) {
+/* Alg. 4 literal: x ~ b (word 1), x' ~ T(x,a,.) over the clamped row in its
+ * stored order (word 2), z ~ O(x',.) (word 3).  Only the state draw can be near a CDF boundary
+ * (the other two CDFs are exact model tables), so *flag reports that draw (A.6 rule). */
+static int ancestral_draw(const or_model *m, const double *b, int a, const uint32_t w[4], int *flag) {
+    int x = or_inverse_cdf(b, m->nx, or_uniform(w[1]), flag);
+    int e0 = m->t_start[x * m->na + a], e1 = m->t_start[x * m->na + a + 1];
+    double p[9];
+    for (int e = e0; e < e1; ++e) p[e - e0] = m->t_p[e];
+    int xp = m->t_y[e0 + or_inverse_cdf(p, e1 - e0, or_uniform(w[2]), NULL)];
+    return or_inverse_cdf(&m->O[xp * m->nz], m->nz, or_uniform(w[3]), NULL);
+}
+
+static void qnode_draws(const or_model *m, const double *b, int a, const or_plan_cfg *cfg, int nz,
+                        const double *P, uint64_t qpath, uint8_t *zs, uint8_t *flags, uint16_t *cnt) {
     double C[16];
     double s = 0.0;
     for (int k = 0; k < nz; ++k) { s += P[k]; C[k] = s; cnt[k] = 0; }
@@ -514,6 +526,15 @@ static void qnode_draws(const or_plan_cfg *cfg, int nz, const double *P, uint64_
         uint32_t ctr[4] = {(uint32_t)j, (uint32_t)qpath, (uint32_t)(qpath >> 32), cfg->step};
         uint32_t key[2] = {cfg->seed, cfg->episode}, w[4];
         or_philox4x32_10(ctr, key, w);
+        if (cfg->sampler == OR_SAMPLER_ANCESTRAL) {
+            int flag, zr, z = ancestral_draw(m, b, a, w, &flag);
+            /* a flagged state draw may land in the neighbouring state: replay the GPU's z */
+            if (flag && cfg->n_replay > 0 && replay_lookup(cfg, qpath, j, &zr)) z = zr;
+            zs[j] = (uint8_t)z;
+            flags[j] = (uint8_t)flag;
+            cnt[z]++;
+            continue;
+        }
         double u = or_uniform(w[0]);
         int flag;
         int z = or_inverse_cdf(P, nz, u, &flag);
@@ -551,7 +572,7 @@ static double qnode_rec(plan_ctx *c, const double *b, int a, uint64_t qpath, int
     or_marginal(m, bbar, P);                              /* P(z|b,a)       */
     double R = or_belief_reward(m, b, a);                 /* R(b,a)         */
     if (cfg->mode == OR_MODE_BRUTE) { for (int z = 0; z < nz; ++z) cnt[z] = 0; }
-    else qnode_draws(cfg, nz, P, qpath, zs, flags, cnt);  /* Alg. 3 l.4-5   */
+    else qnode_draws(m, b, a, cfg, nz, P, qpath, zs, flags, cnt);  /* Alg. 3 l.4-5 */
     double acc = 0.0;
     for (int z = 0; z < nz; ++z) {                        /* unique z ascending (R17) */
         int take = (cfg->mode == OR_MODE_BRUTE) ? (P[z] > OR_ZERO_LIK) : (cnt[z] > 0);
@@ -644,7 +665,7 @@ int or_qnode_sample(const or_model *m, const double *b, int a, uint64_t qpath, c
     or_predict(m, b, a, bbar);
     or_marginal(m, bbar, P);
     *R = or_belief_reward(m, b, a);
-    qnode_draws(cfg, m->nz, P, qpath, z, flag, cnt);
+    qnode_draws(m, b, a, cfg, m->nz, P, qpath, z, flag, cnt);
     free(bbar);
     return OR_OK;
 }

@@ -65,9 +65,12 @@ double or_qmdp_value(const or_model *m, const double *Q, const double *b, int *a
 
 /* ---- plan step (Alg. 1-7 read per SURVEY §8(c) O6) ---- */
 enum { OR_MODE_FREQ = 0, OR_MODE_EXACT = 1, OR_MODE_BRUTE = 2 };
+enum { OR_SAMPLER_MARGINAL = 0, OR_SAMPLER_ANCESTRAL = 1 };
 typedef struct {
     int depth, n_samples, mode, threads;
     uint32_t seed, step, episode;
+    int sampler;   /* OR_SAMPLER_MARGINAL (reading R9, Philox word 0) or OR_SAMPLER_ANCESTRAL
+                      (Alg. 4 literal: x ~ b, x' ~ T(x,a,.), z ~ O(x',.) with words 1..3) */
     /* replay table for flagged, mismatched draws (SURVEY c.5 step 3) */
     int n_replay;
     const uint64_t *replay_path;

@@ -458,7 +458,7 @@ extern "C" qvts_status qvts_run_episodes(qvts_model *m, const qvts_episode_cfg *
             RootBatch rb{bel[cur].as<float>(), (long long)m->HWp, (long long)no, root_step, root_ep, act_w, nw};
             m->cur_leaf = QVTS_LEAF_QMDP;
             if (cfg->planner == QVTS_PLANNER_QVTS) {
-                qvts_plan_cfg pc{cfg->depth, cfg->n_samples, cfg->seed, 0u, 0u, 0, QVTS_LEAF_QMDP};
+                qvts_plan_cfg pc{cfg->depth, cfg->n_samples, cfg->seed, 0u, 0u, 0, QVTS_LEAF_QMDP, QVTS_SAMPLER_MARGINAL};
                 long long nv[kMaxLevels + 1];
                 EP_TRY(plan_levels(*m, rb, pc, nullptr, st, nv));
                 k_pick_qvts<<<(nw + 127) / 128, 128, 0, st>>>(ea, act_w, nw, m->ql[0].Q.as<double>(), NA,

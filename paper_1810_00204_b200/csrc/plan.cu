@@ -76,7 +76,53 @@ struct ReduceArgs {
     uint8_t *zdraw;
     double *Q, *leafV;
     unsigned long long *counters;   // [0] flagged draws, [1] leaf V-nodes
+    // ancestral sampler (NEXT-3): state draws x[q][j] and the tables for x' and z
+    const int32_t *xs;
+    const uint8_t *m8, *sig;
+    int W;
+    double acc;
 };
+
+// Alg. 4 steps 2-3 for one sample: x' ~ T(x,a,.) on u2 over the clamped row in stencil order
+// (blocked targets merged into the stay entry at first occurrence), then z ~ O(x',.) on u3
+// (product over the 4 independent sensors, R7); fp64 CDFs, min{k : u C_last < C_k} (A.5).
+__device__ __forceinline__ int ancestral_tail(const ReduceArgs &a, int x, int k, double u2, double u3) {
+    int ty[4];
+    double tp[4];
+    int nt = 0;
+    const int m8 = a.m8[x];
+    for (int kk = 0; kk < 9; ++kk) {
+        double w = 0.0;
+        if (k == 4) w = (kk == 4) ? 1.0 : 0.0;
+        else if (kk == k) w = a.p_int;
+        else if (kk == 4) w = a.p_stay;
+        else if (kk == lat1(k) || kk == lat2(k)) w = a.p_lat;
+        if (w == 0.0) continue;
+        int y = x;
+        if (kk != 4 && !((m8 >> nbit(kk)) & 1)) y = x + st_dr(kk) * a.W + st_dc(kk);
+        int found = -1;
+        for (int e = 0; e < nt; ++e) if (ty[e] == y) found = e;
+        if (found >= 0) tp[found] += w;
+        else { ty[nt] = y; tp[nt] = w; ++nt; }
+    }
+    double C[4], acc = 0.0;
+    for (int e = 0; e < nt; ++e) { acc += tp[e]; C[e] = acc; }
+    double t = u2 * C[nt - 1];
+    int xp = ty[nt - 1];
+    for (int e = 0; e < nt; ++e) if (t < C[e]) { xp = ty[e]; break; }
+    const int sg = a.sig[xp];
+    double Cz[16];
+    acc = 0.0;
+    for (int z = 0; z < 16; ++z) {
+        double o = 1.0;
+        for (int bb = 0; bb < 4; ++bb) o *= (((z >> bb) & 1) == ((sg >> bb) & 1)) ? a.acc : (1.0 - a.acc);
+        acc += o;
+        Cz[z] = acc;
+    }
+    t = u3 * Cz[15];
+    for (int z = 0; z < 16; ++z) if (t < Cz[z]) return z;
+    return 15;
+}
 
 // One CTA per parent V-node, one warp per action (Q-node).  The CTA first sums the parent's band
 // partials into shared memory (coalesced, fixed band order, fp64); then each warp: per-action
@@ -195,17 +241,21 @@ __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int
         if (jj < a.n) {
             const uint4 r = philox4x32_10(make_uint4((uint32_t)jj, (uint32_t)qpath, (uint32_t)(qpath >> 32), step),
                                           make_uint2(a.seed, ep));
-            const double u = philox_uniform(r.x);
-            const double tt = u * C[15];
-            z = 0;
-            double gap = INFINITY;
+            if (a.xs) {            // Alg. 4 literal: x drawn by k_ancestral_x, then x' and z
+                z = ancestral_tail(a, a.xs[q * a.n + jj], k, philox_uniform(r.z), philox_uniform(r.w));
+            } else {
+                const double u = philox_uniform(r.x);
+                const double tt = u * C[15];
+                z = 0;
+                double gap = INFINITY;
 #pragma unroll
-            for (int kk = 0; kk < 16; ++kk) {
-                z += (C[kk] <= tt) ? 1 : 0;
-                if (kk < 15) gap = fmin(gap, fabs(tt - C[kk]));
+                for (int kk = 0; kk < 16; ++kk) {
+                    z += (C[kk] <= tt) ? 1 : 0;
+                    if (kk < 15) gap = fmin(gap, fabs(tt - C[kk]));
+                }
+                z = min(z, 15);
+                nflag += gap < 1e-6 ? 1 : 0;
             }
-            z = min(z, 15);
-            nflag += gap < 1e-6 ? 1 : 0;
             if (a.zdraw) a.zdraw[q * a.n + jj] = (uint8_t)z;
         }
 #pragma unroll
@@ -291,6 +341,74 @@ template <uint32_t MASK, bool LEAF>
 __global__ void __launch_bounds__(mask_count(MASK) * 32) k_reduce(ReduceArgs a) {
     extern __shared__ double rsm[];
     reduce_parent<MASK, LEAF>(a, blockIdx.x, rsm, mask_count(MASK) * 32);
+}
+
+// ---- NEXT-3: the state draw x ~ b of Alg. 4 for every sample of every Q-node of a parent ------
+// One CTA per parent: fp64 sums of 256-cell chunks (warp per chunk, fixed order), their exclusive
+// prefix, then per (action, sample) target t = u1 * C_total: the chunk by binary search and the
+// cell by a sequential fp64 scan inside it, min{x : t < C_x} (A.5; zero-mass cells never drawn).
+template <uint32_t MASK>
+__global__ void __launch_bounds__(256) k_ancestral_x(const float *__restrict__ beliefs, long long bstride,
+                                                     const int32_t *vmap, long long nwork, int HW,
+                                                     const uint64_t *vpath, const int32_t *vroot,
+                                                     const uint32_t *root_step, const uint32_t *root_ep,
+                                                     uint32_t seed, int level, int n, int32_t *xs) {
+    constexpr int NA = mask_count(MASK);
+    constexpr int CH = 256;
+    extern __shared__ double sx[];   // [nch] chunk sums, then exclusive prefix in place
+    const long long w = blockIdx.x;
+    const long long v = vmap ? (long long)vmap[w] : w;
+    const float *__restrict__ b = beliefs + v * bstride;
+    const int nch = (HW + CH - 1) / CH;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double *csum = sx, *cpre = sx + nch;
+    for (int c = warp; c < nch; c += 8) {
+        double s = 0.0;
+        for (int i = lane; i < CH; i += 32) {
+            const int x = c * CH + i;
+            if (x < HW) s += (double)b[x];
+        }
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) csum[c] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double acc = 0.0;
+        for (int c = 0; c < nch; ++c) { cpre[c] = acc; acc += csum[c]; }
+        cpre[nch] = acc;
+    }
+    __syncthreads();
+    const double total = cpre[nch];
+    const uint64_t vp = vpath[v];
+    const int root = vroot[v];
+    const uint32_t step = root_step[root], ep = root_ep[root];
+    for (int idx = threadIdx.x; idx < NA * n; idx += 256) {
+        const int j = idx / n, s = idx % n;
+        int kk = 0;
+#pragma unroll
+        for (int i = 0; i < NA; ++i) if (i == j) kk = mask_action(MASK, i);
+        const uint64_t qpath = vp | ((uint64_t)(kk + 1) << (8 * level));
+        const uint4 r = philox4x32_10(make_uint4((uint32_t)s, (uint32_t)qpath, (uint32_t)(qpath >> 32), step),
+                                      make_uint2(seed, ep));
+        const double t = philox_uniform(r.y) * total;
+        int lo = 0, hi = nch - 1;                   // first chunk whose end exceeds t
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (t < cpre[mid + 1]) hi = mid; else lo = mid + 1;
+        }
+        double acc = cpre[lo];
+        int xsel = -1, last = -1;
+        for (int i = 0; i < CH; ++i) {
+            const int x = lo * CH + i;
+            if (x >= HW) break;
+            const double bv = (double)b[x];
+            acc += bv;
+            if (bv > 0.0) last = x;
+            if (t < acc) { xsel = x; break; }
+        }
+        if (xsel < 0) xsel = last >= 0 ? last : lo * CH;   // rounding at the very end of a chunk
+        xs[((long long)w * NA + j) * n + s] = xsel;
+    }
 }
 
 // ---- S1 + S2 (+ S5): signature-binned histograms ----------------------------------------------
@@ -994,9 +1112,20 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
             r.zdraw = trace ? ql.zdraw.as<uint8_t>() : nullptr;
             r.Q = ql.Q.as<double>(); r.leafV = (trace && leaf) ? ql.leafV.as<double>() : nullptr;
             r.counters = m.counters.as<unsigned long long>();
+            r.xs = nullptr; r.m8 = m.d_m8.as<uint8_t>(); r.sig = m.d_sig.as<uint8_t>(); r.W = m.W; r.acc = m.acc;
+            if (cfg.sampler == QVTS_SAMPLER_ANCESTRAL) {
+                QVTS_TRY(m.xs.ensure(sizeof(int32_t) * (size_t)nq * n));
+                const int nch = (m.HW + 255) / 256;
+                QVTS_PROF(7, k_ancestral_x<MASK><<<(unsigned)nwork, 256, sizeof(double) * (2 * nch + 1), st>>>(
+                                 bel, bstride, vmap, nwork, m.HW, vl.path.as<uint64_t>(), vl.root.as<int32_t>(),
+                                 roots.step_dev, roots.episode_dev, cfg.seed, d, n, m.xs.as<int32_t>()));
+                QVTS_CUDA(cudaGetLastError());
+                r.xs = m.xs.as<int32_t>();
+            }
             bool fused = false;
-            if (leaf) QVTS_TRY((launch_hist<MASK, true>(m, bs, bel, bstride, vmap, nwork, pstride, st, &nb_eff, &r, &fused)));
-            else QVTS_TRY((launch_hist<MASK, false>(m, bs, bel, bstride, vmap, nwork, pstride, st, &nb_eff, &r, &fused)));
+            const ReduceArgs *rf = r.xs ? nullptr : &r;   // the fused reduce has no x draws
+            if (leaf) QVTS_TRY((launch_hist<MASK, true>(m, bs, bel, bstride, vmap, nwork, pstride, st, &nb_eff, rf, &fused)));
+            else QVTS_TRY((launch_hist<MASK, false>(m, bs, bel, bstride, vmap, nwork, pstride, st, &nb_eff, rf, &fused)));
             r.nb = nb_eff;
             if (!fused) {
             if (leaf) QVTS_TRY((launch_reduce<MASK, true>(m, r, st)));
@@ -1185,6 +1314,7 @@ extern "C" qvts_status qvts_plan_step(qvts_model *m, const float *root_dev, cons
     if (!m->have_q) { set_error("run qvts_value_iteration before planning"); return QVTS_ERR_STATE; }
     if (cfg->leaf_bound != QVTS_LEAF_QMDP && cfg->leaf_bound != QVTS_LEAF_FIB) { set_error("bad leaf_bound"); return QVTS_ERR_INVALID_ARG; }
     if (cfg->leaf_bound == QVTS_LEAF_FIB && !m->have_fib) { set_error("run qvts_fib_iteration before FIB leaves"); return QVTS_ERR_STATE; }
+    if (cfg->sampler != QVTS_SAMPLER_MARGINAL && cfg->sampler != QVTS_SAMPLER_ANCESTRAL) { set_error("bad sampler"); return QVTS_ERR_INVALID_ARG; }
     QVTS_CUDA(cudaSetDevice(m->device));
     cudaStream_t st = (cudaStream_t)stream;
     QVTS_TRY(m->ep_root_step.ensure(sizeof(uint32_t) * 2));

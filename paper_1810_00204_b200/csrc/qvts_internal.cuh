@@ -95,7 +95,7 @@ struct Model {
     // plan workspace
     VLevel vl[kMaxLevels + 1];
     QLevel ql[kMaxLevels];
-    DevBuf part, scan_tmp, total, counters, vshard, tickets;
+    DevBuf part, scan_tmp, total, counters, vshard, tickets, xs;
     int last_depth = -1, last_n = 0, last_shard_level = -1;
     long long last_flagged = 0;
     bool last_trace = false;

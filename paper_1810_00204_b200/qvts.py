@@ -26,6 +26,7 @@ EXPORTS = [
     "qvts_trace_counts", "qvts_set_profiling", "qvts_get_profile", "qvts_fib_iteration", "qvts_get_alpha",
 ]
 QVTS_LEAF_QMDP, QVTS_LEAF_FIB = 0, 1
+QVTS_SAMPLER_MARGINAL, QVTS_SAMPLER_ANCESTRAL = 0, 1
 
 
 class QvtsError(RuntimeError):
@@ -43,7 +44,8 @@ class qvts_model_desc(C.Structure):
 
 class qvts_plan_cfg(C.Structure):
     _fields_ = [("depth", C.c_int32), ("n_samples", C.c_int32), ("seed", C.c_uint32), ("step", C.c_uint32),
-                ("episode", C.c_uint32), ("want_trace", C.c_int32), ("leaf_bound", C.c_int32)]
+                ("episode", C.c_uint32), ("want_trace", C.c_int32), ("leaf_bound", C.c_int32),
+                ("sampler", C.c_int32)]
 
 
 class qvts_plan_result(C.Structure):
@@ -213,9 +215,9 @@ def qvts_belief_update(h, b_dev, action, z, out_dev, stream=None):
 
 
 def qvts_plan_step(h, root_dev, depth, n_samples, seed=1, step=0, episode=0, want_trace=False, comm=None,
-                   stream=None, leaf_bound=QVTS_LEAF_QMDP) -> qvts_plan_result:
+                   stream=None, leaf_bound=QVTS_LEAF_QMDP, sampler=QVTS_SAMPLER_MARGINAL) -> qvts_plan_result:
     cfg = qvts_plan_cfg(int(depth), int(n_samples), int(seed), int(step), int(episode), 1 if want_trace else 0,
-                        int(leaf_bound))
+                        int(leaf_bound), int(sampler))
     res = qvts_plan_result()
     _check(lib().qvts_plan_step(h, _ptr(root_dev), C.byref(cfg), C.byref(comm) if comm is not None else None,
                                 C.byref(res), _stream(stream)), "qvts_plan_step")

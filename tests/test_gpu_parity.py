@@ -87,18 +87,18 @@ def test_belief_update_zero_likelihood(Q):
     assert e.value.code == 5
 
 
-def run_parity(Q, gm, mask, depth, n, b0, seed=1, step=0, episode=0, beliefs=True):
+def run_parity(Q, gm, mask, depth, n, b0, seed=1, step=0, episode=0, beliefs=True, sampler=0):
     g, o, Qo, _, _ = pair(Q, gm, mask)
     b32 = np.asarray(b0, np.float32)
-    res = g.plan_step(dev(b32), depth, n, seed=seed, step=step, episode=episode, want_trace=True)
+    res = g.plan_step(dev(b32), depth, n, seed=seed, step=step, episode=episode, want_trace=True, sampler=sampler)
     gq, gv, gbel, _ = PT.gpu_tree(g, n, with_beliefs=beliefs)
     ores = o.plan(Qo, b32.astype(np.float64), depth, n, seed=seed, step=step, episode=episode, trace=True,
-                  capture_beliefs=beliefs)
+                  capture_beliefs=beliefs, sampler=sampler)
     oq, ov, obel = PT.oracle_tree(ores)
     replay, nmis = PT.draw_mismatches(gq, oq)
     if replay:   # flagged draws decided differently: replay the GPU's decision in the oracle
         ores = o.plan(Qo, b32.astype(np.float64), depth, n, seed=seed, step=step, episode=episode, trace=True,
-                      capture_beliefs=beliefs, replay=replay)
+                      capture_beliefs=beliefs, replay=replay, sampler=sampler)
         oq, ov, obel = PT.oracle_tree(ores)
         PT.draw_mismatches(gq, oq)
     err = PT.compare_trees(gq, gv, oq, ov, gbel if beliefs else None, obel if beliefs else None)
@@ -274,3 +274,11 @@ def test_fib_alpha_and_fib_leaf_plan(Q, name):
     PT.compare_trees(gq, gv, oq, ov)
     assert np.max(np.abs(np.array(res.q_root[:g.n_actions]) - ro.qroot)) <= PT.TOL
     PT.check_action(res.action, ro.action, ro.qroot, g.action_ids)
+
+
+@pytest.mark.parametrize("name,depth,n", [("C1", 2, 4), ("ragged", 3, 8), ("paper", 2, 16)])
+def test_plan_ancestral_sampler(Q, name, depth, n):
+    """NEXT-3: Alg. 4 literally (x ~ b, x' ~ T, z ~ O on Philox words 1..3) on the GPU."""
+    gm, mask = MAPS[name][0](), MAPS[name][1]
+    res, err, nmis = run_parity(Q, gm, mask, depth, n, W.random_belief(gm, 8), seed=3, step=1,
+                                beliefs=(name != "paper"), sampler=Q.QVTS_SAMPLER_ANCESTRAL)

@@ -464,3 +464,17 @@ def test_fib_constant_reward_and_bounds_on_grid():
     # FIB is an upper bound no looser than Q_MDP (the max over a' moved inside the z-sum)
     assert np.all(alpha[:, free] <= Q[:, free] + 1e-9)
     assert np.any(alpha[:, free] < Q[:, free] - 1e-3)
+
+
+# ---- NEXT-3: Alg. 4 literal (ancestral) sampler inside the plan ------------------------------
+def test_ancestral_sampler_in_plan_matches_alg4_and_marginal():
+    gm = W.random_map(8, 9, 0.2, seed=4)
+    m = O.Model.grid(gm, action_mask=W.A8, acc=0.85)
+    b = W.random_belief(gm, 6)
+    qpath = 0x27
+    P, R, z, flag, cnt = m.qnode_sample(b, 3, qpath, 40000, seed=5, step=2, sampler=O.SAMPLER_ANCESTRAL)
+    for j in range(0, 40000, 997):   # each draw is Alg. 4 on Philox words 1..3 of its counter
+        assert z[j] == m.ancestral_sample(b, 3, [j, qpath, 0, 2], [5, 0])
+    n = 40000
+    sd = np.sqrt(n * P * (1 - P))
+    assert np.all(np.abs(cnt - n * P) <= 5 * sd + 1)      # distribution = the marginal P(z|b,a)

@@ -43,6 +43,10 @@ for leaf in (Q.QVTS_LEAF_QMDP, Q.QVTS_LEAF_FIB):
     dt, r = timed(lambda: m.plan_step(b, 4, 16, seed=1, step=1, leaf_bound=leaf), reps=3)
     out[f"plan_C4_leaf_{'fib' if leaf else 'qmdp'}"] = {"ms": dt * 1e3, "updates": r.n_belief_updates,
                                                          "updates_per_s": r.n_belief_updates / dt}
+m.plan_step(b, 4, 16, seed=1, step=0, sampler=Q.QVTS_SAMPLER_ANCESTRAL)
+dt, r = timed(lambda: m.plan_step(b, 4, 16, seed=1, step=1, sampler=Q.QVTS_SAMPLER_ANCESTRAL), reps=3)
+out["NEXT3_plan_C4_ancestral_sampler"] = {"ms": dt * 1e3, "updates": r.n_belief_updates,
+                                          "updates_per_s": r.n_belief_updates / dt}
 m.close()
 
 E = int(os.environ.get("EPISODES", "128"))
