@@ -100,6 +100,15 @@ def _declare(L):
     L.or_value_iteration.argtypes = [vp, C.c_double, C.c_int, _dp, _dp, C.POINTER(C.c_int),
                                      C.POINTER(C.c_double)]
     L.or_fib.argtypes = [vp, C.c_double, C.c_int, _dp, C.POINTER(C.c_int), C.POINTER(C.c_double)]
+    L.or_pbvi_build.restype = vp
+    L.or_pbvi_build.argtypes = [vp, _dp, C.c_int, C.c_int, C.c_uint32, C.c_int]
+    L.or_pbvi_free.argtypes = [vp]
+    L.or_pbvi_npoints.argtypes = [vp]
+    L.or_pbvi_nalpha.argtypes = [vp]
+    L.or_pbvi_point.argtypes = [vp, C.c_int, _dp]
+    L.or_pbvi_alpha.argtypes = [vp, C.c_int, _dp, C.POINTER(C.c_int)]
+    L.or_pbvi_value.restype = C.c_double
+    L.or_pbvi_value.argtypes = [vp, _dp]
     L.or_qmdp_value.restype = C.c_double
     L.or_qmdp_value.argtypes = [vp, _dp, _dp, C.POINTER(C.c_int)]
     L.or_trace_new.restype = vp
@@ -278,6 +287,23 @@ class Model:
         it, res = C.c_int(0), C.c_double(0)
         st = lib().or_fib(self._h, eps, max_iter, alpha, C.byref(it), C.byref(res))
         return st, alpha.reshape(self.na, self.nx), it.value, res.value
+
+    def pbvi(self, b0, expansions=3, max_points=16, seed=1, sweeps=30):
+        """PBVI lower bound: returns (points [nb][nx], alphas [n][nx], alpha actions)."""
+        L = lib()
+        h = L.or_pbvi_build(self._h, np.ascontiguousarray(b0, dtype=np.float64), expansions, max_points, seed, sweeps)
+        nb, nal = L.or_pbvi_npoints(h), L.or_pbvi_nalpha(h)
+        pts = np.zeros((nb, self.nx))
+        for i in range(nb):
+            L.or_pbvi_point(h, i, pts[i])
+        al = np.zeros((nal, self.nx))
+        acts = np.zeros(nal, np.int32)
+        for i in range(nal):
+            a = C.c_int(0)
+            L.or_pbvi_alpha(h, i, al[i], C.byref(a))
+            acts[i] = a.value
+        L.or_pbvi_free(h)
+        return pts, al, acts
 
     def qmdp_value(self, Q, b):
         arg = C.c_int(0)

@@ -391,6 +391,143 @@ int or_fib(const or_model *m, double eps, int max_iter, double *alpha, int *iter
     return st;
 }
 
+/* ---- PBVI (§IV-B) ------------------------------------------------------------------------------ */
+static int ancestral_draw(const or_model *m, const double *b, int a, const uint32_t w[4], int *flag);
+struct or_pbvi {
+    int nx, nb, na_alpha;
+    double *B;        /* [nb][nx] */
+    double *G;        /* [na_alpha][nx] */
+    int *gact;
+};
+
+/* b . g_{a,z}^alpha = sum_x b(x) sum_x' O(x',z) T(x,a,x') alpha(x') (scatter over T rows) */
+static double pbvi_dot(const or_model *m, const double *b, int a, int z, const double *alpha) {
+    double s = 0.0;
+    for (int x = 0; x < m->nx; ++x) {
+        if (b[x] == 0.0) continue;
+        double g = 0.0;
+        for (int e = m->t_start[x * m->na + a]; e < m->t_start[x * m->na + a + 1]; ++e) {
+            int y = m->t_y[e];
+            g += m->O[y * m->nz + z] * m->t_p[e] * alpha[y];
+        }
+        s += b[x] * g;
+    }
+    return s;
+}
+
+or_pbvi *or_pbvi_build(const or_model *m, const double *b0, int expansions, int max_points, uint32_t seed,
+                       int sweeps) {
+    int nx = m->nx, na = m->na, nz = m->nz;
+    or_pbvi *p = (or_pbvi *)calloc(1, sizeof(or_pbvi));
+    p->nx = nx;
+    p->B = (double *)malloc(sizeof(double) * nx * (size_t)(max_points > 0 ? max_points : 1));
+    memcpy(p->B, b0, sizeof(double) * nx);
+    p->nb = 1;
+    double *cand = (double *)malloc(sizeof(double) * nx * na);
+    /* belief set expansion */
+    for (int r = 0; r < expansions && p->nb < max_points; ++r) {
+        int n0 = p->nb;
+        for (int i = 0; i < n0 && p->nb < max_points; ++i) {
+            const double *b = &p->B[(size_t)i * nx];
+            int best_a = -1;
+            double best_d = 0.0;
+            for (int a = 0; a < na; ++a) {
+                uint32_t ctr[4] = {(uint32_t)a, (uint32_t)i, (uint32_t)r, 0x7BB1u}, key[2] = {seed, 0xB5E7u}, w[4];
+                or_philox4x32_10(ctr, key, w);
+                int z = ancestral_draw(m, b, a, w, NULL);
+                double pz;
+                if (or_belief_update(m, b, a, z, &cand[(size_t)a * nx], &pz) != OR_OK) continue;
+                double dmin = INFINITY;      /* L1 distance to the set as grown so far */
+                for (int k = 0; k < p->nb; ++k) {
+                    double d = 0.0;
+                    for (int x = 0; x < nx; ++x) d += fabs(cand[(size_t)a * nx + x] - p->B[(size_t)k * nx + x]);
+                    if (d < dmin) dmin = d;
+                }
+                if (dmin > best_d) { best_d = dmin; best_a = a; }
+            }
+            if (best_a >= 0) {
+                memcpy(&p->B[(size_t)p->nb * nx], &cand[(size_t)best_a * nx], sizeof(double) * nx);
+                p->nb++;
+            }
+        }
+    }
+    free(cand);
+    /* point-based backups from the blind lower bound */
+    double rmin = INFINITY;
+    for (int i = 0; i < nx * na; ++i)
+        if (!(m->is_grid && m->occ[i / na]) && m->R[i] < rmin) rmin = m->R[i];
+    p->na_alpha = 1;
+    p->G = (double *)malloc(sizeof(double) * nx * (size_t)(p->nb > 1 ? p->nb : 1));
+    p->gact = (int *)calloc(p->nb > 1 ? p->nb : 1, sizeof(int));
+    for (int x = 0; x < nx; ++x) p->G[x] = (m->is_grid && m->occ[x]) ? 0.0 : rmin / (1.0 - m->gamma);
+    double *Gn = (double *)malloc(sizeof(double) * nx * (size_t)p->nb);
+    int *an = (int *)malloc(sizeof(int) * p->nb);
+    int *sel = (int *)malloc(sizeof(int) * na * nz);
+    for (int sw = 0; sw < sweeps; ++sw) {
+        for (int i = 0; i < p->nb; ++i) {
+            const double *b = &p->B[(size_t)i * nx];
+            double best_v = -INFINITY;
+            int best_a = 0;
+            for (int a = 0; a < na; ++a) {
+                double v = or_belief_reward(m, b, a);
+                double acc = 0.0;
+                for (int z = 0; z < nz; ++z) {
+                    double bz = -INFINITY;
+                    int bk = 0;
+                    for (int k = 0; k < p->na_alpha; ++k) {
+                        double d = pbvi_dot(m, b, a, z, &p->G[(size_t)k * nx]);
+                        if (d > bz) { bz = d; bk = k; }
+                    }
+                    sel[a * nz + z] = bk;
+                    acc += bz;
+                }
+                v += m->gamma * acc;
+                if (v > best_v) { best_v = v; best_a = a; }
+            }
+            /* alpha_b(x) = R(x,a*) + gamma sum_z sum_x' O(x',z) T(x,a*,x') alpha*_z(x') */
+            double *out = &Gn[(size_t)i * nx];
+            for (int x = 0; x < nx; ++x) {
+                if (m->is_grid && m->occ[x]) { out[x] = 0.0; continue; }
+                double acc = 0.0;
+                for (int z = 0; z < nz; ++z) {
+                    const double *al = &p->G[(size_t)sel[best_a * nz + z] * nx];
+                    double g = 0.0;
+                    for (int e = m->t_start[x * na + best_a]; e < m->t_start[x * na + best_a + 1]; ++e)
+                        g += m->O[m->t_y[e] * nz + z] * m->t_p[e] * al[m->t_y[e]];
+                    acc += g;
+                }
+                out[x] = m->R[x * na + best_a] + m->gamma * acc;
+            }
+            an[i] = m->action_id[best_a];
+        }
+        memcpy(p->G, Gn, sizeof(double) * nx * (size_t)p->nb);
+        memcpy(p->gact, an, sizeof(int) * p->nb);
+        p->na_alpha = p->nb;
+    }
+    free(Gn); free(an); free(sel);
+    return p;
+}
+void or_pbvi_free(or_pbvi *p) {
+    if (!p) return;
+    free(p->B); free(p->G); free(p->gact); free(p);
+}
+int or_pbvi_npoints(const or_pbvi *p) { return p->nb; }
+int or_pbvi_nalpha(const or_pbvi *p) { return p->na_alpha; }
+void or_pbvi_point(const or_pbvi *p, int i, double *out) { memcpy(out, &p->B[(size_t)i * p->nx], sizeof(double) * p->nx); }
+void or_pbvi_alpha(const or_pbvi *p, int i, double *out, int *action) {
+    memcpy(out, &p->G[(size_t)i * p->nx], sizeof(double) * p->nx);
+    if (action) *action = p->gact[i];
+}
+double or_pbvi_value(const or_pbvi *p, const double *b) {
+    double best = -INFINITY;
+    for (int k = 0; k < p->na_alpha; ++k) {
+        double s = 0.0;
+        for (int x = 0; x < p->nx; ++x) s += p->G[(size_t)k * p->nx + x] * b[x];
+        if (s > best) best = s;
+    }
+    return best;
+}
+
 /* Eq. 4 with one alpha-vector per action, alpha_a = Q(.,a) (north star Q_MDP leaf; R14). */
 double or_qmdp_value(const or_model *m, const double *Q, const double *b, int *argmax) {
     double best = -INFINITY;

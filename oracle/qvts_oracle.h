@@ -60,6 +60,24 @@ int or_value_iteration(const or_model *m, double eps, int max_sweeps, double *V,
  * alpha = R_max/(1-gamma) until max|alpha' - alpha| < eps; layout [na][nx].
  * Occupied grid cells: alpha = 0 (unreachable, as for Q). */
 int or_fib(const or_model *m, double eps, int max_iter, double *alpha, int *iters, double *resid);
+/* ---- PBVI lower bound (§IV-B) ----
+ * Belief set: B0 = {b0}; each expansion round, for every point b (in order) and every action a
+ * (ascending) one Alg. 4 sample (x ~ b, x' ~ T, z ~ O; Philox words 1..3 of counter
+ * (a, point, round, 0x7BB1), key (seed, 0xB5E7)) gives the candidate Phi(b,a,z); the candidate
+ * farthest in L1 from the set (as grown so far) is added if that distance is > 0 (ties: lowest a).
+ * Backups: Gamma0 = {R_min/(1-gamma)}; a sweep replaces Gamma by one vector per point,
+ * alpha_b = R(.,a*) + gamma sum_z g_{a*,z}^{alpha*_{a*,z}}, g_{a,z}^alpha(x) = sum_x' O(x',z)
+ * T(x,a,x') alpha(x'), alpha*_{a,z} = argmax_{alpha in Gamma} b . g_{a,z}^alpha, a* = argmax_a of
+ * b.R(.,a) + gamma sum_z max_alpha b . g (ties: lowest index). */
+typedef struct or_pbvi or_pbvi;
+or_pbvi *or_pbvi_build(const or_model *m, const double *b0, int expansions, int max_points, uint32_t seed,
+                       int sweeps);
+void or_pbvi_free(or_pbvi *p);
+int or_pbvi_npoints(const or_pbvi *p);
+int or_pbvi_nalpha(const or_pbvi *p);
+void or_pbvi_point(const or_pbvi *p, int i, double *out);      /* belief point i [nx] */
+void or_pbvi_alpha(const or_pbvi *p, int i, double *out, int *action);
+double or_pbvi_value(const or_pbvi *p, const double *b);       /* V_PBVI(b) = max alpha . b */
 /* Eq. 4 with alpha_a = Q(.,a): max_a sum_x b(x) Q(x,a); argmax lowest index. */
 double or_qmdp_value(const or_model *m, const double *Q, const double *b, int *argmax);
 

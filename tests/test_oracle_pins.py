@@ -478,3 +478,53 @@ def test_ancestral_sampler_in_plan_matches_alg4_and_marginal():
     n = 40000
     sd = np.sqrt(n * P * (1 - P))
     assert np.all(np.abs(cnt - n * P) <= 5 * sd + 1)      # distribution = the marginal P(z|b,a)
+
+
+# ---- NEXT-2 (part A): PBVI lower bound (§IV-B) --------------------------------------------------
+def _chain(nx=5, gamma=0.9):
+    """Deterministic left/right chain, perfectly observed (O = identity), goal at the right end."""
+    T = np.zeros((nx, 2, nx))
+    R = np.full((nx, 2), -1.0)
+    for x in range(nx):
+        T[x, 0, max(0, x - 1)] = 1
+        T[x, 1, min(nx - 1, x + 1)] = 1
+    R[nx - 1, :] = 0.0
+    return O.Model.dense(T, np.eye(nx), R, gamma)
+
+
+def test_pbvi_zero_sweeps_is_the_blind_bound():
+    gm = W.random_map(6, 7, 0.2, seed=2)
+    m = O.Model.grid(gm, action_mask=W.A8, acc=0.9)
+    b0 = W.uniform_belief(gm)
+    pts, al, _ = m.pbvi(b0, expansions=2, max_points=8, seed=1, sweeps=0)
+    rmin = min(m.R(x, a) for x in range(m.nx) for a in range(m.na) if gm.occupancy[x] == 0)
+    for b in pts:
+        assert max(a @ b for a in al) == pytest.approx(rmin / (1 - 0.95), abs=1e-12)
+
+
+def test_pbvi_perfect_observation_chain_reaches_mdp_values():
+    m = _chain()
+    b0 = np.eye(5)[0]
+    pts, al, _ = m.pbvi(b0, expansions=6, max_points=8, seed=3, sweeps=400)
+    _, V, Q, _, _ = m.value_iteration(1e-12)
+    for b in pts:                      # the expansion reaches point masses along the chain
+        x = int(np.argmax(b))
+        assert b[x] == 1.0
+        assert max(a @ b for a in al) == pytest.approx(V[x], abs=1e-9)
+
+
+def test_pbvi_sandwich_and_monotone_sweeps():
+    gm = W.random_map(6, 8, 0.2, seed=6)
+    m = O.Model.grid(gm, action_mask=W.A8, acc=0.85)
+    b0 = W.uniform_belief(gm)
+    _, A, _, _ = m.fib(1e-9)
+    prev = None
+    for sw in (5, 10, 20):
+        pts, al, _ = m.pbvi(b0, expansions=3, max_points=8, seed=2, sweeps=sw)
+        vals = np.array([max(a @ b for a in al) for b in pts])
+        probes = list(pts) + [W.random_belief(gm, s) for s in range(4)]
+        for b in probes:               # V_PBVI <= V_FIB (<= Q_MDP)
+            assert max(a @ b for a in al) <= max(A @ b) + 1e-9
+        if prev is not None:           # from the blind lower bound, values at B never decrease
+            assert np.all(vals >= prev - 1e-12)
+        prev = vals
