@@ -105,6 +105,26 @@ QVTS_API qvts_status qvts_fib_iteration(qvts_model *model, double eps, int32_t m
 /* Host copy of alpha_FIB in fp64, [|A|][H*W]; QVTS_ERR_STATE before qvts_fib_iteration. */
 QVTS_API qvts_status qvts_get_alpha(const qvts_model *model, double *alpha_host);
 
+/* ---- (2c) PBVI lower bound (§IV-B), fp64 ---------
+ * Belief set: starts at {b0} (b0_dev: device fp32 [H*W], or NULL = uniform over free cells);
+ * `expansions` rounds, each visiting the points present at its start in order: one Alg. 4 sample
+ * per action (Philox4x32-10 ctr = (action index, point, round, 0x7BB1), key = (seed, 0xB5E7),
+ * words 1..3 = x ~ b, x' ~ T, z ~ O), the Bayes posterior of each, and the one farthest in L1
+ * from the set as grown so far is appended if that distance is > 0 (ties: lowest action index;
+ * zero-likelihood posteriors skipped); stops at max_points (1..1024).
+ * Backups: Gamma = {R_min / (1 - gamma)} (R_min over free cells and actions), then `sweeps`
+ * point-based backups; each gives every point b the vector
+ * alpha_b = R(.,a*) + gamma sum_z g_{a*,z}^{alpha*_{a*,z}}, alpha* = argmax_alpha b . g, a* = argmax of
+ * the backed-up value (ties: lowest index).  Occupied cells: alpha = 0.  Synchronises `stream`;
+ * *n_points_out = the number of belief points (= alpha vectors after >= 1 sweep). */
+QVTS_API qvts_status qvts_pbvi(qvts_model *model, const float *b0_dev, int32_t expansions, int32_t max_points,
+                               uint32_t seed, int32_t sweeps, int32_t *n_points_out, void *stream);
+/* Host copies after qvts_pbvi (any pointer may be NULL): points fp64 [n_points][H*W], alpha fp64
+ * [n_alpha][H*W], actions int32 [n_points] (stencil ids; 0 before any sweep); QVTS_ERR_STATE
+ * before qvts_pbvi. */
+QVTS_API qvts_status qvts_get_pbvi(const qvts_model *model, double *points_host, double *alpha_host,
+                                   int32_t *actions_host, int32_t *n_alpha_out);
+
 /* ---- (3) Bayes belief update, Eq. 3 ----------------------------------
  * out(x') = O(x',z) sum_x T(x,a,x') b(x) / P(z|b,a); *p_obs_out = P(z|b,a) (fp64).
  * b_dev and out_dev: device fp32 [H*W] (may not alias).  QVTS_ERR_ZERO_LIKELIHOOD when

@@ -393,6 +393,10 @@ int or_fib(const or_model *m, double eps, int max_iter, double *alpha, int *iter
 
 /* ---- PBVI (§IV-B) ------------------------------------------------------------------------------ */
 static int ancestral_draw(const or_model *m, const double *b, int a, const uint32_t w[4], int *flag);
+/* PBVI arg-max rule (reading B4): v replaces the incumbent only if it is larger by more
+ * than 1e-10 (1 + |incumbent|) -> near-ties go to the lowest index on any summation order. */
+#define OR_PBVI_TIE 1e-10
+static int pbvi_beats(double v, double best) { return v > best + OR_PBVI_TIE * (1.0 + fabs(best)); }
 struct or_pbvi {
     int nx, nb, na_alpha;
     double *B;        /* [nb][nx] */
@@ -443,7 +447,7 @@ or_pbvi *or_pbvi_build(const or_model *m, const double *b0, int expansions, int 
                     for (int x = 0; x < nx; ++x) d += fabs(cand[(size_t)a * nx + x] - p->B[(size_t)k * nx + x]);
                     if (d < dmin) dmin = d;
                 }
-                if (dmin > best_d) { best_d = dmin; best_a = a; }
+                if (pbvi_beats(dmin, best_d)) { best_d = dmin; best_a = a; }
             }
             if (best_a >= 0) {
                 memcpy(&p->B[(size_t)p->nb * nx], &cand[(size_t)best_a * nx], sizeof(double) * nx);
@@ -472,17 +476,17 @@ or_pbvi *or_pbvi_build(const or_model *m, const double *b0, int expansions, int 
                 double v = or_belief_reward(m, b, a);
                 double acc = 0.0;
                 for (int z = 0; z < nz; ++z) {
-                    double bz = -INFINITY;
+                    double bz = 0.0;
                     int bk = 0;
                     for (int k = 0; k < p->na_alpha; ++k) {
                         double d = pbvi_dot(m, b, a, z, &p->G[(size_t)k * nx]);
-                        if (d > bz) { bz = d; bk = k; }
+                        if (k == 0 || pbvi_beats(d, bz)) { bz = d; bk = k; }
                     }
                     sel[a * nz + z] = bk;
                     acc += bz;
                 }
                 v += m->gamma * acc;
-                if (v > best_v) { best_v = v; best_a = a; }
+                if (a == 0 || pbvi_beats(v, best_v)) { best_v = v; best_a = a; }
             }
             /* alpha_b(x) = R(x,a*) + gamma sum_z sum_x' O(x',z) T(x,a*,x') alpha*_z(x') */
             double *out = &Gn[(size_t)i * nx];

@@ -533,7 +533,9 @@ extern "C" void qvts_model_destroy(qvts_model *m) {
                       &m->bu_U, &m->bu_off, &m->bu_path, &m->bu_root, &m->bu_key, &m->d_ctab, &m->d_R64, &m->d_O64, &m->d_O32, &m->d_gc_cell,
                       &m->d_gc_act, &m->d_gc_val, &m->d_free, &m->d_V[0], &m->d_V[1], &m->d_A[0], &m->d_A[1], &m->d_alpha64, &m->d_resid,
                       &m->d_Q64, &m->part, &m->tickets, &m->xs, &m->scan_tmp, &m->total, &m->counters, &m->vshard,
-                      &m->ep_b[0], &m->ep_b[1], &m->ep_state, &m->ep_root_step, &m->ep_root_ep};
+                      &m->ep_b[0], &m->ep_b[1], &m->ep_state, &m->ep_root_step, &m->ep_root_ep,
+                      &m->pb_b0, &m->pb_B, &m->pb_G, &m->pb_Gn, &m->pb_GT, &m->pb_Bbar, &m->pb_Sc, &m->pb_Rb,
+                      &m->pb_sel, &m->pb_astar, &m->pb_cand, &m->pb_misc, &m->pb_cls};
     for (DevBuf *b : bufs) b->release();
     for (BandSet *bs : {&m->band_big, &m->band_small}) {
         bs->bands.release(); bs->entries.release(); bs->slot_cell.release(); bs->qlist.release(); bs->qlist_fib.release();

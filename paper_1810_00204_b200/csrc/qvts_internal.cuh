@@ -112,6 +112,11 @@ struct Model {
     DevBuf bu_R, bu_P, bu_cnt, bu_umask, bu_U, bu_off, bu_path, bu_root, bu_key;
     // episodes
     DevBuf ep_b[2], ep_state, ep_root_step, ep_root_ep;
+    // PBVI lower bound (NEXT-2, pbvi.cu)
+    bool have_pbvi = false;
+    int pb_np = 0, pb_nal = 0, pb_P = 0;
+    std::vector<int32_t> pb_act;
+    DevBuf pb_b0, pb_B, pb_G, pb_Gn, pb_GT, pb_Bbar, pb_Sc, pb_Rb, pb_sel, pb_astar, pb_cand, pb_misc, pb_cls;
 };
 
 // instrumentation helpers (model.cu)

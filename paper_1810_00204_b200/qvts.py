@@ -24,6 +24,7 @@ EXPORTS = [
     "qvts_value_iteration", "qvts_get_q", "qvts_belief_update", "qvts_plan_step", "qvts_trace_qnodes",
     "qvts_trace_vnodes", "qvts_trace_leaf_values", "qvts_trace_belief", "qvts_run_episodes",
     "qvts_trace_counts", "qvts_set_profiling", "qvts_get_profile", "qvts_fib_iteration", "qvts_get_alpha",
+    "qvts_pbvi", "qvts_get_pbvi",
 ]
 QVTS_LEAF_QMDP, QVTS_LEAF_FIB = 0, 1
 QVTS_SAMPLER_MARGINAL, QVTS_SAMPLER_ANCESTRAL = 0, 1
@@ -105,6 +106,8 @@ def lib() -> C.CDLL:
         L.qvts_get_q.argtypes = [vp, vp]
         L.qvts_fib_iteration.argtypes = [vp, C.c_double, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_double), vp]
         L.qvts_get_alpha.argtypes = [vp, vp]
+        L.qvts_pbvi.argtypes = [vp, vp, C.c_int32, C.c_int32, C.c_uint32, C.c_int32, C.POINTER(C.c_int32), vp]
+        L.qvts_get_pbvi.argtypes = [vp, vp, vp, vp, C.POINTER(C.c_int32)]
         L.qvts_belief_update.argtypes = [vp, vp, C.c_int32, C.c_int32, vp, C.POINTER(C.c_double), vp]
         L.qvts_plan_step.argtypes = [vp, vp, C.POINTER(qvts_plan_cfg), C.POINTER(qvts_comm),
                                      C.POINTER(qvts_plan_result), vp]
@@ -205,6 +208,24 @@ def qvts_get_alpha(h, n_actions, n_cells):
     a = np.zeros((n_actions, n_cells), np.float64)
     _check(lib().qvts_get_alpha(h, a.ctypes.data), "qvts_get_alpha")
     return a
+
+
+def qvts_pbvi(h, b0_dev=None, expansions=3, max_points=16, seed=1, sweeps=30, stream=None):
+    n = C.c_int32()
+    _check(lib().qvts_pbvi(h, _ptr(b0_dev) if b0_dev is not None else None, int(expansions), int(max_points),
+                           int(seed), int(sweeps), C.byref(n), _stream(stream)), "qvts_pbvi")
+    return n.value
+
+
+def qvts_get_pbvi(h, n_points, n_cells):
+    """-> (points [n_points][n_cells] fp64, alphas [n_alpha][n_cells] fp64, actions [n_points])."""
+    nal = C.c_int32()
+    _check(lib().qvts_get_pbvi(h, None, None, None, C.byref(nal)), "qvts_get_pbvi")
+    pts = np.zeros((n_points, n_cells), np.float64)
+    al = np.zeros((nal.value, n_cells), np.float64)
+    act = np.zeros(n_points, np.int32)
+    _check(lib().qvts_get_pbvi(h, pts.ctypes.data, al.ctypes.data, act.ctypes.data, None), "qvts_get_pbvi")
+    return pts, al, act
 
 
 def qvts_belief_update(h, b_dev, action, z, out_dev, stream=None):
@@ -371,6 +392,11 @@ class Model:
 
     def alpha(self):
         return qvts_get_alpha(self.h, self.n_actions, self.n_cells)
+
+    def pbvi(self, b0_dev=None, expansions=3, max_points=16, seed=1, sweeps=30):
+        """PBVI lower bound on the GPU -> (points, alphas, actions) as host fp64 / int32 arrays."""
+        n = qvts_pbvi(self.h, b0_dev, expansions, max_points, seed, sweeps)
+        return qvts_get_pbvi(self.h, n, self.n_cells)
 
     def tables(self):
         return qvts_model_tables(self.h, self.n_actions, self.n_cells)

@@ -282,3 +282,39 @@ def test_plan_ancestral_sampler(Q, name, depth, n):
     gm, mask = MAPS[name][0](), MAPS[name][1]
     res, err, nmis = run_parity(Q, gm, mask, depth, n, W.random_belief(gm, 8), seed=3, step=1,
                                 beliefs=(name != "paper"), sampler=Q.QVTS_SAMPLER_ANCESTRAL)
+
+
+@pytest.mark.parametrize("name,b0,exp,maxp,sweeps", [("C1", "uniform", 3, 12, 20), ("ragged", "random", 3, 16, 15),
+                                                     ("paper", "uniform", 2, 10, 8)])
+def test_pbvi_against_oracle(Q, name, b0, exp, maxp, sweeps):
+    """NEXT-2: PBVI lower bound — the belief set (Alg. 4 draws + farthest-posterior rule) and the
+    alpha-vectors after `sweeps` point-based backups, element by element against the oracle."""
+    gm, mask = MAPS[name][0](), MAPS[name][1]
+    g = Q.Model(gm, action_mask=mask)
+    o = O.Model.grid(gm, action_mask=mask)
+    b32 = np.asarray(W.uniform_belief(gm) if b0 == "uniform" else W.random_belief(gm, 5), np.float32)
+    pts, al, act = g.pbvi(dev(b32), expansions=exp, max_points=maxp, seed=7, sweeps=sweeps)
+    opts, oal, oact = o.pbvi(b32.astype(np.float64), expansions=exp, max_points=maxp, seed=7, sweeps=sweeps)
+    assert pts.shape == opts.shape and pts.shape[0] > 1
+    assert np.max(np.abs(pts - opts)) <= 1e-12
+    assert al.shape == oal.shape
+    assert np.max(np.abs(al - oal)) <= 1e-9 * max(1.0, np.max(np.abs(oal)))
+    assert np.array_equal(act[:len(oact)], oact)
+    # lower bound on the belief points: below FIB's upper bound
+    code, _, _ = g.fib_iteration(1e-9)
+    A = g.alpha()
+    for b in pts:
+        assert np.max(al @ b) <= np.max(A @ b) + 1e-9
+    g.close()
+
+
+def test_pbvi_zero_sweeps_and_single_point(Q):
+    """Degenerate cases: no sweeps leaves the blind vector; expansions = 0 keeps {b0} only."""
+    gm = W.CONFIGS["C1"]["map"]()
+    g = Q.Model(gm, action_mask=W.A4)
+    pts, al, act = g.pbvi(None, expansions=0, max_points=8, seed=1, sweeps=0)
+    assert pts.shape[0] == 1 and al.shape[0] == 1
+    o = O.Model.grid(gm, action_mask=W.A4)
+    opts, oal, _ = o.pbvi(np.asarray(W.uniform_belief(gm), np.float64), expansions=0, max_points=8, seed=1, sweeps=0)
+    assert np.max(np.abs(pts - opts)) <= 1e-15 and np.max(np.abs(al - oal)) == 0.0
+    g.close()
