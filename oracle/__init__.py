@@ -55,6 +55,11 @@ class PlanCfg(C.Structure):
                 ("replay_j", C.c_void_p), ("replay_z", C.c_void_p)]
 
 
+class BfCfg(C.Structure):
+    _fields_ = [("expansions", C.c_int), ("max_depth", C.c_int), ("gap_tol", C.c_double),
+                ("n_replay", C.c_int), ("replay_path", C.c_void_p), ("replay_tol", C.c_double)]
+
+
 class EpisodeCfg(C.Structure):
     _fields_ = [("planner", C.c_int), ("depth", C.c_int), ("n_samples", C.c_int),
                 ("max_steps", C.c_int), ("stop_patience", C.c_int),
@@ -64,6 +69,22 @@ class EpisodeCfg(C.Structure):
 class EpisodeRecord(C.Structure):
     _fields_ = [("outcome", C.c_int32), ("steps", C.c_int32), ("collisions", C.c_int32),
                 ("x0", C.c_int32), ("x_final", C.c_int32), ("disc_return", C.c_double)]
+
+
+def bf_q_update(R, gamma, w, U, L, H, E):
+    """Alg. 6 on explicit child values -> (U_Q, L_Q, H_Q, E_Q)."""
+    out = [C.c_double(), C.c_double(), C.c_double(), C.c_int()]
+    lib().or_bf_q_update(R, gamma, len(w), *[np.ascontiguousarray(a, dtype=np.float64) for a in (w, U, L, H)],
+                         np.ascontiguousarray(E, dtype=np.int32), *[C.byref(o) for o in out])
+    return tuple(o.value for o in out)
+
+
+def bf_v_update(UQ, LQ, HQ, EQ):
+    """Alg. 7 (argmax-U_Q child) on explicit Q values -> (U, L, H, E)."""
+    out = [C.c_double(), C.c_double(), C.c_double(), C.c_int()]
+    lib().or_bf_v_update(len(UQ), *[np.ascontiguousarray(a, dtype=np.float64) for a in (UQ, LQ, HQ)],
+                         np.ascontiguousarray(EQ, dtype=np.int32), *[C.byref(o) for o in out])
+    return tuple(o.value for o in out)
 
 
 def _declare(L):
@@ -109,6 +130,22 @@ def _declare(L):
     L.or_pbvi_alpha.argtypes = [vp, C.c_int, _dp, C.POINTER(C.c_int)]
     L.or_pbvi_value.restype = C.c_double
     L.or_pbvi_value.argtypes = [vp, _dp]
+    L.or_bf_q_update.argtypes = [C.c_double, C.c_double, C.c_int, _dp, _dp, _dp, _dp, _i32p,
+                                 C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                 C.POINTER(C.c_int)]
+    L.or_bf_v_update.argtypes = [C.c_int, _dp, _dp, _dp, _i32p, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                 C.POINTER(C.c_double), C.POINTER(C.c_int)]
+    L.or_bf_plan.restype = vp
+    L.or_bf_plan.argtypes = [vp, _dp, C.c_int, _dp, C.c_int, _i32p, _dp, C.POINTER(PlanCfg), C.POINTER(BfCfg)]
+    L.or_bf_free.argtypes = [vp]
+    L.or_bf_summary.argtypes = [vp] + [C.POINTER(C.c_int)] * 6
+    L.or_bf_root.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_double), _dp, _dp]
+    L.or_bf_vnode.argtypes = [vp, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                              C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double),
+                              C.POINTER(C.c_double), C.POINTER(C.c_int), C.POINTER(C.c_int)]
+    L.or_bf_expanded.restype = C.c_uint64
+    L.or_bf_expanded.argtypes = [vp, C.c_int]
+    L.or_bf_root_trace.argtypes = [vp, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.or_qmdp_value.restype = C.c_double
     L.or_qmdp_value.argtypes = [vp, _dp, _dp, C.POINTER(C.c_int)]
     L.or_trace_new.restype = vp
@@ -304,6 +341,50 @@ class Model:
             acts[i] = a.value
         L.or_pbvi_free(h)
         return pts, al, acts
+
+    def best_first(self, alphaU, alphaL, actL, b0, n, expansions, max_depth=8, gap_tol=0.0, seed=1, step=0,
+                   episode=0, mode=MODE_FREQ, sampler=0, replay=None, replay_tol=1e-4):
+        """Anytime best-first QVTS (Alg. 1-7, Eq. 8) with U = V_FIB, L = V_PBVI leaves.  Returns a
+        dict: action, stop, n_exp, subs, mism, U, L, UQ, LQ, expanded (paths), root_trace
+        [(U, L) after k expansions], and per V-node arrays path/depth/f/w/U/L/H/E/expanded."""
+        L_ = lib()
+        aU = np.ascontiguousarray(alphaU, dtype=np.float64)
+        aL = np.ascontiguousarray(alphaL, dtype=np.float64)
+        acts = np.ascontiguousarray(actL, dtype=np.int32)
+        cfg, _k = self._cfg(0, n, seed, step, episode, mode, 0, None, sampler)
+        rp = np.ascontiguousarray(replay if replay is not None else [], dtype=np.uint64)
+        bc = BfCfg(expansions, max_depth, gap_tol, len(rp), rp.ctypes.data if len(rp) else None, replay_tol)
+        h = L_.or_bf_plan(self._h, aU, aU.shape[0], aL, aL.shape[0], acts,
+                          np.ascontiguousarray(b0, dtype=np.float64), C.byref(cfg), C.byref(bc))
+        if not h:
+            raise ValueError("or_bf_plan rejected its arguments")
+        out = {}
+        vals = [C.c_int() for _ in range(6)]
+        L_.or_bf_summary(h, *[C.byref(v) for v in vals])
+        for k, v in zip(("action", "stop", "n_exp", "n_v", "subs", "mism"), vals):
+            out[k] = v.value
+        U, Lo = C.c_double(), C.c_double()
+        UQ, LQ = np.zeros(self.na), np.zeros(self.na)
+        L_.or_bf_root(h, C.byref(U), C.byref(Lo), UQ, LQ)
+        out.update(U=U.value, L=Lo.value, UQ=UQ, LQ=LQ)
+        out["expanded"] = np.array([L_.or_bf_expanded(h, k) for k in range(out["n_exp"])], dtype=np.uint64)
+        rt = []
+        for k in range(out["n_exp"] + 1):
+            L_.or_bf_root_trace(h, k, C.byref(U), C.byref(Lo))
+            rt.append((U.value, Lo.value))
+        out["root_trace"] = np.array(rt)
+        nv = out["n_v"]
+        cols = {k: [] for k in ("path", "depth", "f", "w", "U", "L", "H", "E", "expanded")}
+        p, d, f, E, ex = C.c_uint64(), C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        w, u, l, hh = C.c_double(), C.c_double(), C.c_double(), C.c_double()
+        for i in range(nv):
+            L_.or_bf_vnode(h, i, C.byref(p), C.byref(d), C.byref(f), C.byref(w), C.byref(u), C.byref(l),
+                           C.byref(hh), C.byref(E), C.byref(ex))
+            for k, v in zip(cols, (p, d, f, w, u, l, hh, E, ex)):
+                cols[k].append(v.value)
+        out["v"] = {k: np.array(v, dtype=np.uint64 if k == "path" else None) for k, v in cols.items()}
+        L_.or_bf_free(h)
+        return out
 
     def qmdp_value(self, Q, b):
         arg = C.c_int(0)

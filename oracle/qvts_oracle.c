@@ -988,3 +988,276 @@ int or_run_episode(const or_model *m, const double *Q, const double *b0, const o
     free(b); free(bn); free(qroot);
     return OR_OK;
 }
+
+/* ------------------------------------------------------------------------------------------ */
+/* Anytime best-first QVTS (Alg. 1-7, Eq. 8).          */
+/* Nodes live in flat arrays; V-node i carries its belief, (U, L, H, E) and its Q-children     */
+/* [q0, q0 + na); Q-node j carries (R, U, L, H, E) and its V-children [c0, c0 + nc).           */
+void or_bf_q_update(double R, double gamma, int nc, const double *w, const double *U, const double *L,
+                    const double *H, const int *E, double *UQ, double *LQ, double *HQ, int *EQ) {
+    double su = 0.0, sl = 0.0, bh = 0.0;
+    int bc = 0;
+    for (int c = 0; c < nc; ++c) {
+        su += w[c] * U[c];
+        sl += w[c] * L[c];
+        double h = gamma * w[c] * H[c];                 /* Alg. 6: gamma x weight x heuristic */
+        if (c == 0 || h > bh) { bh = h; bc = c; }
+    }
+    *UQ = R + gamma * su;                               /* Alg. 6 with gamma (R13, Eq. 2)     */
+    *LQ = R + gamma * sl;
+    *HQ = bh;
+    *EQ = E[bc];
+}
+
+void or_bf_v_update(int na, const double *UQ, const double *LQ, const double *HQ, const int *EQ,
+                    double *U, double *L, double *H, int *E) {
+    int bq = 0;
+    double bl = LQ[0];
+    for (int a = 1; a < na; ++a) {
+        if (UQ[a] > UQ[bq]) bq = a;                     /* H(b,a) = 1 at argmax U_Q (Sec. IV-C) */
+        if (LQ[a] > bl) bl = LQ[a];
+    }
+    *U = UQ[bq];
+    *L = bl;
+    *H = HQ[bq];
+    *E = EQ[bq];
+}
+
+typedef struct {
+    double *b;
+    uint64_t path;
+    int depth, pq, z, f, q0, E;
+    double w, U, L, H;
+} bf_v;
+typedef struct {
+    int pv, a, c0, nc, E;
+    double R, U, L, H;
+} bf_q;
+struct or_bf_tree {
+    const or_model *m;
+    int na;
+    bf_v *v;
+    bf_q *q;
+    int nv, nq, cap_v, cap_q;
+    int action, stop, n_exp, subs, mism;
+    uint64_t *exp_path;
+    double *rootU, *rootL;
+};
+
+static double bf_dot_max(const double *A, int n, int nx, const double *b, int *arg) {
+    double best = 0.0;
+    int ba = 0;
+    for (int k = 0; k < n; ++k) {
+        double s = 0.0;
+        for (int x = 0; x < nx; ++x) s += A[(size_t)k * nx + x] * b[x];
+        if (k == 0 || s > best) { best = s; ba = k; }
+    }
+    if (arg) *arg = ba;
+    return best;
+}
+
+static int bf_new_v(or_bf_tree *t) {
+    if (t->nv == t->cap_v) {
+        t->cap_v *= 2;
+        t->v = (bf_v *)realloc(t->v, sizeof(bf_v) * t->cap_v);
+    }
+    memset(&t->v[t->nv], 0, sizeof(bf_v));
+    return t->nv++;
+}
+
+static void bf_update_q(or_bf_tree *t, int j) {
+    bf_q *q = &t->q[j];
+    int nc = q->nc;
+    double w[16], U[16], L[16], H[16];
+    int E[16];
+    for (int c = 0; c < nc; ++c) {
+        const bf_v *v = &t->v[q->c0 + c];
+        w[c] = v->w; U[c] = v->U; L[c] = v->L; H[c] = v->H; E[c] = v->E;
+    }
+    or_bf_q_update(q->R, t->m->gamma, nc, w, U, L, H, E, &q->U, &q->L, &q->H, &q->E);
+}
+
+static void bf_update_v(or_bf_tree *t, int i) {
+    bf_v *v = &t->v[i];
+    double UQ[9], LQ[9], HQ[9];
+    int EQ[9];
+    for (int a = 0; a < t->na; ++a) {
+        const bf_q *q = &t->q[v->q0 + a];
+        UQ[a] = q->U; LQ[a] = q->L; HQ[a] = q->H; EQ[a] = q->E;
+    }
+    or_bf_v_update(t->na, UQ, LQ, HQ, EQ, &v->U, &v->L, &v->H, &v->E);
+}
+
+/* Alg. 5: a new leaf V-node with U = V_FIB(b), L = V_PBVI(b), H = U - L, E = self. */
+static void bf_leaf(or_bf_tree *t, int i, const double *aU, int nU, const double *aL, int nL, int max_depth) {
+    bf_v *v = &t->v[i];
+    int nx = t->m->nx;
+    v->U = bf_dot_max(aU, nU, nx, v->b, NULL);
+    v->L = bf_dot_max(aL, nL, nx, v->b, NULL);
+    v->H = v->depth >= max_depth ? 0.0 : v->U - v->L;    /* terminal leaves (reading B5) */
+    v->E = i;
+    v->q0 = -1;
+}
+
+/* Alg. 2 + Alg. 3: all |A| Q-nodes of leaf i, one child per unique sampled z (or every z with
+ * P > 0 in EXACT mode), then the Alg. 6 / Alg. 7 updates of i. */
+static void bf_expand(or_bf_tree *t, int i, const double *aU, int nU, const double *aL, int nL,
+                      const or_plan_cfg *pcfg, int max_depth) {
+    const or_model *m = t->m;
+    int nx = m->nx, nz = m->nz, na = t->na, n = pcfg->n_samples;
+    double *bbar = (double *)malloc(sizeof(double) * nx);
+    uint8_t *zs = (uint8_t *)calloc(n > 0 ? n : 1, 1), *fl = (uint8_t *)calloc(n > 0 ? n : 1, 1);
+    if (t->nq + na > t->cap_q) {
+        while (t->nq + na > t->cap_q) t->cap_q *= 2;
+        t->q = (bf_q *)realloc(t->q, sizeof(bf_q) * t->cap_q);
+    }
+    int q0 = t->nq;
+    t->nq += na;
+    t->v[i].q0 = q0;
+    for (int a = 0; a < na; ++a) {
+        const double *b = t->v[i].b;
+        uint64_t vpath = t->v[i].path;
+        int depth = t->v[i].depth;
+        uint64_t qpath = qpath_of(vpath, depth, m->action_id[a]);
+        double P[16];
+        uint16_t cnt[16];
+        or_predict(m, b, a, bbar);
+        or_marginal(m, bbar, P);
+        bf_q *q = &t->q[q0 + a];
+        q->pv = i; q->a = a;
+        q->R = or_belief_reward(m, b, a);
+        if (pcfg->mode == OR_MODE_EXACT) { for (int z = 0; z < nz; ++z) cnt[z] = 0; }
+        else qnode_draws(m, b, a, pcfg, nz, P, qpath, zs, fl, cnt);
+        q->c0 = t->nv;
+        q->nc = 0;
+        for (int z = 0; z < nz; ++z) {
+            int take = pcfg->mode == OR_MODE_EXACT ? (P[z] > OR_ZERO_LIK) : (cnt[z] > 0);
+            if (!take) continue;
+            int c = bf_new_v(t);
+            bf_v *v = &t->v[c];
+            v->b = (double *)malloc(sizeof(double) * nx);
+            for (int y = 0; y < nx; ++y) v->b[y] = m->O[y * nz + z] * bbar[y] / P[z];   /* Eq. 3 */
+            v->path = vpath_of(qpath, depth, z);
+            v->depth = depth + 1;
+            v->pq = q0 + a;
+            v->z = z;
+            v->f = cnt[z];
+            v->w = pcfg->mode == OR_MODE_EXACT ? P[z] : (double)cnt[z] / (double)n;
+            bf_leaf(t, c, aU, nU, aL, nL, max_depth);
+            t->q[q0 + a].nc++;
+        }
+        bf_update_q(t, q0 + a);
+    }
+    bf_update_v(t, i);
+    free(bbar); free(zs); free(fl);
+}
+
+/* Admissible descent: at every decision the chosen child is within `tol` of the rule's best. */
+static int bf_admissible(const or_bf_tree *t, uint64_t path, double tol) {
+    int i = 0;
+    for (;;) {
+        const bf_v *v = &t->v[i];
+        if (v->q0 < 0) return v->path == path ? i : -1;
+        int lvl = v->depth;
+        int aid = (int)((path >> (8 * lvl)) & 15) - 1;
+        int z = (int)((path >> (8 * lvl + 4)) & 15);
+        int a = -1;
+        for (int k = 0; k < t->na; ++k) if (t->m->action_id[k] == aid) a = k;
+        if (a < 0) return -1;
+        double bu = -INFINITY;
+        for (int k = 0; k < t->na; ++k) bu = fmax(bu, t->q[v->q0 + k].U);
+        const bf_q *q = &t->q[v->q0 + a];
+        if (q->U < bu - tol) return -1;
+        double bh = -INFINITY;
+        int c = -1;
+        for (int k = 0; k < q->nc; ++k) {
+            const bf_v *ch = &t->v[q->c0 + k];
+            bh = fmax(bh, t->m->gamma * ch->w * ch->H);
+            if (ch->z == z) c = q->c0 + k;
+        }
+        if (c < 0 || t->m->gamma * t->v[c].w * t->v[c].H < bh - tol) return -1;
+        i = c;
+    }
+}
+
+or_bf_tree *or_bf_plan(const or_model *m, const double *alphaU, int nU, const double *alphaL, int nL,
+                       const int *actL, const double *b0, const or_plan_cfg *pcfg, const or_bf_cfg *bcfg) {
+    if (bcfg->max_depth < 1 || bcfg->max_depth > 8 || nU < 1 || nL < 1 || bcfg->expansions < 0) return NULL;
+    or_bf_tree *t = (or_bf_tree *)calloc(1, sizeof(or_bf_tree));
+    t->m = m;
+    t->na = m->na;
+    t->cap_v = 64; t->cap_q = 64;
+    t->v = (bf_v *)malloc(sizeof(bf_v) * t->cap_v);
+    t->q = (bf_q *)malloc(sizeof(bf_q) * t->cap_q);
+    t->exp_path = (uint64_t *)calloc(bcfg->expansions + 1, sizeof(uint64_t));
+    t->rootU = (double *)calloc(bcfg->expansions + 1, sizeof(double));
+    t->rootL = (double *)calloc(bcfg->expansions + 1, sizeof(double));
+    int r = bf_new_v(t);                                   /* Alg. 1: s = QVSearchTree(b0) */
+    t->v[r].b = (double *)malloc(sizeof(double) * m->nx);
+    memcpy(t->v[r].b, b0, sizeof(double) * m->nx);
+    t->v[r].pq = -1;
+    t->v[r].f = pcfg->n_samples;
+    t->v[r].w = 1.0;
+    bf_leaf(t, r, alphaU, nU, alphaL, nL, bcfg->max_depth);
+    t->stop = 0;
+    for (;;) {
+        t->rootU[t->n_exp] = t->v[0].U;
+        t->rootL[t->n_exp] = t->v[0].L;
+        if (t->n_exp >= bcfg->expansions) { t->stop = 0; break; }          /* planningFinished() */
+        if (t->v[0].U - t->v[0].L <= bcfg->gap_tol) { t->stop = 1; break; }
+        int e = t->v[0].E;                                 /* findVNodeToExpand() = root.E */
+        if (bcfg->n_replay > t->n_exp) {
+            int g = bf_admissible(t, bcfg->replay_path[t->n_exp], bcfg->replay_tol);
+            if (g < 0) t->mism++;
+            else if (g != e) { t->subs++; e = g; }
+        }
+        if (t->v[e].depth >= bcfg->max_depth) { t->stop = 2; break; }
+        t->exp_path[t->n_exp++] = t->v[e].path;
+        bf_expand(t, e, alphaU, nU, alphaL, nL, pcfg, bcfg->max_depth);     /* v.expand() */
+        for (int p = t->v[e].pq; p >= 0; p = t->v[t->q[p].pv].pq) {         /* p.update() to the root */
+            bf_update_q(t, p);
+            bf_update_v(t, t->q[p].pv);
+        }
+    }
+    /* getOptimalAction: max L_Q, ties by U_Q then index (SPEC plan); an unexpanded root takes the
+     * action of its PBVI arg-max vector. */
+    if (t->v[0].q0 < 0) {
+        int arg;
+        bf_dot_max(alphaL, nL, m->nx, t->v[0].b, &arg);
+        t->action = actL ? actL[arg] : 0;
+    } else {
+        int best = 0;
+        for (int a = 1; a < t->na; ++a) {
+            const bf_q *q = &t->q[t->v[0].q0 + a], *bq = &t->q[t->v[0].q0 + best];
+            if (q->L > bq->L || (q->L == bq->L && q->U > bq->U)) best = a;
+        }
+        t->action = m->action_id[best];
+    }
+    return t;
+}
+
+void or_bf_free(or_bf_tree *t) {
+    if (!t) return;
+    for (int i = 0; i < t->nv; ++i) free(t->v[i].b);
+    free(t->v); free(t->q); free(t->exp_path); free(t->rootU); free(t->rootL); free(t);
+}
+void or_bf_summary(const or_bf_tree *t, int *action, int *stop, int *n_exp, int *n_v, int *subs, int *mism) {
+    *action = t->action; *stop = t->stop; *n_exp = t->n_exp; *n_v = t->nv; *subs = t->subs; *mism = t->mism;
+}
+void or_bf_root(const or_bf_tree *t, double *U, double *L, double *UQ, double *LQ) {
+    *U = t->v[0].U;
+    *L = t->v[0].L;
+    for (int a = 0; a < t->na; ++a) {
+        int ok = t->v[0].q0 >= 0;
+        if (UQ) UQ[a] = ok ? t->q[t->v[0].q0 + a].U : NAN;
+        if (LQ) LQ[a] = ok ? t->q[t->v[0].q0 + a].L : NAN;
+    }
+}
+void or_bf_vnode(const or_bf_tree *t, int i, uint64_t *path, int *depth, int *f, double *w, double *U,
+                 double *L, double *H, int *E, int *expanded) {
+    const bf_v *v = &t->v[i];
+    *path = v->path; *depth = v->depth; *f = v->f; *w = v->w; *U = v->U; *L = v->L; *H = v->H; *E = v->E;
+    *expanded = v->q0 >= 0;
+}
+uint64_t or_bf_expanded(const or_bf_tree *t, int k) { return t->exp_path[k]; }
+void or_bf_root_trace(const or_bf_tree *t, int k, double *U, double *L) { *U = t->rootU[k]; *L = t->rootL[k]; }

@@ -118,6 +118,37 @@ int or_qnode_sample(const or_model *m, const double *b, int a, uint64_t qpath, c
 double or_vnode_value(const or_model *m, const double *Q, const double *b, uint64_t vpath, int level,
                       const or_plan_cfg *cfg, double *qvals /*[na] or NULL*/);
 
+/* ---- anytime best-first QVTS (Alg. 1-7 with U/L/H/E, Eq. 8) ----
+ * Alg. 6 (with gamma, R13) on one Q-node from its children (ascending z): U_Q = R + gamma sum w U,
+ * L_Q likewise; the heuristic child maximises gamma w H (ties lowest) and gives H_Q, E_Q. */
+void or_bf_q_update(double R, double gamma, int nc, const double *w, const double *U, const double *L,
+                    const double *H, const int *E, double *UQ, double *LQ, double *HQ, int *EQ);
+/* Alg. 7 with the Sec. IV-C indicator read as "the argmax-U_Q child" (ties lowest). */
+void or_bf_v_update(int na, const double *UQ, const double *LQ, const double *HQ, const int *EQ,
+                    double *U, double *L, double *H, int *E);
+typedef struct {
+    int expansions;       /* budget: V-node expansions (Alg. 1 planningFinished)                 */
+    int max_depth;        /* 1..8; leaves at this depth are terminal: H := 0 (reading B5)        */
+    double gap_tol;       /* stop once root U - L <= gap_tol                       */
+    int n_replay;         /* GPU expansion order (V-node paths); followed when admissible       */
+    const uint64_t *replay_path;
+    double replay_tol;    /* near-tie band of the admissibility check                            */
+} or_bf_cfg;
+typedef struct or_bf_tree or_bf_tree;
+/* pcfg: n_samples, mode (FREQ: weights f/n; EXACT: every z with P > 0, weight P), seed, step,
+ * episode, sampler.  alphaU [nU][nx] (FIB), alphaL [nL][nx] with actions actL (PBVI). */
+or_bf_tree *or_bf_plan(const or_model *m, const double *alphaU, int nU, const double *alphaL, int nL,
+                       const int *actL, const double *b0, const or_plan_cfg *pcfg, const or_bf_cfg *bcfg);
+void or_bf_free(or_bf_tree *t);
+/* action (stencil id), stop reason (0 budget, 1 gap, 2 terminal leaf selected), expansions done,
+ * V-nodes, replay substitutions (admissible GPU choices that differ) and mismatches. */
+void or_bf_summary(const or_bf_tree *t, int *action, int *stop, int *n_exp, int *n_v, int *subs, int *mism);
+void or_bf_root(const or_bf_tree *t, double *U, double *L, double *UQ, double *LQ);   /* UQ/LQ [na] or NULL */
+void or_bf_vnode(const or_bf_tree *t, int i, uint64_t *path, int *depth, int *f, double *w, double *U,
+                 double *L, double *H, int *E, int *expanded);
+uint64_t or_bf_expanded(const or_bf_tree *t, int k);    /* path of the k-th expanded V-node   */
+void or_bf_root_trace(const or_bf_tree *t, int k, double *U, double *L);   /* root U, L after k expansions */
+
 /* ---- episodes (reading R26/R27) ---- */
 enum { OR_PLANNER_QVTS = 0, OR_PLANNER_MDP = 1, OR_PLANNER_ASTAR = 2 };
 typedef struct {

@@ -528,3 +528,109 @@ def test_pbvi_sandwich_and_monotone_sweeps():
         if prev is not None:           # from the blind lower bound, values at B never decrease
             assert np.all(vals >= prev - 1e-12)
         prev = vals
+
+
+# ---- anytime best-first QVTS (Alg. 1-7, Eq. 8) ----------------------------
+def test_bf_update_rules_spec_examples():
+    """SPEC.md:340-350 hand values: Alg. 7 keeps H of the argmax-U child (not the larger H);
+    Alg. 6 weights 0.55/0.45 with gaps 2/1 give H_Q = 0.95 max(1.10, 0.45) = 1.045."""
+    U, L, H, E = O.bf_v_update([5.0, 3.0], [1.0, 2.0], [2.0, 4.0], [10, 11])
+    assert (U, L, H, E) == (5.0, 2.0, 2.0, 10)
+    assert O.bf_v_update([1.0, 1.0], [0.0, 0.0], [3.0, 3.0], [7, 8])[3] == 7       # ties -> first
+    UQ, LQ, HQ, EQ = O.bf_q_update(-1.0, 0.95, [0.55, 0.45], [0.0, 0.0], [-2.0, -1.0], [2.0, 1.0], [3, 4])
+    assert HQ == pytest.approx(1.045, abs=1e-15) and EQ == 3
+    assert LQ == pytest.approx(-1.0 + 0.95 * (0.55 * -2.0 + 0.45 * -1.0), abs=1e-15)
+    UQ, _, _, _ = O.bf_q_update(-1.0, 0.95, [1.0], [-3.0], [-4.0], [1.0], [0])       # single child
+    assert UQ == pytest.approx(-1.0 + 0.95 * -3.0, abs=1e-15)
+
+
+def _bounds(m, gm, b0, sweeps=20):
+    _, A, _, _ = m.fib(1e-9)
+    pts, al, act = m.pbvi(b0, expansions=3, max_points=8, seed=2, sweeps=sweeps)
+    return A, al, act
+
+
+def test_bf_zero_expansions_is_the_leaf():
+    gm = W.random_map(6, 7, 0.2, seed=3)
+    m = O.Model.grid(gm, action_mask=W.A8, acc=0.9)
+    b0 = W.random_belief(gm, 2)
+    A, al, act = _bounds(m, gm, b0)
+    r = m.best_first(A, al, act, b0, n=8, expansions=0)
+    assert r["n_exp"] == 0 and r["stop"] == 0
+    assert r["U"] == pytest.approx(max(A @ b0), abs=1e-12)
+    assert r["L"] == pytest.approx(max(al @ b0), abs=1e-12)
+    assert r["action"] == act[int(np.argmax(al @ b0))]
+
+
+def test_bf_one_expansion_matches_depth1_plan_with_fib_leaves():
+    """One expansion with terminal children is a depth-1 tree: U_Q(a) is or_plan's Q(root, a)
+    with the FIB alpha-vectors as leaf vectors (same Philox keys), and in EXACT mode
+    L_Q(a) = R(b,a) + gamma sum_z P(z|b,a) V_PBVI(Phi(b,a,z)) (Eq. 2)."""
+    gm = W.random_map(7, 6, 0.2, seed=5)
+    m = O.Model.grid(gm, action_mask=W.A8, acc=0.9)
+    b0 = W.random_belief(gm, 4)
+    A, al, act = _bounds(m, gm, b0)
+    r = m.best_first(A, al, act, b0, n=16, expansions=1, max_depth=1, seed=3, step=2)
+    p = m.plan(A, b0, 1, 16, seed=3, step=2)
+    assert r["n_exp"] == 1 and r["stop"] == 0
+    assert np.max(np.abs(r["UQ"] - p.qroot)) <= 1e-12
+    r = m.best_first(A, al, act, b0, n=16, expansions=1, max_depth=1, mode=O.MODE_EXACT)
+    for a in range(m.na):
+        bbar = m.predict(b0, a)
+        P = m.marginal(bbar)
+        acc = 0.0
+        for z in range(16):
+            if P[z] > 1e-300:
+                bz, _ = m.belief_update(b0, a, z)
+                acc += P[z] * max(al @ bz)
+        assert r["LQ"][a] == pytest.approx(m.belief_reward(b0, a) + 0.95 * acc, abs=1e-12)
+
+
+def test_bf_exact_weights_bounds_tighten_monotonically():
+    """With exact weights each expansion replaces a leaf interval by a Bellman image of its
+    children's intervals; FIB and PBVI are uniformly improvable (V_PBVI <= H V_PBVI,
+    H V_FIB <= V_FIB), so the root U never rises and L never falls (Sec. IV-C anytime)."""
+    gm = W.random_map(6, 7, 0.2, seed=8)
+    m = O.Model.grid(gm, action_mask=W.A8, acc=0.9)
+    b0 = W.uniform_belief(gm)
+    A, al, act = _bounds(m, gm, b0, sweeps=30)
+    r = m.best_first(A, al, act, b0, n=1, expansions=25, max_depth=4, mode=O.MODE_EXACT)
+    rt = r["root_trace"]
+    assert r["n_exp"] >= 5
+    assert np.all(np.diff(rt[:, 0]) <= 1e-12) and np.all(np.diff(rt[:, 1]) >= -1e-12)
+    assert np.all(rt[:, 1] <= rt[:, 0] + 1e-9)
+    assert rt[-1, 0] - rt[-1, 1] < rt[0, 0] - rt[0, 1]
+    v = r["v"]
+    assert np.all(v["L"] <= v["U"] + 1e-9)
+
+
+def test_bf_E_pointer_is_a_leaf_and_H_is_its_discounted_gap():
+    """Alg. 6/7 carry H upward as gamma w H of the selected child: root H = prod(gamma w) H(E)
+    along the path to E = root.E, and E is an unexpanded V-node."""
+    gm = W.random_map(6, 8, 0.2, seed=9)
+    m = O.Model.grid(gm, action_mask=W.A8, acc=0.9)
+    b0 = W.uniform_belief(gm)
+    A, al, act = _bounds(m, gm, b0)
+    r = m.best_first(A, al, act, b0, n=8, expansions=12, max_depth=5, seed=4)
+    v = r["v"]
+    e = int(v["E"][0])
+    assert v["expanded"][e] == 0
+    path = int(v["path"][e])
+    by_path = {int(p): i for i, p in enumerate(v["path"])}
+    prod = 1.0
+    for lvl in range(int(v["depth"][e])):         # ancestors' children along the path
+        sub = path & ((1 << (8 * (lvl + 1))) - 1)
+        prod *= 0.95 * v["w"][by_path[sub]]
+    assert v["H"][0] == pytest.approx(prod * v["H"][e], rel=1e-12, abs=1e-15)
+    assert v["H"][0] >= 0.0
+
+
+def test_bf_degenerate_bounds_stop_at_once():
+    """Identity O: FIB = MDP and PBVI reaches the MDP values at the point masses, so
+    the root gap is 0 and planning finishes before any expansion (SPEC new_tree example)."""
+    m = _chain()
+    b0 = np.eye(5)[0]
+    _, A, _, _ = m.fib(1e-12)
+    pts, al, act = m.pbvi(b0, expansions=6, max_points=8, seed=3, sweeps=400)
+    r = m.best_first(A, al, act, b0, n=4, expansions=10, gap_tol=1e-6)
+    assert r["stop"] == 1 and r["n_exp"] == 0
