@@ -213,6 +213,50 @@ QVTS_API qvts_status qvts_trace_leaf_values(const qvts_model *model, double *V /
 QVTS_API qvts_status qvts_trace_counts(const qvts_model *model, int32_t *depth, int64_t *n_v, int64_t *n_qwork);
 QVTS_API qvts_status qvts_trace_belief(const qvts_model *model, int32_t level, int64_t index, float *out_host);
 
+/* ---- (4b) anytime best-first QVTS (Alg. 1 inner loop + Algs. 2-7, Eq. 8; PAPER.md:130-298;
+ * SURVEY §8(f) NEXT-2; reading B5) -------------------------------------------------
+ * Tree s = QVSearchTree(b0): one leaf with U = V_FIB(b0), L = V_PBVI(b0), H = U - L, E = itself
+ * (Alg. 5).  Each iteration expands v = root.E (Alg. 2: all |A| Q-nodes; Alg. 3: n draws keyed as
+ * in qvts_plan_step, one child per unique z, weight f/n, Eq. 3 posterior, Alg. 5 leaf bounds),
+ * then updates v and its ancestors to the root: Alg. 6 with gamma (U_Q = R + gamma sum w U,
+ * L_Q likewise; H_Q = gamma w H of the child maximising it; E_Q = its E), Alg. 7 (U = max U_Q,
+ * L = max L_Q; H, E of the argmax-U_Q child).  Ties go to the lowest index.  planningFinished():
+ * max_expansions reached, root U - L <= gap_tol, root.E at max_depth (terminal, H = 0), the node
+ * pool full, or time_budget_ms (> 0) elapsed.  getOptimalAction(): max L_Q, ties by U_Q then
+ * index; an unexpanded root takes the action of its PBVI arg-max vector.
+ * Needs qvts_fib_iteration and qvts_pbvi.  root_dev: device fp32 [H*W].  Node beliefs stay in
+ * HBM (H*W*4 bytes each); the pool holds 1 + max_expansions*|A|*min(n,16) V-nodes, capped at
+ * half the free device memory.  Synchronises `stream` once or twice per expansion. */
+typedef struct {
+    int32_t n_samples;        /* draws per Q-node, 1..4096                                  */
+    uint32_t seed, step, episode;
+    int32_t sampler;          /* qvts_sampler                                               */
+    int32_t max_expansions;   /* >= 0                                                       */
+    int32_t max_depth;        /* 1..8                                                       */
+    double gap_tol;           /* stop once root U - L <= gap_tol                            */
+    double time_budget_ms;    /* > 0: also stop after this much wall-clock time (anytime)   */
+} qvts_bf_cfg;
+typedef enum { QVTS_BF_BUDGET = 0, QVTS_BF_GAP = 1, QVTS_BF_TERMINAL = 2, QVTS_BF_POOL = 3, QVTS_BF_TIME = 4 } qvts_bf_stop;
+typedef struct {
+    int32_t action;           /* stencil id                                                 */
+    int32_t n_actions;
+    int32_t n_expansions;
+    int32_t stop_reason;      /* qvts_bf_stop                                               */
+    int64_t n_vnodes;
+    double U, L;              /* root bounds                                                */
+    double u_q[9], l_q[9];    /* root Q-node bounds (NaN while the root is unexpanded)      */
+    double device_ms;         /* CUDA-event time from the first to the last kernel          */
+} qvts_bf_result;
+QVTS_API qvts_status qvts_plan_best_first(qvts_model *model, const float *root_dev, const qvts_bf_cfg *cfg,
+                                          qvts_bf_result *res, void *stream);
+/* The last best-first tree (any pointer may be NULL): per V-node [n_v] path, depth, sampled count
+ * f, U, L, H, E (node index), expanded (0/1); exp_order [n_expansions] = expanded node indices in
+ * order; root_trace [(n_expansions+1)][2] = root (U, L) before the first and after each expansion. */
+QVTS_API qvts_status qvts_trace_best_first(const qvts_model *model, int64_t *n_v, int32_t *n_expansions,
+                                           uint64_t *path, int32_t *depth, int32_t *f, double *U, double *L,
+                                           double *H, int32_t *E, int32_t *expanded, int32_t *exp_order,
+                                           double *root_trace);
+
 /* ---- (5) closed-loop episodes (Alg. 1 outer loop) -----
  * Each episode e draws x0 ~ b0 and then repeats: plan (QVTS over all active episodes at once,
  * or MDP on the belief mode), true motion y ~ T'(x,a,.) (an occupied/off-map y is a collision

@@ -542,6 +542,16 @@ extern "C" void qvts_model_destroy(qvts_model *m) {
     }
     for (cudaEvent_t e : m->evpool) cudaEventDestroy(e);
     for (auto &v : m->vl) { v.path.release(); v.parent_q.release(); v.z.release(); v.f.release(); v.root.release(); v.V.release(); v.belief.release(); }
+    for (DevBuf *b : {&m->bf_bel, &m->bf_path, &m->bf_pq, &m->bf_z, &m->bf_f, &m->bf_root, &m->bf_depth, &m->bf_vU,
+                      &m->bf_vL, &m->bf_vH, &m->bf_vE, &m->bf_vq0, &m->bf_vLa, &m->bf_qR, &m->bf_qU, &m->bf_qL,
+                      &m->bf_qH, &m->bf_qE, &m->bf_qc0, &m->bf_qnc, &m->bf_qv, &m->bf_VT, &m->bf_part, &m->bf_sum,
+                      &m->bf_keys})
+        b->release();
+    {
+        QLevel &q = m->bf_ql;
+        q.vmap.release(); q.R.release(); q.P.release(); q.cnt.release(); q.umask.release(); q.U.release();
+        q.off.release(); q.Q.release(); q.zdraw.release(); q.leafV.release();
+    }
     for (auto &q : m->ql) { q.vmap.release(); q.R.release(); q.P.release(); q.cnt.release(); q.umask.release(); q.U.release(); q.off.release(); q.Q.release(); q.zdraw.release(); q.leafV.release(); }
     if (m->ev0) cudaEventDestroy(m->ev0);
     if (m->ev1) cudaEventDestroy(m->ev1);

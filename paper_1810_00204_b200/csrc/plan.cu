@@ -1271,6 +1271,101 @@ static qvts_status correct_selected_t(Model &m, const RootBatch &roots, const in
     return QVTS_OK;
 }
 
+// ---- explicit V-node batches (best-first QVTS, bestfirst.cu) --------------------------------------
+// S1-S3 of `nwork` V-nodes of one level (the same kernels and Philox keys as plan_levels), then the
+// exclusive child offsets; *total = number of children (synchronises `st`).
+template <uint32_t MASK>
+static qvts_status expand_marginals_t(Model &m, const ExpandSpec &e, QLevel &ql, cudaStream_t st, long long *total) {
+    constexpr int NA = mask_count(MASK);
+    const long long nwork = e.nwork, nq = nwork * NA;
+    ql.nwork = nwork;
+    ql.mapped = false;
+    ql.vmap_ptr = nullptr;
+    QVTS_TRY(ql.R.ensure(sizeof(double) * nq));
+    QVTS_TRY(ql.P.ensure(sizeof(double) * 16 * nq));
+    QVTS_TRY(ql.cnt.ensure(sizeof(uint16_t) * 16 * nq));
+    QVTS_TRY(ql.umask.ensure(sizeof(uint16_t) * nq));
+    QVTS_TRY(ql.U.ensure(sizeof(int32_t) * nq));
+    QVTS_TRY(ql.off.ensure(sizeof(int32_t) * nq));
+    QVTS_TRY(ql.Q.ensure(sizeof(double) * nq));
+    QVTS_TRY(m.counters.ensure(sizeof(unsigned long long) * 4));
+    QVTS_TRY(m.total.ensure(sizeof(long long)));
+    const BandSet &bs = m.band_small;
+    const int pstride = pstride_of<MASK>(false);
+    QVTS_TRY(m.part.ensure(sizeof(double) * (size_t)(nwork + 1) * bs.nb * pstride));
+    ReduceArgs r;
+    std::memset(&r, 0, sizeof(r));
+    r.part = m.part.as<double>(); r.pstride = pstride; r.nb = bs.nb; r.nwork = nwork; r.vmap = nullptr;
+    r.beliefs = e.beliefs; r.bstride = e.bstride; r.vpath = e.vpath; r.vroot = e.vroot;
+    r.root_step = e.root_step; r.root_ep = e.root_ep; r.seed = e.seed; r.level = e.level; r.n = e.n;
+    r.O64 = m.d_O64.as<double>(); r.ngc = m.ngc; r.gc_cell = m.d_gc_cell.as<int32_t>();
+    r.gc_act = m.d_gc_act.as<int32_t>(); r.gc_val = m.d_gc_val.as<double>(); r.goal = m.goal;
+    r.p_stay = m.p_stay; r.p_int = m.p_int; r.p_lat = m.p_lat; r.gamma = m.gamma;
+    r.R = ql.R.as<double>(); r.P = ql.P.as<double>(); r.cnt = ql.cnt.as<uint16_t>();
+    r.umask = ql.umask.as<uint16_t>(); r.U = ql.U.as<int32_t>(); r.Q = ql.Q.as<double>();
+    r.counters = m.counters.as<unsigned long long>();
+    r.m8 = m.d_m8.as<uint8_t>(); r.sig = m.d_sig.as<uint8_t>(); r.W = m.W; r.acc = m.acc;
+    if (e.sampler == QVTS_SAMPLER_ANCESTRAL) {
+        QVTS_TRY(m.xs.ensure(sizeof(int32_t) * (size_t)nq * e.n));
+        const int nch = (m.HW + 255) / 256;
+        QVTS_PROF(7, k_ancestral_x<MASK><<<(unsigned)nwork, 256, sizeof(double) * (2 * nch + 1), st>>>(
+                         e.beliefs, e.bstride, nullptr, nwork, m.HW, e.vpath, e.vroot, e.root_step, e.root_ep,
+                         e.seed, e.level, e.n, m.xs.as<int32_t>()));
+        QVTS_CUDA(cudaGetLastError());
+        r.xs = m.xs.as<int32_t>();
+    }
+    int nb_eff = bs.nb;
+    QVTS_TRY((launch_hist<MASK, false>(m, bs, e.beliefs, e.bstride, nullptr, nwork, pstride, st, &nb_eff)));
+    r.nb = nb_eff;
+    QVTS_TRY((launch_reduce<MASK, false>(m, r, st)));
+    QVTS_PROF(4, k_scan<<<1, 1024, 0, st>>>(ql.U.as<int32_t>(), ql.off.as<int32_t>(), nq, m.total.as<long long>()));
+    QVTS_CUDA(cudaGetLastError());
+    QVTS_CUDA(cudaMemcpyAsync(total, m.total.p, sizeof(long long), cudaMemcpyDeviceToHost, st));
+    QVTS_CUDA(cudaStreamSynchronize(st));
+    return QVTS_OK;
+}
+
+// S4 of the batch prepared by expand_marginals: child j of Q-node q lands at off[q] + j.
+template <uint32_t MASK>
+static qvts_status expand_children_t(Model &m, const ExpandSpec &e, const QLevel &ql, const ChildOut &o,
+                                     cudaStream_t st) {
+    constexpr int NA = mask_count(MASK);
+    CorrectArgs c;
+    std::memset(&c, 0, sizeof(c));
+    c.beliefs = e.beliefs; c.bstride = e.bstride; c.vmap = nullptr;
+    c.m8 = m.d_m8.as<uint8_t>(); c.cell = m.d_cell.as<uint8_t>();
+    c.O64 = m.d_O64.as<double>(); c.P = ql.P.as<double>(); c.cnt = ql.cnt.as<uint16_t>();
+    c.umask = ql.umask.as<uint16_t>(); c.off = ql.off.as<int32_t>();
+    c.vpath = e.vpath; c.vroot = e.vroot; c.level = e.level;
+    c.child = o.belief; c.cstride = o.stride;
+    c.cpath = o.path; c.cparent = o.parent_q; c.cz = o.z; c.cf = o.f; c.croot = o.root;
+    c.H = m.H; c.W = m.W; c.G = (m.W + 3) / 4;
+    c.rows_cta = correct_rows_per_cta(m.H, c.G);
+    c.ntiles = (m.H + c.rows_cta - 1) / c.rows_cta;
+    c.p_int = (float)m.p_int; c.p_stay = (float)m.p_stay; c.p_lat = (float)m.p_lat; c.qsel = -1;
+    const long long nblocks = e.nwork * NA * c.ntiles;
+    if (nblocks > 0x7FFFFFFFLL) { set_error("too many correct blocks"); return QVTS_ERR_INVALID_ARG; }
+    QVTS_PROF(5, k_correct<MASK><<<(unsigned)nblocks, 256, 0, st>>>(c));
+    QVTS_CUDA(cudaGetLastError());
+    return QVTS_OK;
+}
+
+qvts_status expand_marginals(Model &m, const ExpandSpec &e, QLevel &ql, cudaStream_t st, long long *total) {
+    qvts_status s = QVTS_ERR_INVALID_ARG;
+#define QVTS_EM(MASK) s = expand_marginals_t<MASK>(m, e, ql, st, total)
+    QVTS_DISPATCH_MASK(m.mask, QVTS_EM);
+#undef QVTS_EM
+    return s;
+}
+
+qvts_status expand_children(Model &m, const ExpandSpec &e, const QLevel &ql, const ChildOut &o, cudaStream_t st) {
+    qvts_status s = QVTS_ERR_INVALID_ARG;
+#define QVTS_EC(MASK) s = expand_children_t<MASK>(m, e, ql, o, st)
+    QVTS_DISPATCH_MASK(m.mask, QVTS_EC);
+#undef QVTS_EC
+    return s;
+}
+
 qvts_status root_marginals(Model &m, const RootBatch &roots, cudaStream_t st) {
     qvts_status s = QVTS_ERR_INVALID_ARG;
 #define QVTS_RM(MASK) s = root_marginals_t<MASK>(m, roots, st)

@@ -117,6 +117,16 @@ struct Model {
     int pb_np = 0, pb_nal = 0, pb_P = 0;
     std::vector<int32_t> pb_act;
     DevBuf pb_b0, pb_B, pb_G, pb_Gn, pb_GT, pb_Bbar, pb_Sc, pb_Rb, pb_sel, pb_astar, pb_cand, pb_misc, pb_cls;
+    // anytime best-first QVTS (NEXT-2, bestfirst.cu): node pool of the last qvts_plan_best_first
+    bool bf_valid = false;
+    long long bf_nv = 0, bf_nq = 0;
+    int bf_nexp = 0;
+    DevBuf bf_bel, bf_path, bf_pq, bf_z, bf_f, bf_root, bf_depth, bf_vU, bf_vL, bf_vH, bf_vE, bf_vq0, bf_vLa;
+    DevBuf bf_qR, bf_qU, bf_qL, bf_qH, bf_qE, bf_qc0, bf_qnc, bf_qv;
+    DevBuf bf_VT, bf_part, bf_sum, bf_keys;
+    QLevel bf_ql;
+    std::vector<int32_t> bf_exp;          // expanded V-node ids, in order
+    std::vector<double> bf_rtrace;        // root (U, L) after 0, 1, ... expansions
 };
 
 // instrumentation helpers (model.cu)
@@ -142,6 +152,25 @@ qvts_status plan_levels(Model &m, const RootBatch &roots, const qvts_plan_cfg &c
                         cudaStream_t st, long long *nv_out /*[depth+1]*/);
 // P(z|b,a) and R(b,a) of the (active) roots only, into ql[0] (S1+S2 without sampling)
 qvts_status root_marginals(Model &m, const RootBatch &roots, cudaStream_t st);
+// Explicit V-node batch of one level (best-first QVTS): S1-S3 + child offsets, then S4.
+struct ExpandSpec {
+    const float *beliefs;
+    long long bstride, nwork;
+    const uint64_t *vpath;
+    const int32_t *vroot;
+    const uint32_t *root_step, *root_ep;
+    int level, n;
+    uint32_t seed;
+    int sampler;
+};
+struct ChildOut {
+    float *belief;
+    long long stride;
+    uint64_t *path;
+    int32_t *parent_q, *z, *f, *root;
+};
+qvts_status expand_marginals(Model &m, const ExpandSpec &e, QLevel &ql, cudaStream_t st, long long *total);
+qvts_status expand_children(Model &m, const ExpandSpec &e, const QLevel &ql, const ChildOut &o, cudaStream_t st);
 // Bayes correction of selected (Q-node, z) pairs of level 0 into out[sel_out[g]*ostride]
 qvts_status correct_selected(Model &m, const RootBatch &roots, const int32_t *sel_q, const int32_t *sel_z,
                              const int32_t *sel_out, long long n, float *out, long long ostride, cudaStream_t st);

@@ -24,8 +24,9 @@ EXPORTS = [
     "qvts_value_iteration", "qvts_get_q", "qvts_belief_update", "qvts_plan_step", "qvts_trace_qnodes",
     "qvts_trace_vnodes", "qvts_trace_leaf_values", "qvts_trace_belief", "qvts_run_episodes",
     "qvts_trace_counts", "qvts_set_profiling", "qvts_get_profile", "qvts_fib_iteration", "qvts_get_alpha",
-    "qvts_pbvi", "qvts_get_pbvi",
+    "qvts_pbvi", "qvts_get_pbvi", "qvts_plan_best_first", "qvts_trace_best_first",
 ]
+QVTS_BF_BUDGET, QVTS_BF_GAP, QVTS_BF_TERMINAL, QVTS_BF_POOL, QVTS_BF_TIME = 0, 1, 2, 3, 4
 QVTS_LEAF_QMDP, QVTS_LEAF_FIB = 0, 1
 QVTS_SAMPLER_MARGINAL, QVTS_SAMPLER_ANCESTRAL = 0, 1
 
@@ -53,6 +54,18 @@ class qvts_plan_result(C.Structure):
     _fields_ = [("action", C.c_int32), ("n_actions", C.c_int32), ("q_root", C.c_double * 9),
                 ("n_vnodes", C.c_int64 * 9), ("n_belief_updates", C.c_int64), ("device_ms", C.c_double),
                 ("shard_level", C.c_int32)]
+
+
+class qvts_bf_cfg(C.Structure):
+    _fields_ = [("n_samples", C.c_int32), ("seed", C.c_uint32), ("step", C.c_uint32), ("episode", C.c_uint32),
+                ("sampler", C.c_int32), ("max_expansions", C.c_int32), ("max_depth", C.c_int32),
+                ("gap_tol", C.c_double), ("time_budget_ms", C.c_double)]
+
+
+class qvts_bf_result(C.Structure):
+    _fields_ = [("action", C.c_int32), ("n_actions", C.c_int32), ("n_expansions", C.c_int32),
+                ("stop_reason", C.c_int32), ("n_vnodes", C.c_int64), ("U", C.c_double), ("L", C.c_double),
+                ("u_q", C.c_double * 9), ("l_q", C.c_double * 9), ("device_ms", C.c_double)]
 
 
 class qvts_profile(C.Structure):
@@ -108,6 +121,8 @@ def lib() -> C.CDLL:
         L.qvts_get_alpha.argtypes = [vp, vp]
         L.qvts_pbvi.argtypes = [vp, vp, C.c_int32, C.c_int32, C.c_uint32, C.c_int32, C.POINTER(C.c_int32), vp]
         L.qvts_get_pbvi.argtypes = [vp, vp, vp, vp, C.POINTER(C.c_int32)]
+        L.qvts_plan_best_first.argtypes = [vp, vp, C.POINTER(qvts_bf_cfg), C.POINTER(qvts_bf_result), vp]
+        L.qvts_trace_best_first.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int32)] + [vp] * 10
         L.qvts_belief_update.argtypes = [vp, vp, C.c_int32, C.c_int32, vp, C.POINTER(C.c_double), vp]
         L.qvts_plan_step.argtypes = [vp, vp, C.POINTER(qvts_plan_cfg), C.POINTER(qvts_comm),
                                      C.POINTER(qvts_plan_result), vp]
@@ -226,6 +241,28 @@ def qvts_get_pbvi(h, n_points, n_cells):
     act = np.zeros(n_points, np.int32)
     _check(lib().qvts_get_pbvi(h, pts.ctypes.data, al.ctypes.data, act.ctypes.data, None), "qvts_get_pbvi")
     return pts, al, act
+
+
+def qvts_plan_best_first(h, root_dev, n_samples, max_expansions, max_depth=8, gap_tol=0.0, seed=1, step=0,
+                         episode=0, sampler=QVTS_SAMPLER_MARGINAL, time_budget_ms=0.0, stream=None):
+    cfg = qvts_bf_cfg(n_samples, seed, step, episode, sampler, max_expansions, max_depth, gap_tol, time_budget_ms)
+    res = qvts_bf_result()
+    _check(lib().qvts_plan_best_first(h, _ptr(root_dev), C.byref(cfg), C.byref(res), _stream(stream)),
+           "qvts_plan_best_first")
+    return res
+
+
+def qvts_trace_best_first(h):
+    """-> dict: per V-node arrays path/depth/f/U/L/H/E/expanded, exp_order, root_trace [(U, L)]."""
+    nv, ne = C.c_int64(), C.c_int32()
+    _check(lib().qvts_trace_best_first(h, C.byref(nv), C.byref(ne), *([None] * 10)), "qvts_trace_best_first")
+    n, k = nv.value, ne.value
+    out = dict(path=np.zeros(n, np.uint64), depth=np.zeros(n, np.int32), f=np.zeros(n, np.int32),
+               U=np.zeros(n), L=np.zeros(n), H=np.zeros(n), E=np.zeros(n, np.int32),
+               expanded=np.zeros(n, np.int32), exp_order=np.zeros(k, np.int32), root_trace=np.zeros((k + 1, 2)))
+    order = ("path", "depth", "f", "U", "L", "H", "E", "expanded", "exp_order", "root_trace")
+    _check(lib().qvts_trace_best_first(h, None, None, *[out[o].ctypes.data for o in order]), "qvts_trace_best_first")
+    return out
 
 
 def qvts_belief_update(h, b_dev, action, z, out_dev, stream=None):
@@ -406,6 +443,13 @@ class Model:
 
     def plan_step(self, root_dev, depth, n_samples, **kw):
         return qvts_plan_step(self.h, root_dev, depth, n_samples, **kw)
+
+    def plan_best_first(self, root_dev, n_samples, max_expansions, **kw):
+        """Anytime best-first QVTS (needs fib_iteration and pbvi first)."""
+        return qvts_plan_best_first(self.h, root_dev, n_samples, max_expansions, **kw)
+
+    def trace_best_first(self):
+        return qvts_trace_best_first(self.h)
 
     def run_episodes(self, n_episodes, **kw):
         return qvts_run_episodes(self.h, n_episodes, **kw)

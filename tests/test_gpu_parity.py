@@ -318,3 +318,71 @@ def test_pbvi_zero_sweeps_and_single_point(Q):
     opts, oal, _ = o.pbvi(np.asarray(W.uniform_belief(gm), np.float64), expansions=0, max_points=8, seed=1, sweeps=0)
     assert np.max(np.abs(pts - opts)) <= 1e-15 and np.max(np.abs(al - oal)) == 0.0
     g.close()
+
+
+def _bf_pair(Q, gm, mask, b32, pbvi_kw):
+    g = Q.Model(gm, action_mask=mask)
+    o = O.Model.grid(gm, action_mask=mask)
+    code, _, _ = g.fib_iteration(1e-9)
+    assert code == 0
+    g.pbvi(dev(b32), **pbvi_kw)
+    st, Ao, _, _ = o.fib(1e-9)
+    _, alo, acto = o.pbvi(b32.astype(np.float64), **pbvi_kw)
+    return g, o, Ao, alo, acto
+
+
+@pytest.mark.parametrize("name,n,exps,maxd", [("C1", 8, 25, 4), ("ragged", 16, 30, 5), ("paper", 8, 20, 3)])
+def test_best_first_against_oracle(Q, name, n, exps, maxd):
+    """NEXT-2: the anytime best-first QVTS (Alg. 1-7, Eq. 8) on the GPU against the oracle: same
+    expansion order (near-tied selections replayed, reading B5), every V-node's f, U, L, H, the
+    root Q bounds and the executed action."""
+    gm, mask = MAPS[name][0](), MAPS[name][1]
+    b32 = np.asarray(W.uniform_belief(gm), np.float32)
+    g, o, Ao, alo, acto = _bf_pair(Q, gm, mask, b32, dict(expansions=3, max_points=12, seed=5, sweeps=20))
+    res = g.plan_best_first(dev(b32), n, exps, max_depth=maxd, seed=2, step=1)
+    tr = g.trace_best_first()
+    gpaths = tr["path"][tr["exp_order"]]
+    r = o.best_first(Ao, alo, acto, b32.astype(np.float64), n, exps, max_depth=maxd, seed=2, step=1,
+                     replay=gpaths, replay_tol=1e-4)
+    assert r["mism"] == 0
+    assert r["subs"] <= max(1, exps // 10)
+    assert r["n_exp"] == res.n_expansions and r["stop"] == res.stop_reason
+    assert r["n_v"] == res.n_vnodes
+    ov = r["v"]
+    idx = {int(p): i for i, p in enumerate(ov["path"])}
+    scale = max(1.0, float(np.max(np.abs(ov["U"]))))
+    for i, p in enumerate(tr["path"]):
+        j = idx[int(p)]
+        assert tr["f"][i] == ov["f"][j] and tr["depth"][i] == ov["depth"][j]
+        assert abs(tr["U"][i] - ov["U"][j]) <= PT.TOL * scale
+        assert abs(tr["L"][i] - ov["L"][j]) <= PT.TOL * scale
+        assert abs(tr["H"][i] - ov["H"][j]) <= 2 * PT.TOL * scale
+        assert bool(tr["expanded"][i]) == bool(ov["expanded"][j])
+    assert abs(res.U - r["U"]) <= PT.TOL * scale and abs(res.L - r["L"]) <= PT.TOL * scale
+    na = g.n_actions
+    assert np.max(np.abs(np.array(res.u_q[:na]) - r["UQ"])) <= PT.TOL * scale
+    assert np.max(np.abs(np.array(res.l_q[:na]) - r["LQ"])) <= PT.TOL * scale
+    assert np.max(np.abs(tr["root_trace"] - r["root_trace"])) <= PT.TOL * scale
+    # executed action: max L_Q (ties by U_Q) -- equal, or the oracle's L_Q values are near-tied
+    j = g.action_ids.index(res.action)
+    assert res.action == r["action"] or r["LQ"][j] >= np.max(r["LQ"]) - PT.TIE * scale
+    g.close()
+
+
+def test_best_first_stop_rules(Q):
+    """planningFinished(): zero budget (root = leaf, PBVI action), a huge gap tolerance, the
+    depth cap (terminal E) and the wall-clock budget."""
+    gm, mask = MAPS["ragged"][0](), MAPS["ragged"][1]
+    b32 = np.asarray(W.random_belief(gm, 3), np.float32)
+    g, o, Ao, alo, acto = _bf_pair(Q, gm, mask, b32, dict(expansions=2, max_points=8, seed=1, sweeps=10))
+    res = g.plan_best_first(dev(b32), 8, 0)
+    r = o.best_first(Ao, alo, acto, b32.astype(np.float64), 8, 0)
+    assert res.n_expansions == 0 and res.stop_reason == Q.QVTS_BF_BUDGET and res.action == r["action"]
+    assert abs(res.U - r["U"]) <= 1e-5 * abs(r["U"]) and abs(res.L - r["L"]) <= 1e-5 * abs(r["L"])
+    res = g.plan_best_first(dev(b32), 8, 50, gap_tol=1e9)
+    assert res.n_expansions == 0 and res.stop_reason == Q.QVTS_BF_GAP
+    res = g.plan_best_first(dev(b32), 8, 10000, max_depth=1)
+    assert res.n_expansions == 1 and res.stop_reason == Q.QVTS_BF_TERMINAL
+    res = g.plan_best_first(dev(b32), 8, 100000, max_depth=8, time_budget_ms=30.0)
+    assert res.stop_reason == Q.QVTS_BF_TIME and res.n_expansions > 0
+    g.close()
