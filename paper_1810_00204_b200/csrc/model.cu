@@ -545,7 +545,7 @@ extern "C" void qvts_model_destroy(qvts_model *m) {
     for (DevBuf *b : {&m->bf_bel, &m->bf_path, &m->bf_pq, &m->bf_z, &m->bf_f, &m->bf_root, &m->bf_depth, &m->bf_vU,
                       &m->bf_vL, &m->bf_vH, &m->bf_vE, &m->bf_vq0, &m->bf_vLa, &m->bf_qR, &m->bf_qU, &m->bf_qL,
                       &m->bf_qH, &m->bf_qE, &m->bf_qc0, &m->bf_qnc, &m->bf_qv, &m->bf_VT, &m->bf_part, &m->bf_sum,
-                      &m->bf_keys})
+                      &m->bf_keys, &m->bf_anc, &m->bf_rtr})
         b->release();
     {
         QLevel &q = m->bf_ql;
@@ -553,6 +553,9 @@ extern "C" void qvts_model_destroy(qvts_model *m) {
         q.off.release(); q.Q.release(); q.zdraw.release(); q.leafV.release();
     }
     for (auto &q : m->ql) { q.vmap.release(); q.R.release(); q.P.release(); q.cnt.release(); q.umask.release(); q.U.release(); q.off.release(); q.Q.release(); q.zdraw.release(); q.leafV.release(); }
+    if (m->bf_gexec) cudaGraphExecDestroy(m->bf_gexec);
+    if (m->bf_stream) cudaStreamDestroy(m->bf_stream);
+    if (m->bf_join) cudaEventDestroy(m->bf_join);
     if (m->ev0) cudaEventDestroy(m->ev0);
     if (m->ev1) cudaEventDestroy(m->ev1);
     delete m;

@@ -81,7 +81,13 @@ struct ReduceArgs {
     const uint8_t *m8, *sig;
     int W;
     double acc;
+    const int32_t *skip = nullptr;  // device flag: non-zero -> the launch does nothing (best-first)
 };
+
+// tree level of a V-node path: one non-zero byte per action level (low nibble a+1 >= 1)
+__device__ __forceinline__ int path_level(uint64_t vpath) {
+    return vpath ? (64 - __clzll((long long)vpath) + 7) >> 3 : 0;
+}
 
 // Alg. 4 steps 2-3 for one sample: x' ~ T(x,a,.) on u2 over the clamped row in stencil order
 // (blocked targets merged into the stay entry at first occurrence), then z ~ O(x',.) on u3
@@ -233,7 +239,8 @@ __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int
         C[z] = acc;
     }
     // S3: n draws keyed by the tree path (Appendix A.2-A.5)
-    const uint64_t qpath = vpath | ((uint64_t)(k + 1) << (8 * a.level));
+    const int level = a.level >= 0 ? a.level : path_level(vpath);   // level < 0: from the path
+    const uint64_t qpath = vpath | ((uint64_t)(k + 1) << (8 * level));
     int cntk = 0;
     for (int j0 = 0; j0 < a.n; j0 += 32) {
         const int jj = j0 + lane;
@@ -340,6 +347,7 @@ __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int
 template <uint32_t MASK, bool LEAF>
 __global__ void __launch_bounds__(mask_count(MASK) * 32) k_reduce(ReduceArgs a) {
     extern __shared__ double rsm[];
+    if (a.skip && *a.skip) return;
     reduce_parent<MASK, LEAF>(a, blockIdx.x, rsm, mask_count(MASK) * 32);
 }
 
@@ -352,10 +360,12 @@ __global__ void __launch_bounds__(256) k_ancestral_x(const float *__restrict__ b
                                                      const int32_t *vmap, long long nwork, int HW,
                                                      const uint64_t *vpath, const int32_t *vroot,
                                                      const uint32_t *root_step, const uint32_t *root_ep,
-                                                     uint32_t seed, int level, int n, int32_t *xs) {
+                                                     uint32_t seed, int level, int n, int32_t *xs,
+                                                     const int32_t *skip = nullptr) {
     constexpr int NA = mask_count(MASK);
     constexpr int CH = 256;
     extern __shared__ double sx[];   // [nch] chunk sums, then exclusive prefix in place
+    if (skip && *skip) return;
     const long long w = blockIdx.x;
     const long long v = vmap ? (long long)vmap[w] : w;
     const float *__restrict__ b = beliefs + v * bstride;
@@ -380,6 +390,7 @@ __global__ void __launch_bounds__(256) k_ancestral_x(const float *__restrict__ b
     __syncthreads();
     const double total = cpre[nch];
     const uint64_t vp = vpath[v];
+    if (level < 0) level = path_level(vp);
     const int root = vroot[v];
     const uint32_t step = root_step[root], ep = root_ep[root];
     for (int idx = threadIdx.x; idx < NA * n; idx += 256) {
@@ -441,6 +452,7 @@ struct HistArgs {
     int fused;            // 1: the last band CTA of a pair runs reduce_parent (tickets[pair])
     int *tickets;
     ReduceArgs red;
+    const int32_t *skip = nullptr;  // device flag (best-first)
 };
 
 template <uint32_t MASK, bool LEAF>
@@ -453,6 +465,7 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_hist(HistArgs a) {
     constexpr int T = kHistThreads;
     constexpr int ZB = 9, HQ = 9 + NA;               // offsets in the flat accumulator array
     extern __shared__ float4 smem4[];
+    if (a.skip && *a.skip) return;
     float *smem = reinterpret_cast<float *>(smem4);
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int p = lane >> 4;                       // parent of this half-warp
@@ -692,9 +705,10 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_hist(HistArgs a) {
 
 // ---- child offsets: single-CTA exclusive scan -------------------------------------------------
 __global__ void __launch_bounds__(1024) k_scan(const int32_t *__restrict__ U, int32_t *__restrict__ off, long long n,
-                                               long long *total) {
+                                               long long *total, const int32_t *skip = nullptr) {
     __shared__ long long wsum[32];
     __shared__ long long carry_s;
+    if (skip && *skip) return;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     if (t == 0) carry_s = 0;
     __syncthreads();
@@ -752,6 +766,8 @@ struct CorrectArgs {
     float p_int, p_stay, p_lat;
     long long qsel;   // >= 0: only this Q-node (belief_update)
     const int32_t *sel_q, *sel_z, *sel_out;   // optional per-block-group selection (episodes)
+    const int32_t *skip = nullptr;             // device flag (best-first)
+    const long long *cbase_dev = nullptr;      // device child-index base (best-first pool)
 };
 
 // bbar_a for 4 consecutive cells (r, c0..c0+3): bbar = p_stay b + p_int h_a + p_lat (h_l1 + h_l2),
@@ -798,6 +814,7 @@ __device__ __forceinline__ void correct_predict(const CorrectArgs &a, int r, int
 template <uint32_t MASK>
 __global__ void __launch_bounds__(256) k_correct(CorrectArgs a) {
     constexpr int NA = mask_count(MASK);
+    if (a.skip && *a.skip) return;
     const long long grp = blockIdx.x / a.ntiles;
     const long long q = a.sel_q ? (long long)a.sel_q[grp] : (a.qsel >= 0 ? a.qsel : grp);
     const int tile = blockIdx.x % a.ntiles;
@@ -807,7 +824,8 @@ __global__ void __launch_bounds__(256) k_correct(CorrectArgs a) {
     const long long v = a.vmap ? (long long)a.vmap[w] : w;
     const unsigned um = a.sel_q ? (1u << a.sel_z[grp]) : a.umask[q];
     const int U = __popc(um);
-    const long long base = a.sel_q ? (long long)a.sel_out[grp] : (a.qsel >= 0 ? 0 : a.off[q]);
+    const long long base = (a.sel_q ? (long long)a.sel_out[grp] : (a.qsel >= 0 ? 0 : a.off[q])) +
+                           (a.cbase_dev ? *a.cbase_dev : 0);
     __shared__ float s_w[16][16];   // [rank u][signature s] = O[s][z_u] / P(z_u)
     {
         const int t = threadIdx.x;
@@ -819,7 +837,8 @@ __global__ void __launch_bounds__(256) k_correct(CorrectArgs a) {
             s_w[u][sg] = (float)(a.O64[sg * 16 + z] / a.P[q * 16 + z]);
             if (tile == 0 && sg == 0 && a.cpath) {
                 const long long c = base + u;
-                a.cpath[c] = a.vpath[v] | ((uint64_t)(k + 1) << (8 * a.level)) | ((uint64_t)z << (8 * a.level + 4));
+                const int level = a.level >= 0 ? a.level : path_level(a.vpath[v]);
+                a.cpath[c] = a.vpath[v] | ((uint64_t)(k + 1) << (8 * level)) | ((uint64_t)z << (8 * level + 4));
                 a.cparent[c] = (int32_t)q;
                 a.cz[c] = z;
                 a.cf[c] = a.cnt[q * 16 + z];
@@ -951,9 +970,11 @@ static inline int correct_rows_per_cta(int H, int G) {
 template <uint32_t MASK, bool LEAF>
 static qvts_status launch_hist(Model &m, const BandSet &bs, const float *beliefs, long long bstride,
                                const int32_t *vmap, long long nwork, int pstride, cudaStream_t st, int *nb_eff,
-                               const ReduceArgs *red = nullptr, bool *fused_out = nullptr) {
+                               const ReduceArgs *red = nullptr, bool *fused_out = nullptr,
+                               const int32_t *skip = nullptr) {
     constexpr int NOUT = 16 * hist_cb<MASK, LEAF>() + 8;
     HistArgs a;
+    a.skip = skip;
     a.beliefs = beliefs; a.bstride = bstride; a.vmap = vmap; a.nwork = nwork;
     a.bands = bs.bands.as<BandInfo>(); a.nb = bs.nb;
     a.entries = bs.entries.as<uint32_t>();
@@ -1348,6 +1369,89 @@ static qvts_status expand_children_t(Model &m, const ExpandSpec &e, const QLevel
     QVTS_PROF(5, k_correct<MASK><<<(unsigned)nblocks, 256, 0, st>>>(c));
     QVTS_CUDA(cudaGetLastError());
     return QVTS_OK;
+}
+
+// One best-first expansion with every index on the device, so the launches can be captured in a
+// CUDA graph: the V-node *L.sel of the pool (its level read from its path) gets S1-S3, the child
+// offsets (*L.total = child count) and S4 into the pool at *L.cbase + off; while *L.skip is set
+// every launch returns at once.
+template <uint32_t MASK>
+static qvts_status bf_expand_launch_t(Model &m, const BfLaunch &L, QLevel &ql, cudaStream_t st) {
+    constexpr int NA = mask_count(MASK);
+    const BandSet &bs = m.band_small;
+    const int pstride = pstride_of<MASK>(false);
+    ReduceArgs r;
+    std::memset(&r, 0, sizeof(r));
+    r.part = m.part.as<double>(); r.pstride = pstride; r.nb = bs.nb; r.nwork = 1; r.vmap = L.sel;
+    r.beliefs = L.bel; r.bstride = L.stride; r.vpath = L.path; r.vroot = L.root;
+    r.root_step = L.root_step; r.root_ep = L.root_ep; r.seed = L.seed; r.level = -1; r.n = L.n;
+    r.O64 = m.d_O64.as<double>(); r.ngc = m.ngc; r.gc_cell = m.d_gc_cell.as<int32_t>();
+    r.gc_act = m.d_gc_act.as<int32_t>(); r.gc_val = m.d_gc_val.as<double>(); r.goal = m.goal;
+    r.p_stay = m.p_stay; r.p_int = m.p_int; r.p_lat = m.p_lat; r.gamma = m.gamma;
+    r.R = ql.R.as<double>(); r.P = ql.P.as<double>(); r.cnt = ql.cnt.as<uint16_t>();
+    r.umask = ql.umask.as<uint16_t>(); r.U = ql.U.as<int32_t>(); r.Q = ql.Q.as<double>();
+    r.counters = m.counters.as<unsigned long long>();
+    r.m8 = m.d_m8.as<uint8_t>(); r.sig = m.d_sig.as<uint8_t>(); r.W = m.W; r.acc = m.acc;
+    r.skip = L.skip;
+    if (L.sampler == QVTS_SAMPLER_ANCESTRAL) {
+        const int nch = (m.HW + 255) / 256;
+        QVTS_PROF(7, k_ancestral_x<MASK><<<1, 256, sizeof(double) * (2 * nch + 1), st>>>(
+                         L.bel, L.stride, L.sel, 1, m.HW, L.path, L.root, L.root_step, L.root_ep, L.seed, -1, L.n,
+                         m.xs.as<int32_t>(), L.skip));
+        QVTS_CUDA(cudaGetLastError());
+        r.xs = m.xs.as<int32_t>();
+    }
+    int nb_eff = bs.nb;
+    QVTS_TRY((launch_hist<MASK, false>(m, bs, L.bel, L.stride, L.sel, 1, pstride, st, &nb_eff, nullptr, nullptr,
+                                       L.skip)));
+    r.nb = nb_eff;
+    QVTS_TRY((launch_reduce<MASK, false>(m, r, st)));
+    QVTS_PROF(4, k_scan<<<1, 1024, 0, st>>>(ql.U.as<int32_t>(), ql.off.as<int32_t>(), NA, L.total, L.skip));
+    QVTS_CUDA(cudaGetLastError());
+    CorrectArgs c;
+    std::memset(&c, 0, sizeof(c));
+    c.beliefs = L.bel; c.bstride = L.stride; c.vmap = L.sel;
+    c.m8 = m.d_m8.as<uint8_t>(); c.cell = m.d_cell.as<uint8_t>();
+    c.O64 = m.d_O64.as<double>(); c.P = ql.P.as<double>(); c.cnt = ql.cnt.as<uint16_t>();
+    c.umask = ql.umask.as<uint16_t>(); c.off = ql.off.as<int32_t>();
+    c.vpath = L.path; c.vroot = L.root; c.level = -1;
+    c.child = L.bel; c.cstride = L.stride;
+    c.cpath = L.path; c.cparent = L.pq; c.cz = L.z; c.cf = L.f; c.croot = L.root;
+    c.H = m.H; c.W = m.W; c.G = (m.W + 3) / 4;
+    c.rows_cta = correct_rows_per_cta(m.H, c.G);
+    c.ntiles = (m.H + c.rows_cta - 1) / c.rows_cta;
+    c.p_int = (float)m.p_int; c.p_stay = (float)m.p_stay; c.p_lat = (float)m.p_lat; c.qsel = -1;
+    c.skip = L.skip; c.cbase_dev = L.cbase;
+    QVTS_PROF(5, k_correct<MASK><<<(unsigned)(NA * c.ntiles), 256, 0, st>>>(c));
+    QVTS_CUDA(cudaGetLastError());
+    return QVTS_OK;
+}
+
+qvts_status bf_expand_prepare(Model &m, QLevel &ql, int n, int sampler) {
+    const long long nq = m.NA;
+    QVTS_TRY(ql.R.ensure(sizeof(double) * nq));
+    QVTS_TRY(ql.P.ensure(sizeof(double) * 16 * nq));
+    QVTS_TRY(ql.cnt.ensure(sizeof(uint16_t) * 16 * nq));
+    QVTS_TRY(ql.umask.ensure(sizeof(uint16_t) * nq));
+    QVTS_TRY(ql.U.ensure(sizeof(int32_t) * nq));
+    QVTS_TRY(ql.off.ensure(sizeof(int32_t) * nq));
+    QVTS_TRY(ql.Q.ensure(sizeof(double) * nq));
+    QVTS_TRY(m.counters.ensure(sizeof(unsigned long long) * 4));
+    int pstride = 0;
+#define QVTS_PS(MASK) pstride = pstride_of<MASK>(false)
+    QVTS_DISPATCH_MASK(m.mask, QVTS_PS);
+#undef QVTS_PS
+    QVTS_TRY(m.part.ensure(sizeof(double) * 2 * m.band_small.nb * pstride));
+    if (sampler == QVTS_SAMPLER_ANCESTRAL) QVTS_TRY(m.xs.ensure(sizeof(int32_t) * (size_t)nq * n));
+    return QVTS_OK;
+}
+
+qvts_status bf_expand_launch(Model &m, const BfLaunch &L, QLevel &ql, cudaStream_t st) {
+    qvts_status s = QVTS_ERR_INVALID_ARG;
+#define QVTS_BL(MASK) s = bf_expand_launch_t<MASK>(m, L, ql, st)
+    QVTS_DISPATCH_MASK(m.mask, QVTS_BL);
+#undef QVTS_BL
+    return s;
 }
 
 qvts_status expand_marginals(Model &m, const ExpandSpec &e, QLevel &ql, cudaStream_t st, long long *total) {

@@ -123,10 +123,12 @@ struct Model {
     int bf_nexp = 0;
     DevBuf bf_bel, bf_path, bf_pq, bf_z, bf_f, bf_root, bf_depth, bf_vU, bf_vL, bf_vH, bf_vE, bf_vq0, bf_vLa;
     DevBuf bf_qR, bf_qU, bf_qL, bf_qH, bf_qE, bf_qc0, bf_qnc, bf_qv;
-    DevBuf bf_VT, bf_part, bf_sum, bf_keys;
+    DevBuf bf_VT, bf_part, bf_sum, bf_keys, bf_anc, bf_rtr;
+    cudaStream_t bf_stream = nullptr;
+    cudaGraphExec_t bf_gexec = nullptr;          // cached chunk graph and its key
+    std::vector<uintptr_t> bf_gkey;
+    cudaEvent_t bf_join = nullptr;
     QLevel bf_ql;
-    std::vector<int32_t> bf_exp;          // expanded V-node ids, in order
-    std::vector<double> bf_rtrace;        // root (U, L) after 0, 1, ... expansions
 };
 
 // instrumentation helpers (model.cu)
@@ -170,6 +172,22 @@ struct ChildOut {
     int32_t *parent_q, *z, *f, *root;
 };
 qvts_status expand_marginals(Model &m, const ExpandSpec &e, QLevel &ql, cudaStream_t st, long long *total);
+// Graph-capturable best-first expansion (bestfirst.cu): indices read from device memory.
+struct BfLaunch {
+    float *bel;                       // node pool beliefs [cap][stride]
+    long long stride;
+    uint64_t *path;
+    int32_t *pq, *z, *f, *root;
+    const int32_t *sel, *skip;        // node to expand; non-zero = planning finished
+    const long long *cbase;           // first free pool slot
+    long long *total;                 // out: children of this expansion
+    const uint32_t *root_step, *root_ep;
+    int n;
+    uint32_t seed;
+    int sampler;
+};
+qvts_status bf_expand_prepare(Model &m, QLevel &ql, int n, int sampler);
+qvts_status bf_expand_launch(Model &m, const BfLaunch &L, QLevel &ql, cudaStream_t st);
 qvts_status expand_children(Model &m, const ExpandSpec &e, const QLevel &ql, const ChildOut &o, cudaStream_t st);
 // Bayes correction of selected (Q-node, z) pairs of level 0 into out[sel_out[g]*ostride]
 qvts_status correct_selected(Model &m, const RootBatch &roots, const int32_t *sel_q, const int32_t *sel_z,
