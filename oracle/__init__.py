@@ -71,6 +71,86 @@ class EpisodeRecord(C.Structure):
                 ("x0", C.c_int32), ("x_final", C.c_int32), ("disc_return", C.c_double)]
 
 
+class BfTree:
+    """A persistent oracle best-first tree: plan, then advance(a, z) + cont(...) for tree reuse."""
+
+    def __init__(self, model, alphaU, alphaL, actL, b0, n, expansions, max_depth=8, gap_tol=0.0, seed=1, step=0,
+                 episode=0, mode=0, sampler=0, replay=None, replay_tol=1e-4):
+        self.m = model
+        self.aU = np.ascontiguousarray(alphaU, dtype=np.float64)
+        self.aL = np.ascontiguousarray(alphaL, dtype=np.float64)
+        self.acts = np.ascontiguousarray(actL, dtype=np.int32)
+        cfg, bc, _keep = self._cfgs(n, expansions, max_depth, gap_tol, seed, step, episode, mode, sampler, replay,
+                                    replay_tol)
+        self.h = lib().or_bf_plan(model._h, self.aU, self.aU.shape[0], self.aL, self.aL.shape[0], self.acts,
+                                  np.ascontiguousarray(b0, dtype=np.float64), C.byref(cfg), C.byref(bc))
+        if not self.h:
+            raise ValueError("or_bf_plan rejected its arguments")
+
+    def _cfgs(self, n, expansions, max_depth, gap_tol, seed, step, episode, mode, sampler, replay, replay_tol):
+        cfg, k = self.m._cfg(0, n, seed, step, episode, mode, 0, None, sampler)
+        rp = np.ascontiguousarray(replay if replay is not None else [], dtype=np.uint64)
+        bc = BfCfg(expansions, max_depth, gap_tol, len(rp), rp.ctypes.data if len(rp) else None, replay_tol)
+        return cfg, bc, (k, rp)
+
+    def cont(self, n, expansions, max_depth=8, gap_tol=0.0, seed=1, step=0, episode=0, mode=0, sampler=0,
+             replay=None, replay_tol=1e-4):
+        cfg, bc, _keep = self._cfgs(n, expansions, max_depth, gap_tol, seed, step, episode, mode, sampler, replay,
+                                    replay_tol)
+        st = lib().or_bf_continue(self.h, self.aU, self.aU.shape[0], self.aL, self.aL.shape[0], self.acts,
+                                  C.byref(cfg), C.byref(bc))
+        if st != OK:
+            raise OracleError(st, "or_bf_continue")
+        return self.result()
+
+    def advance(self, a_id, z):
+        return bool(lib().or_bf_advance(self.h, int(a_id), int(z)))
+
+    def belief(self, i):
+        out = np.zeros(self.m.nx)
+        lib().or_bf_belief(self.h, int(i), out)
+        return out
+
+    def result(self):
+        L_, h = lib(), self.h
+        out = {}
+        vals = [C.c_int() for _ in range(6)]
+        L_.or_bf_summary(h, *[C.byref(v) for v in vals])
+        for k, v in zip(("action", "stop", "n_exp", "n_v", "subs", "mism"), vals):
+            out[k] = v.value
+        U, Lo = C.c_double(), C.c_double()
+        UQ, LQ = np.zeros(self.m.na), np.zeros(self.m.na)
+        L_.or_bf_root(h, C.byref(U), C.byref(Lo), UQ, LQ)
+        out.update(U=U.value, L=Lo.value, UQ=UQ, LQ=LQ, root=L_.or_bf_root_index(h))
+        out["expanded"] = np.array([L_.or_bf_expanded(h, k) for k in range(out["n_exp"])], dtype=np.uint64)
+        rt = []
+        for k in range(out["n_exp"] + 1):
+            L_.or_bf_root_trace(h, k, C.byref(U), C.byref(Lo))
+            rt.append((U.value, Lo.value))
+        out["root_trace"] = np.array(rt)
+        cols = {k: [] for k in ("path", "depth", "f", "w", "U", "L", "H", "E", "expanded")}
+        p, d, f, E, ex = C.c_uint64(), C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        w, u, l, hh = C.c_double(), C.c_double(), C.c_double(), C.c_double()
+        for i in range(out["n_v"]):
+            L_.or_bf_vnode(h, i, C.byref(p), C.byref(d), C.byref(f), C.byref(w), C.byref(u), C.byref(l),
+                           C.byref(hh), C.byref(E), C.byref(ex))
+            for k, v in zip(cols, (p, d, f, w, u, l, hh, E, ex)):
+                cols[k].append(v.value)
+        out["v"] = {k: np.array(v, dtype=np.uint64 if k == "path" else None) for k, v in cols.items()}
+        return out
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().or_bf_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
 def bf_q_update(R, gamma, w, U, L, H, E):
     """Alg. 6 on explicit child values -> (U_Q, L_Q, H_Q, E_Q)."""
     out = [C.c_double(), C.c_double(), C.c_double(), C.c_int()]
@@ -138,6 +218,10 @@ def _declare(L):
     L.or_bf_plan.restype = vp
     L.or_bf_plan.argtypes = [vp, _dp, C.c_int, _dp, C.c_int, _i32p, _dp, C.POINTER(PlanCfg), C.POINTER(BfCfg)]
     L.or_bf_free.argtypes = [vp]
+    L.or_bf_continue.argtypes = [vp, _dp, C.c_int, _dp, C.c_int, _i32p, C.POINTER(PlanCfg), C.POINTER(BfCfg)]
+    L.or_bf_advance.argtypes = [vp, C.c_int, C.c_int]
+    L.or_bf_root_index.argtypes = [vp]
+    L.or_bf_belief.argtypes = [vp, C.c_int, _dp]
     L.or_bf_summary.argtypes = [vp] + [C.POINTER(C.c_int)] * 6
     L.or_bf_root.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_double), _dp, _dp]
     L.or_bf_vnode.argtypes = [vp, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_int), C.POINTER(C.c_int),
@@ -347,43 +431,10 @@ class Model:
         """Anytime best-first QVTS (Alg. 1-7, Eq. 8) with U = V_FIB, L = V_PBVI leaves.  Returns a
         dict: action, stop, n_exp, subs, mism, U, L, UQ, LQ, expanded (paths), root_trace
         [(U, L) after k expansions], and per V-node arrays path/depth/f/w/U/L/H/E/expanded."""
-        L_ = lib()
-        aU = np.ascontiguousarray(alphaU, dtype=np.float64)
-        aL = np.ascontiguousarray(alphaL, dtype=np.float64)
-        acts = np.ascontiguousarray(actL, dtype=np.int32)
-        cfg, _k = self._cfg(0, n, seed, step, episode, mode, 0, None, sampler)
-        rp = np.ascontiguousarray(replay if replay is not None else [], dtype=np.uint64)
-        bc = BfCfg(expansions, max_depth, gap_tol, len(rp), rp.ctypes.data if len(rp) else None, replay_tol)
-        h = L_.or_bf_plan(self._h, aU, aU.shape[0], aL, aL.shape[0], acts,
-                          np.ascontiguousarray(b0, dtype=np.float64), C.byref(cfg), C.byref(bc))
-        if not h:
-            raise ValueError("or_bf_plan rejected its arguments")
-        out = {}
-        vals = [C.c_int() for _ in range(6)]
-        L_.or_bf_summary(h, *[C.byref(v) for v in vals])
-        for k, v in zip(("action", "stop", "n_exp", "n_v", "subs", "mism"), vals):
-            out[k] = v.value
-        U, Lo = C.c_double(), C.c_double()
-        UQ, LQ = np.zeros(self.na), np.zeros(self.na)
-        L_.or_bf_root(h, C.byref(U), C.byref(Lo), UQ, LQ)
-        out.update(U=U.value, L=Lo.value, UQ=UQ, LQ=LQ)
-        out["expanded"] = np.array([L_.or_bf_expanded(h, k) for k in range(out["n_exp"])], dtype=np.uint64)
-        rt = []
-        for k in range(out["n_exp"] + 1):
-            L_.or_bf_root_trace(h, k, C.byref(U), C.byref(Lo))
-            rt.append((U.value, Lo.value))
-        out["root_trace"] = np.array(rt)
-        nv = out["n_v"]
-        cols = {k: [] for k in ("path", "depth", "f", "w", "U", "L", "H", "E", "expanded")}
-        p, d, f, E, ex = C.c_uint64(), C.c_int(), C.c_int(), C.c_int(), C.c_int()
-        w, u, l, hh = C.c_double(), C.c_double(), C.c_double(), C.c_double()
-        for i in range(nv):
-            L_.or_bf_vnode(h, i, C.byref(p), C.byref(d), C.byref(f), C.byref(w), C.byref(u), C.byref(l),
-                           C.byref(hh), C.byref(E), C.byref(ex))
-            for k, v in zip(cols, (p, d, f, w, u, l, hh, E, ex)):
-                cols[k].append(v.value)
-        out["v"] = {k: np.array(v, dtype=np.uint64 if k == "path" else None) for k, v in cols.items()}
-        L_.or_bf_free(h)
+        t = BfTree(self, alphaU, alphaL, actL, b0, n, expansions, max_depth, gap_tol, seed, step, episode, mode,
+                   sampler, replay, replay_tol)
+        out = t.result()
+        t.close()
         return out
 
     def qmdp_value(self, Q, b):

@@ -1035,7 +1035,7 @@ typedef struct {
 } bf_q;
 struct or_bf_tree {
     const or_model *m;
-    int na;
+    int na, root;
     bf_v *v;
     bf_q *q;
     int nv, nq, cap_v, cap_q;
@@ -1154,7 +1154,7 @@ static void bf_expand(or_bf_tree *t, int i, const double *aU, int nU, const doub
 
 /* Admissible descent: at every decision the chosen child is within `tol` of the rule's best. */
 static int bf_admissible(const or_bf_tree *t, uint64_t path, double tol) {
-    int i = 0;
+    int i = t->root;
     for (;;) {
         const bf_v *v = &t->v[i];
         if (v->q0 < 0) return v->path == path ? i : -1;
@@ -1180,32 +1180,23 @@ static int bf_admissible(const or_bf_tree *t, uint64_t path, double tol) {
     }
 }
 
-or_bf_tree *or_bf_plan(const or_model *m, const double *alphaU, int nU, const double *alphaL, int nL,
-                       const int *actL, const double *b0, const or_plan_cfg *pcfg, const or_bf_cfg *bcfg) {
-    if (bcfg->max_depth < 1 || bcfg->max_depth > 8 || nU < 1 || nL < 1 || bcfg->expansions < 0) return NULL;
-    or_bf_tree *t = (or_bf_tree *)calloc(1, sizeof(or_bf_tree));
-    t->m = m;
-    t->na = m->na;
-    t->cap_v = 64; t->cap_q = 64;
-    t->v = (bf_v *)malloc(sizeof(bf_v) * t->cap_v);
-    t->q = (bf_q *)malloc(sizeof(bf_q) * t->cap_q);
+/* Alg. 1 inner loop from the current root: expansions until planningFinished(), then
+ * getOptimalAction.  Counters and traces are per call. */
+static void bf_run(or_bf_tree *t, const double *alphaU, int nU, const double *alphaL, int nL, const int *actL,
+                   const or_plan_cfg *pcfg, const or_bf_cfg *bcfg) {
+    const or_model *m = t->m;
+    free(t->exp_path); free(t->rootU); free(t->rootL);
     t->exp_path = (uint64_t *)calloc(bcfg->expansions + 1, sizeof(uint64_t));
     t->rootU = (double *)calloc(bcfg->expansions + 1, sizeof(double));
     t->rootL = (double *)calloc(bcfg->expansions + 1, sizeof(double));
-    int r = bf_new_v(t);                                   /* Alg. 1: s = QVSearchTree(b0) */
-    t->v[r].b = (double *)malloc(sizeof(double) * m->nx);
-    memcpy(t->v[r].b, b0, sizeof(double) * m->nx);
-    t->v[r].pq = -1;
-    t->v[r].f = pcfg->n_samples;
-    t->v[r].w = 1.0;
-    bf_leaf(t, r, alphaU, nU, alphaL, nL, bcfg->max_depth);
-    t->stop = 0;
+    t->n_exp = 0; t->subs = 0; t->mism = 0; t->stop = 0;
+    const int r = t->root;
     for (;;) {
-        t->rootU[t->n_exp] = t->v[0].U;
-        t->rootL[t->n_exp] = t->v[0].L;
+        t->rootU[t->n_exp] = t->v[r].U;
+        t->rootL[t->n_exp] = t->v[r].L;
         if (t->n_exp >= bcfg->expansions) { t->stop = 0; break; }          /* planningFinished() */
-        if (t->v[0].U - t->v[0].L <= bcfg->gap_tol) { t->stop = 1; break; }
-        int e = t->v[0].E;                                 /* findVNodeToExpand() = root.E */
+        if (t->v[r].U - t->v[r].L <= bcfg->gap_tol) { t->stop = 1; break; }
+        int e = t->v[r].E;                                 /* findVNodeToExpand() = root.E */
         if (bcfg->n_replay > t->n_exp) {
             int g = bf_admissible(t, bcfg->replay_path[t->n_exp], bcfg->replay_tol);
             if (g < 0) t->mism++;
@@ -1221,19 +1212,81 @@ or_bf_tree *or_bf_plan(const or_model *m, const double *alphaU, int nU, const do
     }
     /* getOptimalAction: max L_Q, ties by U_Q then index (SPEC plan); an unexpanded root takes the
      * action of its PBVI arg-max vector. */
-    if (t->v[0].q0 < 0) {
+    if (t->v[r].q0 < 0) {
         int arg;
-        bf_dot_max(alphaL, nL, m->nx, t->v[0].b, &arg);
+        bf_dot_max(alphaL, nL, m->nx, t->v[r].b, &arg);
         t->action = actL ? actL[arg] : 0;
     } else {
         int best = 0;
         for (int a = 1; a < t->na; ++a) {
-            const bf_q *q = &t->q[t->v[0].q0 + a], *bq = &t->q[t->v[0].q0 + best];
+            const bf_q *q = &t->q[t->v[r].q0 + a], *bq = &t->q[t->v[r].q0 + best];
             if (q->L > bq->L || (q->L == bq->L && q->U > bq->U)) best = a;
         }
         t->action = m->action_id[best];
     }
+}
+
+or_bf_tree *or_bf_plan(const or_model *m, const double *alphaU, int nU, const double *alphaL, int nL,
+                       const int *actL, const double *b0, const or_plan_cfg *pcfg, const or_bf_cfg *bcfg) {
+    if (bcfg->max_depth < 1 || bcfg->max_depth > 8 || nU < 1 || nL < 1 || bcfg->expansions < 0) return NULL;
+    or_bf_tree *t = (or_bf_tree *)calloc(1, sizeof(or_bf_tree));
+    t->m = m;
+    t->na = m->na;
+    t->cap_v = 64; t->cap_q = 64;
+    t->v = (bf_v *)malloc(sizeof(bf_v) * t->cap_v);
+    t->q = (bf_q *)malloc(sizeof(bf_q) * t->cap_q);
+    int r = bf_new_v(t);                                   /* Alg. 1: s = QVSearchTree(b0) */
+    t->root = r;
+    t->v[r].b = (double *)malloc(sizeof(double) * m->nx);
+    memcpy(t->v[r].b, b0, sizeof(double) * m->nx);
+    t->v[r].pq = -1;
+    t->v[r].f = pcfg->n_samples;
+    t->v[r].w = 1.0;
+    bf_leaf(t, r, alphaU, nU, alphaL, nL, bcfg->max_depth);
+    bf_run(t, alphaU, nU, alphaL, nL, actL, pcfg, bcfg);
     return t;
+}
+
+int or_bf_continue(or_bf_tree *t, const double *alphaU, int nU, const double *alphaL, int nL, const int *actL,
+                   const or_plan_cfg *pcfg, const or_bf_cfg *bcfg) {
+    if (bcfg->max_depth < 1 || bcfg->max_depth > 8 || bcfg->expansions < 0) return OR_ERR_INVALID_ARG;
+    bf_run(t, alphaU, nU, alphaL, nL, actL, pcfg, bcfg);
+    return OR_OK;
+}
+
+/* s.update(a, z) (Alg. 1; SPEC advance_root): when the root's Q-node for stencil id a_id has a
+ * child with observation z, that V-node becomes the root and keeps its subtree; its paths lose
+ * their first byte and depths drop by one (so later draws are keyed relative to the new root),
+ * every node outside it is discarded (depth -1).  Returns 1 on reuse, 0 when z was not sampled
+ * (the caller builds a fresh root from Eq. 3). */
+int or_bf_advance(or_bf_tree *t, int a_id, int z) {
+    const bf_v *root = &t->v[t->root];
+    if (root->q0 < 0) return 0;
+    int a = -1;
+    for (int k = 0; k < t->na; ++k) if (t->m->action_id[k] == a_id) a = k;
+    if (a < 0) return 0;
+    const bf_q *q = &t->q[root->q0 + a];
+    int c = -1;
+    for (int i = 0; i < q->nc; ++i) if (t->v[q->c0 + i].z == z) c = q->c0 + i;
+    if (c < 0) return 0;
+    /* subtree membership: walk each node's parent chain up to depth 1 */
+    for (int i = 0; i < t->nv; ++i) {
+        bf_v *v = &t->v[i];
+        if (v->depth < 1) { v->depth = -1; continue; }
+        int j = i;
+        while (t->v[j].depth > 1) j = t->q[t->v[j].pq].pv;
+        if (j != c) { v->depth = -1; continue; }
+    }
+    for (int i = 0; i < t->nv; ++i) {
+        bf_v *v = &t->v[i];
+        if (v->depth < 0) continue;
+        v->depth -= 1;
+        v->path >>= 8;
+    }
+    t->v[c].pq = -1;
+    t->v[c].w = 1.0;
+    t->root = c;
+    return 1;
 }
 
 void or_bf_free(or_bf_tree *t) {
@@ -1245,14 +1298,17 @@ void or_bf_summary(const or_bf_tree *t, int *action, int *stop, int *n_exp, int 
     *action = t->action; *stop = t->stop; *n_exp = t->n_exp; *n_v = t->nv; *subs = t->subs; *mism = t->mism;
 }
 void or_bf_root(const or_bf_tree *t, double *U, double *L, double *UQ, double *LQ) {
-    *U = t->v[0].U;
-    *L = t->v[0].L;
+    const bf_v *r = &t->v[t->root];
+    *U = r->U;
+    *L = r->L;
     for (int a = 0; a < t->na; ++a) {
-        int ok = t->v[0].q0 >= 0;
-        if (UQ) UQ[a] = ok ? t->q[t->v[0].q0 + a].U : NAN;
-        if (LQ) LQ[a] = ok ? t->q[t->v[0].q0 + a].L : NAN;
+        int ok = r->q0 >= 0;
+        if (UQ) UQ[a] = ok ? t->q[r->q0 + a].U : NAN;
+        if (LQ) LQ[a] = ok ? t->q[r->q0 + a].L : NAN;
     }
 }
+int or_bf_root_index(const or_bf_tree *t) { return t->root; }
+void or_bf_belief(const or_bf_tree *t, int i, double *out) { memcpy(out, t->v[i].b, sizeof(double) * t->m->nx); }
 void or_bf_vnode(const or_bf_tree *t, int i, uint64_t *path, int *depth, int *f, double *w, double *U,
                  double *L, double *H, int *E, int *expanded) {
     const bf_v *v = &t->v[i];

@@ -140,6 +140,14 @@ typedef struct or_bf_tree or_bf_tree;
 or_bf_tree *or_bf_plan(const or_model *m, const double *alphaU, int nU, const double *alphaL, int nL,
                        const int *actL, const double *b0, const or_plan_cfg *pcfg, const or_bf_cfg *bcfg);
 void or_bf_free(or_bf_tree *t);
+/* More expansions from the current root (after or_bf_advance: tree reuse). */
+int or_bf_continue(or_bf_tree *t, const double *alphaU, int nU, const double *alphaL, int nL, const int *actL,
+                   const or_plan_cfg *pcfg, const or_bf_cfg *bcfg);
+/* s.update(a, z) (Alg. 1): re-root at the root's (a, z) child if it was sampled (returns 1) and
+ * discard the rest (depth -1); paths/depths become relative to the new root. */
+int or_bf_advance(or_bf_tree *t, int a_id, int z);
+int or_bf_root_index(const or_bf_tree *t);
+void or_bf_belief(const or_bf_tree *t, int i, double *out);   /* V-node i's belief [nx] */
 /* action (stencil id), stop reason (0 budget, 1 gap, 2 terminal leaf selected), expansions done,
  * V-nodes, replay substitutions (admissible GPU choices that differ) and mismatches. */
 void or_bf_summary(const or_bf_tree *t, int *action, int *stop, int *n_exp, int *n_v, int *subs, int *mism);

@@ -634,3 +634,43 @@ def test_bf_degenerate_bounds_stop_at_once():
     pts, al, act = m.pbvi(b0, expansions=6, max_points=8, seed=3, sweeps=400)
     r = m.best_first(A, al, act, b0, n=4, expansions=10, gap_tol=1e-6)
     assert r["stop"] == 1 and r["n_exp"] == 0
+
+
+def test_bf_advance_root_reuses_the_subtree():
+    """s.update(a, z) (Alg. 1; SPEC advance_root): the sampled child becomes the root with its
+    subtree; its belief is Eq. 3's Phi(b0, a, z); kept nodes lose one level (path >> 8, depth - 1);
+    root.E stays inside the new subtree; an unsampled z is refused."""
+    gm = W.random_map(6, 8, 0.2, seed=9)
+    m = O.Model.grid(gm, action_mask=W.A8, acc=0.9)
+    b0 = W.uniform_belief(gm)
+    A, al, act = _bounds(m, gm, b0)
+    t = O.BfTree(m, A, al, act, b0, 8, 15, max_depth=6, seed=4)
+    r0 = t.result()
+    v0 = r0["v"]
+    a_id = r0["action"]
+    j = m.action_ids.index(a_id)
+    kids = [i for i in range(r0["n_v"]) if v0["depth"][i] == 1 and (int(v0["path"][i]) & 15) == a_id + 1]
+    assert kids
+    c = kids[0]
+    z = int(v0["path"][c]) >> 4 & 15
+    unsampled = [zz for zz in range(16) if all((int(v0["path"][i]) >> 4 & 15) != zz for i in kids)]
+    sub_old = {int(v0["path"][i]): i for i in range(r0["n_v"])
+               if v0["depth"][i] >= 1 and (int(v0["path"][i]) & 0xFF) == (int(v0["path"][c]) & 0xFF)}
+    assert t.advance(a_id, z)
+    r1 = t.cont(8, 0, max_depth=6, seed=4, step=1)
+    assert r1["root"] == c and r1["U"] == v0["U"][c] and r1["L"] == v0["L"][c]
+    bz, _ = m.belief_update(b0, j, z)
+    assert np.max(np.abs(t.belief(c) - bz)) <= 1e-15
+    v1 = r1["v"]
+    alive = [i for i in range(r1["n_v"]) if v1["depth"][i] >= 0]
+    assert sorted(alive) == sorted(sub_old.values())
+    for p_old, i in sub_old.items():
+        assert int(v1["path"][i]) == p_old >> 8 and v1["depth"][i] == v0["depth"][i] - 1
+    assert v1["depth"][int(v1["E"][c])] >= 0                 # root.E inside the kept subtree
+    r2 = t.cont(8, 10, max_depth=6, seed=4, step=1)
+    assert r2["n_exp"] > 0 and r2["root"] == c
+    if unsampled:
+        t2 = O.BfTree(m, A, al, act, b0, 8, 15, max_depth=6, seed=4)
+        assert not t2.advance(a_id, unsampled[0])
+        t2.close()
+    t.close()
