@@ -235,6 +235,8 @@ typedef struct {
     int32_t max_depth;        /* 1..8                                                       */
     double gap_tol;           /* stop once root U - L <= gap_tol                            */
     double time_budget_ms;    /* > 0: also stop after this much wall-clock time (anytime)   */
+    int32_t reuse;            /* 1: continue the kept tree (after qvts_bf_advance); root_dev
+                                 is then ignored and may be NULL        */
 } qvts_bf_cfg;
 typedef enum { QVTS_BF_BUDGET = 0, QVTS_BF_GAP = 1, QVTS_BF_TERMINAL = 2, QVTS_BF_POOL = 3, QVTS_BF_TIME = 4 } qvts_bf_stop;
 typedef struct {
@@ -249,9 +251,18 @@ typedef struct {
 } qvts_bf_result;
 QVTS_API qvts_status qvts_plan_best_first(qvts_model *model, const float *root_dev, const qvts_bf_cfg *cfg,
                                           qvts_bf_result *res, void *stream);
-/* The last best-first tree (any pointer may be NULL): per V-node [n_v] path, depth, sampled count
- * f, U, L, H, E (node index), expanded (0/1); exp_order [n_expansions] = expanded node indices in
- * order; root_trace [(n_expansions+1)][2] = root (U, L) before the first and after each expansion. */
+/* s.update(a, z) (Alg. 1, "set the root to be consistent with the current belief";
+ * SPEC advance_root): if the root's Q-node for stencil id `action` has a child with observation z,
+ * that V-node becomes the root and keeps its subtree: paths lose their first byte and depths drop
+ * by one, so later draws are keyed relative to the new root; every other node is discarded
+ * (depth -1 in the trace, pool slots not recycled).  *reused = 1 then, and the next
+ * qvts_plan_best_first with cfg.reuse = 1 continues from it; *reused = 0 when z was not sampled
+ * (or the root is unexpanded): build a fresh root from qvts_belief_update instead. */
+QVTS_API qvts_status qvts_bf_advance(qvts_model *model, int32_t action, int32_t z, int32_t *reused, void *stream);
+/* The last best-first tree (any pointer may be NULL): per V-node [n_v] path, depth (-1: discarded
+ * by qvts_bf_advance), sampled count f, U, L, H, E (node index), expanded (0/1); exp_order
+ * [n_expansions] = node indices expanded by the last call, in order; root_trace
+ * [(n_expansions+1)][2] = root (U, L) before the first and after each expansion of that call. */
 QVTS_API qvts_status qvts_trace_best_first(const qvts_model *model, int64_t *n_v, int32_t *n_expansions,
                                            uint64_t *path, int32_t *depth, int32_t *f, double *U, double *L,
                                            double *H, int32_t *E, int32_t *expanded, int32_t *exp_order,

@@ -39,7 +39,7 @@ struct BfDev {
     long long total;              // children of the current expansion
     long long cap_v;              // pool capacity (V-nodes)
     double U, L, H;               // root bounds and heuristic
-    int32_t budget, max_depth, per_exp, pad;
+    int32_t budget, max_depth, per_exp, root;   // root: pool index of the current root
     double gap_tol;
 };
 
@@ -196,11 +196,37 @@ __global__ void k_bf_init_root(uint64_t *path, int32_t *pq, int32_t *z, int32_t 
 // after the root's leaf bounds: s = QVSearchTree(b0) (Alg. 1), root.E = root
 __global__ void k_bf_root_state(BfDev *S, const double *vU, const double *vL, const double *vH, const int32_t *vLa,
                                 double *rtrace) {
-    S->sel = 0; S->depth = 0; S->nv = 1; S->nq = 0; S->nexp = 0; S->total = 0;
+    S->root = 0; S->sel = 0; S->depth = 0; S->nv = 1; S->nq = 0; S->nexp = 0; S->total = 0;
     S->U = vU[0]; S->L = vL[0]; S->H = vH[0]; S->la0 = vLa[0];
     rtrace[0] = S->U;
     rtrace[1] = S->L;
     bf_check_done(S);
+}
+
+// tree reuse (NEXT-4): resume from the kept tree's root -- root.E, bounds, a fresh per-call count
+__global__ void k_bf_resume(BfDev *S, const int32_t *vE, const int32_t *vdepth, const double *vU, const double *vL,
+                            const double *vH, const int32_t *vLa, double *rtrace) {
+    const int r = S->root;
+    S->sel = vE[r]; S->depth = vdepth[S->sel]; S->nexp = 0; S->total = 0; S->done = 0; S->stop = 0;
+    S->U = vU[r]; S->L = vL[r]; S->H = vH[r]; S->la0 = vLa[r];
+    rtrace[0] = S->U;
+    rtrace[1] = S->L;
+    bf_check_done(S);
+}
+
+// s.update(a, z) (Alg. 1): re-root at pool node c.  Nodes of its subtree (depth-1 ancestor = c) lose
+// one level (path >> 8, depth - 1, ancestor lists shifted); every other node is discarded (depth -1).
+__global__ void k_bf_rebase(long long nv, int c, uint64_t *path, int32_t *vdepth, int32_t *anc, int32_t *pq) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= nv) return;
+    const int d = vdepth[i];
+    int32_t *an = anc + (size_t)i * 16;
+    const bool member = d == 1 ? (i == c) : (d >= 2 && an[1] == c);
+    if (!member) { vdepth[i] = -1; return; }
+    path[i] >>= 8;
+    vdepth[i] = d - 1;
+    for (int l = 0; l < 7; ++l) { an[l] = an[l + 1]; an[8 + l] = an[9 + l]; }
+    if (i == c) pq[i] = -1;
 }
 
 struct BackupArgs {
@@ -355,12 +381,13 @@ __global__ void __launch_bounds__(256) k_bf_backup(BackupArgs a) {
         }
     }
     if (t == 0) {   // publish root.E and the root bounds, advance the pool, planningFinished()
-        const int e = a.vE[0];
+        const int r = S->root;
+        const int e = a.vE[r];
         S->sel = e;
         S->depth = a.vdepth[e];
-        S->U = a.vU[0];
-        S->L = a.vL[0];
-        S->H = a.vH[0];
+        S->U = a.vU[r];
+        S->L = a.vL[r];
+        S->H = a.vH[r];
         S->nv = cbase + S->total;
         S->nq = qbase + NA;
         S->nexp += 1;
@@ -483,7 +510,7 @@ using namespace qvts;
 
 extern "C" qvts_status qvts_plan_best_first(qvts_model *m, const float *root_dev, const qvts_bf_cfg *cfg,
                                             qvts_bf_result *res, void *stream) {
-    if (!m || !root_dev || !cfg || !res) { set_error("NULL argument"); return QVTS_ERR_INVALID_ARG; }
+    if (!m || !cfg || !res) { set_error("NULL argument"); return QVTS_ERR_INVALID_ARG; }
     if (cfg->n_samples < 1 || cfg->n_samples > 4096 || cfg->max_expansions < 0 || cfg->max_depth < 1 ||
         cfg->max_depth > 8 || !(cfg->gap_tol >= 0.0) ||
         (cfg->sampler != QVTS_SAMPLER_MARGINAL && cfg->sampler != QVTS_SAMPLER_ANCESTRAL)) {
@@ -504,18 +531,24 @@ extern "C" qvts_status qvts_plan_best_first(qvts_model *m, const float *root_dev
     const auto t_start = std::chrono::steady_clock::now();
     const int NA = m->NA, HW = m->HW, n = cfg->n_samples;
     const BfGeom g = bf_geom(*m);
-    // node pool: worst case 1 + max_expansions * per_exp nodes, allocated lazily in doublings and
-    // capped at half the free device memory
+    const bool reuse = cfg->reuse && m->bf_valid;
+    m->bf_valid = false;
+    BfDev hs{};
+    if (reuse) {   // keep pool fill and root; new limits below
+        QVTS_CUDA(cudaMemcpyAsync(&hs, m->bf_sum.p, sizeof(BfDev), cudaMemcpyDeviceToHost, st));
+        QVTS_CUDA(cudaStreamSynchronize(st));
+        hs.root = m->bf_root_idx;
+    } else {
+        hs.depth = -1;
+    }
+    const long long used = reuse ? hs.nv : 0;
+    // node pool: worst case used + 1 + max_expansions * per_exp nodes, allocated lazily in doublings
+    // and capped at half the free device memory
     const long long per_exp = (long long)NA * std::min(n, 16);
-    const long long worst = 1 + (long long)cfg->max_expansions * per_exp;
+    const long long worst = used + 1 + (long long)cfg->max_expansions * per_exp;
     size_t free_b = 0, total_b = 0;
     QVTS_CUDA(cudaMemGetInfo(&free_b, &total_b));
     const size_t node_bytes = (size_t)m->HWp * 4 + 200;
-    const long long by_mem = std::max(1LL + per_exp, (long long)(free_b / 2 / node_bytes));
-    const long long cap_max = std::min(worst, by_mem);
-    long long cap = std::min(cap_max, 1 + 64 * per_exp);
-    m->bf_valid = false;
-    QVTS_TRY(bf_pool_grow(*m, 0, cap, st));
     auto pool_nodes = [&]() {   // nodes every pool array can hold now
         std::vector<std::pair<DevBuf *, size_t>> arrs;
         bf_pool_arrays(*m, arrs);
@@ -524,6 +557,11 @@ extern "C" qvts_status qvts_plan_best_first(qvts_model *m, const float *root_dev
         for (auto &pr : arrs) c = std::min(c, (long long)(pr.first->cap / pr.second));
         return c;
     };
+    const long long have = m->bf_bel.p ? pool_nodes() : 0;
+    const long long by_mem = std::max(used + 1 + per_exp, have + (long long)(free_b / 2 / node_bytes));
+    const long long cap_max = std::min(worst, by_mem);
+    long long cap = std::min(cap_max, used + 1 + 64 * per_exp);
+    QVTS_TRY(bf_pool_grow(*m, used, cap, st));
     cap = std::min(cap_max, pool_nodes());
     const int nrows = g.nkb * g.KB;
     QVTS_TRY(m->bf_VT.ensure(sizeof(double) * (size_t)HW * nrows));
@@ -533,9 +571,9 @@ extern "C" qvts_status qvts_plan_best_first(qvts_model *m, const float *root_dev
     QVTS_TRY(m->bf_rtr.ensure(sizeof(double) * 2 * ((size_t)cfg->max_expansions + 1)));
     QVTS_TRY(bf_expand_prepare(*m, m->bf_ql, n, cfg->sampler));
     BfDev *S = m->bf_sum.as<BfDev>();
-    BfDev hs{};
-    hs.depth = -1; hs.budget = cfg->max_expansions; hs.max_depth = cfg->max_depth; hs.per_exp = (int)per_exp;
+    hs.budget = cfg->max_expansions; hs.max_depth = cfg->max_depth; hs.per_exp = (int)per_exp;
     hs.gap_tol = cfg->gap_tol; hs.cap_v = cap;
+    const long long nq0 = reuse ? hs.nq : 0;
     uint32_t keys[2] = {cfg->step, cfg->episode};
     QVTS_CUDA(cudaMemcpyAsync(m->bf_keys.p, keys, sizeof(keys), cudaMemcpyHostToDevice, st));
     QVTS_CUDA(cudaMemcpyAsync(S, &hs, sizeof(BfDev), cudaMemcpyHostToDevice, st));
@@ -544,13 +582,20 @@ extern "C" qvts_status qvts_plan_best_first(qvts_model *m, const float *root_dev
     k_bf_vk<<<(unsigned)(((long long)HW * nrows + 255) / 256), 256, 0, st>>>(m->d_alpha64.as<double>(), NA,
                                                                                m->pb_G.as<double>(), g.nal, HW, nrows,
                                                                                m->bf_VT.as<double>());
-    QVTS_CUDA(cudaMemcpyAsync(m->bf_bel.p, root_dev, sizeof(float) * HW, cudaMemcpyDeviceToDevice, st));
-    k_bf_init_root<<<1, 1, 0, st>>>(m->bf_path.as<uint64_t>(), m->bf_pq.as<int32_t>(), m->bf_z.as<int32_t>(),
-                                    m->bf_f.as<int32_t>(), m->bf_root.as<int32_t>(), n);
-    QVTS_CUDA(cudaGetLastError());
-    QVTS_TRY(bf_leaf_bounds(*m, g, S, st));            // the root (S->depth = -1)
-    k_bf_root_state<<<1, 1, 0, st>>>(S, m->bf_vU.as<double>(), m->bf_vL.as<double>(), m->bf_vH.as<double>(),
-                                     m->bf_vLa.as<int32_t>(), m->bf_rtr.as<double>());
+    if (reuse) {
+        k_bf_resume<<<1, 1, 0, st>>>(S, m->bf_vE.as<int32_t>(), m->bf_depth.as<int32_t>(), m->bf_vU.as<double>(),
+                                     m->bf_vL.as<double>(), m->bf_vH.as<double>(), m->bf_vLa.as<int32_t>(),
+                                     m->bf_rtr.as<double>());
+    } else {
+        if (!root_dev) { set_error("root_dev is NULL without tree reuse"); return QVTS_ERR_INVALID_ARG; }
+        QVTS_CUDA(cudaMemcpyAsync(m->bf_bel.p, root_dev, sizeof(float) * HW, cudaMemcpyDeviceToDevice, st));
+        k_bf_init_root<<<1, 1, 0, st>>>(m->bf_path.as<uint64_t>(), m->bf_pq.as<int32_t>(), m->bf_z.as<int32_t>(),
+                                        m->bf_f.as<int32_t>(), m->bf_root.as<int32_t>(), n);
+        QVTS_CUDA(cudaGetLastError());
+        QVTS_TRY(bf_leaf_bounds(*m, g, S, st));            // the root (S->depth = -1)
+        k_bf_root_state<<<1, 1, 0, st>>>(S, m->bf_vU.as<double>(), m->bf_vL.as<double>(), m->bf_vH.as<double>(),
+                                         m->bf_vLa.as<int32_t>(), m->bf_rtr.as<double>());
+    }
     QVTS_CUDA(cudaGetLastError());
     // chunks of expansions replayed from a CUDA graph; the graph is re-captured after a pool growth
     // (the arrays move).  Profiling mode launches directly so every kernel is timed.
@@ -638,14 +683,16 @@ extern "C" qvts_status qvts_plan_best_first(qvts_model *m, const float *root_dev
     res->U = hs.U;
     res->L = hs.L;
     for (int j = 0; j < 9; ++j) res->u_q[j] = res->l_q[j] = NAN;
-    if (nexp > 0) {   // the root was expanded first: its Q-nodes are 0..NA-1
-        QVTS_CUDA(cudaMemcpy(res->u_q, m->bf_qU.p, sizeof(double) * NA, cudaMemcpyDeviceToHost));
-        QVTS_CUDA(cudaMemcpy(res->l_q, m->bf_qL.p, sizeof(double) * NA, cudaMemcpyDeviceToHost));
+    int32_t rq0 = -1;   // the root's first Q-node (-1: unexpanded)
+    QVTS_CUDA(cudaMemcpy(&rq0, m->bf_vq0.as<int32_t>() + hs.root, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    if (rq0 >= 0) {
+        QVTS_CUDA(cudaMemcpy(res->u_q, m->bf_qU.as<double>() + rq0, sizeof(double) * NA, cudaMemcpyDeviceToHost));
+        QVTS_CUDA(cudaMemcpy(res->l_q, m->bf_qL.as<double>() + rq0, sizeof(double) * NA, cudaMemcpyDeviceToHost));
     }
     float ms = 0.f;
     QVTS_CUDA(cudaEventElapsedTime(&ms, m->ev0, m->ev1));
     res->device_ms = ms;
-    if (nexp == 0) {
+    if (rq0 < 0) {
         res->action = m->pb_act[hs.la0];
     } else {                  // getOptimalAction: max L_Q, ties by U_Q then index
         int best = 0;
@@ -655,7 +702,9 @@ extern "C" qvts_status qvts_plan_best_first(qvts_model *m, const float *root_dev
     }
     m->bf_nv = nv;
     m->bf_nq = hs.nq;
+    m->bf_nq0 = nq0;
     m->bf_nexp = nexp;
+    m->bf_root_idx = hs.root;
     m->bf_valid = true;
     prof_collect(*m);
     return QVTS_OK;
@@ -685,10 +734,43 @@ extern "C" qvts_status qvts_trace_best_first(const qvts_model *m, int64_t *n_v, 
     if (exp_order) {   // Q-node blocks are allocated in expansion order: block e belongs to qv[e * NA]
         std::vector<int32_t> qv((size_t)m->bf_nq);
         if (m->bf_nq) QVTS_CUDA(cudaMemcpy(qv.data(), m->bf_qv.p, sizeof(int32_t) * qv.size(), cudaMemcpyDeviceToHost));
-        for (int e = 0; e < m->bf_nexp; ++e) exp_order[e] = qv[(size_t)e * m->NA];
+        for (int e = 0; e < m->bf_nexp; ++e) exp_order[e] = qv[(size_t)m->bf_nq0 + (size_t)e * m->NA];
     }
     if (root_trace)
         QVTS_CUDA(cudaMemcpy(root_trace, m->bf_rtr.p, sizeof(double) * 2 * ((size_t)m->bf_nexp + 1),
                              cudaMemcpyDeviceToHost));
+    return QVTS_OK;
+}
+
+extern "C" qvts_status qvts_bf_advance(qvts_model *m, int32_t action, int32_t z, int32_t *reused, void *stream) {
+    if (!m || !reused) { set_error("NULL argument"); return QVTS_ERR_INVALID_ARG; }
+    *reused = 0;
+    if (!m->bf_valid) { set_error("qvts_plan_best_first has not run"); return QVTS_ERR_STATE; }
+    if (z < 0 || z > 15) { set_error("z must be 0..15"); return QVTS_ERR_INVALID_ARG; }
+    int j = -1;
+    for (int k = 0; k < m->NA; ++k) if (m->action_id[k] == action) j = k;
+    if (j < 0) { set_error("action is not in the model's action set"); return QVTS_ERR_INVALID_ARG; }
+    QVTS_CUDA(cudaSetDevice(m->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    QVTS_CUDA(cudaStreamSynchronize(m->bf_stream));
+    const int r = m->bf_root_idx;
+    int32_t q0 = -1;
+    QVTS_CUDA(cudaMemcpy(&q0, m->bf_vq0.as<int32_t>() + r, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    if (q0 < 0) return QVTS_OK;                     // unexpanded root: nothing to keep
+    int32_t c0 = 0, nc = 0;
+    QVTS_CUDA(cudaMemcpy(&c0, m->bf_qc0.as<int32_t>() + q0 + j, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    QVTS_CUDA(cudaMemcpy(&nc, m->bf_qnc.as<int32_t>() + q0 + j, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    std::vector<int32_t> zs(std::max(1, nc));
+    if (nc > 0) QVTS_CUDA(cudaMemcpy(zs.data(), m->bf_z.as<int32_t>() + c0, sizeof(int32_t) * nc, cudaMemcpyDeviceToHost));
+    int c = -1;
+    for (int i = 0; i < nc; ++i) if (zs[i] == z) c = c0 + i;
+    if (c < 0) return QVTS_OK;                      // z was not sampled: the caller starts afresh
+    const long long nv = m->bf_nv;
+    k_bf_rebase<<<(unsigned)((nv + 255) / 256), 256, 0, st>>>(nv, c, m->bf_path.as<uint64_t>(), m->bf_depth.as<int32_t>(),
+                                                             m->bf_anc.as<int32_t>(), m->bf_pq.as<int32_t>());
+    QVTS_CUDA(cudaGetLastError());
+    QVTS_CUDA(cudaStreamSynchronize(st));
+    m->bf_root_idx = c;
+    *reused = 1;
     return QVTS_OK;
 }

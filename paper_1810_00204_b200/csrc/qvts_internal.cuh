@@ -119,8 +119,8 @@ struct Model {
     DevBuf pb_b0, pb_B, pb_G, pb_Gn, pb_GT, pb_Bbar, pb_Sc, pb_Rb, pb_sel, pb_astar, pb_cand, pb_misc, pb_cls;
     // anytime best-first QVTS (NEXT-2, bestfirst.cu): node pool of the last qvts_plan_best_first
     bool bf_valid = false;
-    long long bf_nv = 0, bf_nq = 0;
-    int bf_nexp = 0;
+    long long bf_nv = 0, bf_nq = 0, bf_nq0 = 0;
+    int bf_nexp = 0, bf_root_idx = 0;
     DevBuf bf_bel, bf_path, bf_pq, bf_z, bf_f, bf_root, bf_depth, bf_vU, bf_vL, bf_vH, bf_vE, bf_vq0, bf_vLa;
     DevBuf bf_qR, bf_qU, bf_qL, bf_qH, bf_qE, bf_qc0, bf_qnc, bf_qv;
     DevBuf bf_VT, bf_part, bf_sum, bf_keys, bf_anc, bf_rtr;

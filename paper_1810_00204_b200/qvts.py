@@ -24,7 +24,7 @@ EXPORTS = [
     "qvts_value_iteration", "qvts_get_q", "qvts_belief_update", "qvts_plan_step", "qvts_trace_qnodes",
     "qvts_trace_vnodes", "qvts_trace_leaf_values", "qvts_trace_belief", "qvts_run_episodes",
     "qvts_trace_counts", "qvts_set_profiling", "qvts_get_profile", "qvts_fib_iteration", "qvts_get_alpha",
-    "qvts_pbvi", "qvts_get_pbvi", "qvts_plan_best_first", "qvts_trace_best_first",
+    "qvts_pbvi", "qvts_get_pbvi", "qvts_plan_best_first", "qvts_trace_best_first", "qvts_bf_advance",
 ]
 QVTS_BF_BUDGET, QVTS_BF_GAP, QVTS_BF_TERMINAL, QVTS_BF_POOL, QVTS_BF_TIME = 0, 1, 2, 3, 4
 QVTS_LEAF_QMDP, QVTS_LEAF_FIB = 0, 1
@@ -59,7 +59,7 @@ class qvts_plan_result(C.Structure):
 class qvts_bf_cfg(C.Structure):
     _fields_ = [("n_samples", C.c_int32), ("seed", C.c_uint32), ("step", C.c_uint32), ("episode", C.c_uint32),
                 ("sampler", C.c_int32), ("max_expansions", C.c_int32), ("max_depth", C.c_int32),
-                ("gap_tol", C.c_double), ("time_budget_ms", C.c_double)]
+                ("gap_tol", C.c_double), ("time_budget_ms", C.c_double), ("reuse", C.c_int32)]
 
 
 class qvts_bf_result(C.Structure):
@@ -123,6 +123,7 @@ def lib() -> C.CDLL:
         L.qvts_get_pbvi.argtypes = [vp, vp, vp, vp, C.POINTER(C.c_int32)]
         L.qvts_plan_best_first.argtypes = [vp, vp, C.POINTER(qvts_bf_cfg), C.POINTER(qvts_bf_result), vp]
         L.qvts_trace_best_first.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int32)] + [vp] * 10
+        L.qvts_bf_advance.argtypes = [vp, C.c_int32, C.c_int32, C.POINTER(C.c_int32), vp]
         L.qvts_belief_update.argtypes = [vp, vp, C.c_int32, C.c_int32, vp, C.POINTER(C.c_double), vp]
         L.qvts_plan_step.argtypes = [vp, vp, C.POINTER(qvts_plan_cfg), C.POINTER(qvts_comm),
                                      C.POINTER(qvts_plan_result), vp]
@@ -244,12 +245,20 @@ def qvts_get_pbvi(h, n_points, n_cells):
 
 
 def qvts_plan_best_first(h, root_dev, n_samples, max_expansions, max_depth=8, gap_tol=0.0, seed=1, step=0,
-                         episode=0, sampler=QVTS_SAMPLER_MARGINAL, time_budget_ms=0.0, stream=None):
-    cfg = qvts_bf_cfg(n_samples, seed, step, episode, sampler, max_expansions, max_depth, gap_tol, time_budget_ms)
+                         episode=0, sampler=QVTS_SAMPLER_MARGINAL, time_budget_ms=0.0, reuse=False, stream=None):
+    cfg = qvts_bf_cfg(n_samples, seed, step, episode, sampler, max_expansions, max_depth, gap_tol, time_budget_ms,
+                      1 if reuse else 0)
     res = qvts_bf_result()
     _check(lib().qvts_plan_best_first(h, _ptr(root_dev), C.byref(cfg), C.byref(res), _stream(stream)),
            "qvts_plan_best_first")
     return res
+
+
+def qvts_bf_advance(h, action, z, stream=None):
+    """Re-root the last best-first tree at its (action, z) child; True when the subtree is kept."""
+    r = C.c_int32()
+    _check(lib().qvts_bf_advance(h, int(action), int(z), C.byref(r), _stream(stream)), "qvts_bf_advance")
+    return bool(r.value)
 
 
 def qvts_trace_best_first(h):
@@ -450,6 +459,9 @@ class Model:
 
     def trace_best_first(self):
         return qvts_trace_best_first(self.h)
+
+    def bf_advance(self, action, z):
+        return qvts_bf_advance(self.h, action, z)
 
     def run_episodes(self, n_episodes, **kw):
         return qvts_run_episodes(self.h, n_episodes, **kw)

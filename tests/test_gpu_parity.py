@@ -391,3 +391,57 @@ def test_best_first_stop_rules(Q):
     if res.stop_reason == Q.QVTS_BF_TIME:
         assert res.n_expansions > 0 and dt < 20.0 + 50.0
     g.close()
+
+
+def _bf_compare(tr, r, scale, alive_only=False):
+    ov = r["v"]
+    idx = {int(p): i for i, p in enumerate(ov["path"]) if ov["depth"][i] >= 0}
+    n = 0
+    for i, p in enumerate(tr["path"]):
+        if tr["depth"][i] < 0:
+            continue
+        j = idx[int(p)]
+        n += 1
+        assert tr["f"][i] == ov["f"][j] and tr["depth"][i] == ov["depth"][j]
+        assert abs(tr["U"][i] - ov["U"][j]) <= PT.TOL * scale
+        assert abs(tr["L"][i] - ov["L"][j]) <= PT.TOL * scale
+        assert abs(tr["H"][i] - ov["H"][j]) <= 2 * PT.TOL * scale
+    assert n == len(idx)
+
+
+def test_best_first_tree_reuse_against_oracle(Q):
+    """NEXT-4 (tree reuse): plan, s.update(a, z) keeps the sampled (a, z) subtree with relative
+    paths, then more expansions continue it; both trees against the oracle's re-rooted tree."""
+    gm, mask = MAPS["ragged"][0](), MAPS["ragged"][1]
+    b32 = np.asarray(W.uniform_belief(gm), np.float32)
+    g, o, Ao, alo, acto = _bf_pair(Q, gm, mask, b32, dict(expansions=3, max_points=12, seed=5, sweeps=20))
+    res1 = g.plan_best_first(dev(b32), 8, 25, max_depth=6, seed=2, step=0)
+    tr1 = g.trace_best_first()
+    t = O.BfTree(o, Ao, alo, acto, b32.astype(np.float64), 8, 25, max_depth=6, seed=2, step=0,
+                 replay=tr1["path"][tr1["exp_order"]])
+    r1 = t.result()
+    assert r1["mism"] == 0 and r1["n_exp"] == res1.n_expansions
+    scale = max(1.0, float(np.max(np.abs(r1["v"]["U"]))))
+    _bf_compare(tr1, r1, scale)
+    a_id = res1.action
+    kids = [i for i in range(len(tr1["path"])) if tr1["depth"][i] == 1 and (int(tr1["path"][i]) & 15) == a_id + 1]
+    z = int(tr1["path"][kids[-1]]) >> 4 & 15
+    assert g.bf_advance(a_id, z) and t.advance(a_id, z)
+    absent = [zz for zz in range(16) if all((int(tr1["path"][i]) >> 4 & 15) != zz for i in kids)]
+    res2 = g.plan_best_first(None, 8, 20, max_depth=6, seed=2, step=1, reuse=True)
+    tr2 = g.trace_best_first()
+    r2 = t.cont(8, 20, max_depth=6, seed=2, step=1, replay=tr2["path"][tr2["exp_order"]])
+    assert r2["mism"] == 0 and r2["n_exp"] == res2.n_expansions and r2["stop"] == res2.stop_reason
+    _bf_compare(tr2, r2, scale)
+    assert abs(res2.U - r2["U"]) <= PT.TOL * scale and abs(res2.L - r2["L"]) <= PT.TOL * scale
+    assert np.max(np.abs(tr2["root_trace"] - r2["root_trace"])) <= PT.TOL * scale
+    j = g.action_ids.index(res2.action)
+    assert res2.action == r2["action"] or r2["LQ"][j] >= np.max(r2["LQ"]) - PT.TIE * scale
+    if absent:   # the new root's unsampled z: no reuse
+        kids2 = [i for i in range(len(tr2["path"])) if tr2["depth"][i] == 1 and (int(tr2["path"][i]) & 15) == res2.action + 1]
+        zs2 = {int(tr2["path"][i]) >> 4 & 15 for i in kids2}
+        miss = [zz for zz in range(16) if zz not in zs2]
+        if kids2 and miss:
+            assert not g.bf_advance(res2.action, miss[0])
+    t.close()
+    g.close()
