@@ -445,3 +445,35 @@ def test_best_first_tree_reuse_against_oracle(Q):
             assert not g.bf_advance(res2.action, miss[0])
     t.close()
     g.close()
+
+
+# ---- edge shapes and degenerate cases ----------------------------------------------------------
+@pytest.mark.parametrize("H,Wd,mask", [(1, 40, W.A8), (3, 203, W.A8), (203, 3, W.A4), (2, 2, W.A9)])
+def test_plan_extreme_shapes(Q, H, Wd, mask):
+    """One-row, very wide, very tall and 2x2 grids: band construction, halos and clamping at the
+    map edge on every side."""
+    gm = W.random_map(H, Wd, 0.05, seed=11) if H * Wd > 4 else W.from_ascii("G.\n..")
+    run_parity(Q, gm, mask, 2, 4, W.random_belief(gm, 2))
+
+
+def test_plan_single_free_cell(Q):
+    """Every move is blocked: all mass stays, one observation, a one-child chain per action."""
+    gm = W.from_ascii("###\n#G#\n###")
+    res, _, _ = run_parity(Q, gm, W.A9, 3, 8, W.uniform_belief(gm))
+    assert res.n_vnodes[1] >= 9 and res.n_vnodes[3] >= 9 ** 3
+
+
+def test_plan_depth8_single_draw(Q):
+    """The maximum depth (8 action levels, the tree-path limit) with n = 1: 4^8 leaves."""
+    gm = W.from_ascii("..#.\n.G..\n#...")
+    res, _, _ = run_parity(Q, gm, W.A4, 8, 1, W.uniform_belief(gm), beliefs=False)
+    assert res.n_vnodes[8] == 4 ** 8
+
+
+def test_plan_point_mass_root_and_max_n(Q):
+    """A point-mass root in a corner, and the maximum draw count n = 4096 at depth 1."""
+    gm = W.random_map(9, 12, 0.15, seed=6)
+    b = np.zeros(gm.occupancy.size)
+    b[int(np.flatnonzero(gm.occupancy == 0)[0])] = 1.0
+    run_parity(Q, gm, W.A8, 3, 8, b)
+    run_parity(Q, gm, W.A8, 1, 4096, W.random_belief(gm, 4))
