@@ -535,7 +535,7 @@ extern "C" void qvts_model_destroy(qvts_model *m) {
                       &m->d_Q64, &m->part, &m->tickets, &m->xs, &m->scan_tmp, &m->total, &m->counters, &m->vshard,
                       &m->ep_b[0], &m->ep_b[1], &m->ep_state, &m->ep_root_step, &m->ep_root_ep,
                       &m->pb_b0, &m->pb_B, &m->pb_G, &m->pb_Gn, &m->pb_GT, &m->pb_Bbar, &m->pb_Sc, &m->pb_Rb,
-                      &m->pb_sel, &m->pb_astar, &m->pb_cand, &m->pb_misc, &m->pb_cls};
+                      &m->pb_sel, &m->pb_astar, &m->pb_cand, &m->pb_misc, &m->pb_cls, &m->pb_chunks, &m->pb_part};
     for (DevBuf *b : bufs) b->release();
     for (BandSet *bs : {&m->band_big, &m->band_small}) {
         bs->bands.release(); bs->entries.release(); bs->slot_cell.release(); bs->qlist.release(); bs->qlist_fib.release();

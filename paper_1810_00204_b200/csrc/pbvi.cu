@@ -10,7 +10,8 @@
 //   alpha*_{a,z} = argmax_alpha b . g^alpha_{a,z} = argmax_alpha sum_s O[s][z] sum_{sig(x')=s} bbar_a(x') alpha(x'),
 //   a* = argmax_a [b . R(.,a) + gamma sum_z max_alpha b . g],   ties to the lowest index.
 // The b . g values are signature-binned like the leaf kernel: Sc[b][a][s][k] over the free cells
-// of class s (a static class-sorted cell list), then 16x16 O weights.
+// of class s (a static class-sorted cell list, split into chunks for a split-K fp64 product),
+// then 16x16 O weights.
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -76,22 +77,57 @@ __global__ void k_pb_rb(PbviDev d, const double *__restrict__ B, double *__restr
     if (threadIdx.x == 0) Rb[blockIdx.x] = red[0];
 }
 
-// Sc[i][a][s][k] = sum over free cells x of class s of bbar_{i,a}(x) alpha_k(x); one block per
-// (i, a), thread k; GT is alpha transposed [HW][P] so the reads coalesce over k.
-__global__ void k_pb_bins(PbviDev d, const double *__restrict__ Bbar, const double *__restrict__ GT, int nal,
-                          const int32_t *__restrict__ cls_cells, const int32_t *__restrict__ cls_off,
-                          double *__restrict__ Sc) {
-    const int ia = blockIdx.x;          // i * NA + a
-    const double *bb = Bbar + (size_t)ia * d.HW;
-    for (int k = threadIdx.x; k < nal; k += blockDim.x)
-        for (int s = 0; s < 16; ++s) {
-            double acc = 0.0;
-            for (int e = cls_off[s]; e < cls_off[s + 1]; ++e) {
-                const int x = cls_cells[e];
-                acc += bb[x] * GT[(size_t)x * d.P + k];
-            }
-            Sc[((size_t)ia * 16 + s) * d.P + k] = acc;
-        }
+// Sc as a split-K product over the class-sorted free cells: CTA (chunk, row block, vector block)
+// takes one chunk (<= 64 cells of ONE class) and a 32 x 32 tile of (point-action row, alpha k),
+// stages the gathered rows of bbar and the alpha columns in shared memory, and writes one fp64
+// partial per (chunk, row, k); k_pb_bins_sum adds a class's chunks in order.
+constexpr int kPbCh = 64;
+__global__ void __launch_bounds__(256) k_pb_bins_part(const double *__restrict__ Bbar, int HW, int nrows,
+                                                      const double *__restrict__ GT, int P, int nal,
+                                                      const int32_t *__restrict__ cells,
+                                                      const int2 *__restrict__ chunks, double *__restrict__ part,
+                                                      int rows_pad) {
+    __shared__ double Bs[32][kPbCh + 1];
+    __shared__ double Gs[kPbCh][33];
+    const int2 ch = chunks[blockIdx.x];                 // [e0, e1)
+    const int n = ch.y - ch.x;
+    const int r0 = blockIdx.y * 32, k0 = blockIdx.z * 32;
+    const int t = threadIdx.x;
+    for (int i = t; i < 32 * n; i += 256) {
+        const int r = i / n, e = i % n;
+        const int x = cells[ch.x + e];
+        Bs[r][e] = (r0 + r < nrows) ? Bbar[(size_t)(r0 + r) * HW + x] : 0.0;
+    }
+    for (int i = t; i < n * 32; i += 256) {
+        const int e = i >> 5, k = i & 31;
+        const int x = cells[ch.x + e];
+        Gs[e][k] = (k0 + k < nal) ? GT[(size_t)x * P + k0 + k] : 0.0;
+    }
+    __syncthreads();
+    const int tr = t >> 4, tk = t & 15;                 // rows tr, tr+16; vectors tk, tk+16
+    double a00 = 0.0, a01 = 0.0, a10 = 0.0, a11 = 0.0;
+    for (int e = 0; e < n; ++e) {
+        const double b0 = Bs[tr][e], b1 = Bs[tr + 16][e], g0 = Gs[e][tk], g1 = Gs[e][tk + 16];
+        a00 = fma(b0, g0, a00); a01 = fma(b0, g1, a01);
+        a10 = fma(b1, g0, a10); a11 = fma(b1, g1, a11);
+    }
+    double *out = part + (size_t)blockIdx.x * rows_pad * 32 * gridDim.z;
+    const size_t pitch = (size_t)32 * gridDim.z;        // [chunk][row][k]
+    out[(size_t)(r0 + tr) * pitch + k0 + tk] = a00;
+    out[(size_t)(r0 + tr) * pitch + k0 + tk + 16] = a01;
+    out[(size_t)(r0 + tr + 16) * pitch + k0 + tk] = a10;
+    out[(size_t)(r0 + tr + 16) * pitch + k0 + tk + 16] = a11;
+}
+
+// Sc[row][s][k] = sum of class s's chunk partials in chunk order (zero for an empty class)
+__global__ void k_pb_bins_sum(const double *__restrict__ part, const int32_t *__restrict__ cls_chunk, int nrows,
+                              int nal, int P, int rows_pad, int kpad, double *__restrict__ Sc) {
+    const long long tt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (tt >= (long long)nrows * 16 * nal) return;
+    const int k = (int)(tt % nal), s = (int)((tt / nal) % 16), r = (int)(tt / ((long long)nal * 16));
+    double acc = 0.0;
+    for (int c = cls_chunk[s]; c < cls_chunk[s + 1]; ++c) acc += part[((size_t)c * rows_pad + r) * kpad + k];
+    Sc[((size_t)r * 16 + s) * P + k] = acc;
 }
 
 // per point: alpha*_{a,z} (lane z of warp a) and a* (ties: lowest index, strict >)
@@ -348,6 +384,18 @@ static qvts_status pbvi_run(Model &m, const double *b0_dev, int expansions, int 
         for (int x = 0; x < HW; ++x) if (!m.occ[x] && m.sig[x] == s) cells.push_back(x);
     }
     off[16] = (int32_t)cells.size();
+    // chunks of <= kPbCh cells that never cross a class boundary, and each class's chunk range
+    std::vector<int2> chunks;
+    std::vector<int32_t> cls_chunk(17, 0);
+    for (int s2 = 0; s2 < 16; ++s2) {
+        cls_chunk[s2] = (int32_t)chunks.size();
+        for (int e0 = off[s2]; e0 < off[s2 + 1]; e0 += kPbCh) chunks.push_back(make_int2(e0, std::min(off[s2 + 1], e0 + kPbCh)));
+    }
+    cls_chunk[16] = (int32_t)chunks.size();
+    QVTS_TRY(m.pb_chunks.ensure(sizeof(int2) * std::max<size_t>(1, chunks.size()) + sizeof(int32_t) * 17));
+    QVTS_CUDA(cudaMemcpyAsync(m.pb_chunks.p, chunks.data(), sizeof(int2) * chunks.size(), cudaMemcpyHostToDevice, st));
+    int32_t *d_cls_chunk = reinterpret_cast<int32_t *>(m.pb_chunks.as<int2>() + std::max<size_t>(1, chunks.size()));
+    QVTS_CUDA(cudaMemcpyAsync(d_cls_chunk, cls_chunk.data(), sizeof(int32_t) * 17, cudaMemcpyHostToDevice, st));
     QVTS_TRY(m.pb_cls.ensure(sizeof(int32_t) * (cells.size() + 17)));
     QVTS_CUDA(cudaMemcpyAsync(m.pb_cls.p, off.data(), sizeof(int32_t) * 17, cudaMemcpyHostToDevice, st));
     QVTS_CUDA(cudaMemcpyAsync(m.pb_cls.as<int32_t>() + 17, cells.data(), sizeof(int32_t) * cells.size(),
@@ -403,8 +451,20 @@ static qvts_status pbvi_run(Model &m, const double *b0_dev, int expansions, int 
     k_pb_rb<<<nb * NA, 256, 0, st>>>(d, B, m.pb_Rb.as<double>());
     for (int sw = 0; sw < sweeps; ++sw) {
         k_pb_transpose<<<(unsigned)(((long long)nal * HW + 255) / 256), 256, 0, st>>>(G, nal, HW, P, GT);
-        k_pb_bins<<<nb * NA, std::min(256, ((nal + 31) / 32) * 32), 0, st>>>(
-            d, m.pb_Bbar.as<double>(), GT, nal, m.pb_cls.as<int32_t>() + 17, m.pb_cls.as<int32_t>(), m.pb_Sc.as<double>());
+        {
+            const int nrows = nb * NA, rows_pad = ((nrows + 31) / 32) * 32, kb = (nal + 31) / 32;
+            const size_t nch = chunks.size();
+            if (nch > 0) {
+                QVTS_TRY(m.pb_part.ensure(sizeof(double) * nch * rows_pad * 32 * kb));
+                k_pb_bins_part<<<dim3((unsigned)nch, rows_pad / 32, kb), 256, 0, st>>>(
+                    m.pb_Bbar.as<double>(), HW, nrows, GT, P, nal, m.pb_cls.as<int32_t>() + 17, m.pb_chunks.as<int2>(),
+                    m.pb_part.as<double>(), rows_pad);
+            }
+            const long long nout = (long long)nrows * 16 * nal;
+            k_pb_bins_sum<<<(unsigned)((nout + 255) / 256), 256, 0, st>>>(m.pb_part.as<double>(), d_cls_chunk, nrows,
+                                                                         nal, P, rows_pad, 32 * kb,
+                                                                         m.pb_Sc.as<double>());
+        }
         k_pb_select<<<nb, NA * 32, 0, st>>>(d, m.pb_Sc.as<double>(), m.pb_Rb.as<double>(), nal, m.pb_sel.as<int32_t>(),
                                             m.pb_astar.as<int32_t>());
         k_pb_newalpha<MASK><<<(unsigned)((nbx + 255) / 256), 256, 0, st>>>(d, G, nb, m.pb_sel.as<int32_t>(),

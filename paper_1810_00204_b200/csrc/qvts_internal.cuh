@@ -116,7 +116,8 @@ struct Model {
     bool have_pbvi = false;
     int pb_np = 0, pb_nal = 0, pb_P = 0;
     std::vector<int32_t> pb_act;
-    DevBuf pb_b0, pb_B, pb_G, pb_Gn, pb_GT, pb_Bbar, pb_Sc, pb_Rb, pb_sel, pb_astar, pb_cand, pb_misc, pb_cls;
+    DevBuf pb_b0, pb_B, pb_G, pb_Gn, pb_GT, pb_Bbar, pb_Sc, pb_Rb, pb_sel, pb_astar, pb_cand, pb_misc, pb_cls, pb_chunks,
+        pb_part;
     // anytime best-first QVTS (NEXT-2, bestfirst.cu): node pool of the last qvts_plan_best_first
     bool bf_valid = false;
     long long bf_nv = 0, bf_nq = 0, bf_nq0 = 0;

@@ -28,6 +28,11 @@ t0 = time.perf_counter()
 n_pts = Q.qvts_pbvi(m.h, b, 4, PTS, 1, 30)
 torch.cuda.synchronize()
 out["pbvi"] = {"s": time.perf_counter() - t0, "points": n_pts, "sweeps": 30}
+t0 = time.perf_counter()
+n_big = Q.qvts_pbvi(m.h, b, 7, 128, 1, 30)
+torch.cuda.synchronize()
+out["pbvi_128"] = {"s": time.perf_counter() - t0, "points": n_big, "sweeps": 30, "expansion_rounds": 7}
+Q.qvts_pbvi(m.h, b, 4, PTS, 1, 30)   # the set the planner below uses
 for n, E in ((16, 50), (16, 400), (16, 2000)):
     m.plan_best_first(b, n, E, max_depth=8, seed=1)        # warm (pool sized, graph path)
     torch.cuda.synchronize()
