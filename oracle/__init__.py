@@ -13,7 +13,9 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+# QVTS_ORACLE_LIB: load a prebuilt oracle library instead (tools/oracle_mutations.py runs the pins
+# against deliberately broken copies to show they catch plausible mistakes)
+_LIB_PATH = os.environ.get("QVTS_ORACLE_LIB") or os.path.join(_HERE, "liboracle.so")
 
 OK, ERR_INVALID_ARG, ERR_INVALID_MODEL, ERR_NOT_CONVERGED, ERR_ZERO_LIKELIHOOD = 0, 1, 2, 4, 5
 MODE_FREQ, MODE_EXACT, MODE_BRUTE = 0, 1, 2
@@ -22,6 +24,8 @@ SAMPLER_MARGINAL, SAMPLER_ANCESTRAL = 0, 1
 
 
 def build() -> str:
+    if os.environ.get("QVTS_ORACLE_LIB"):
+        return _LIB_PATH
     src = os.path.join(_HERE, "qvts_oracle.c")
     if not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(src):
         subprocess.run(["make", "-s", "-C", _HERE], check=True)

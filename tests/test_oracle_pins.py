@@ -106,6 +106,19 @@ def test_reward_examples():
     assert m.R(8, 4) == -2.0           # stay off goal
 
 
+def test_reward_collision_cases():
+    """PAPER.md:338-355 by hand: R(x,a) = sum_y r(y) T'(x,a,y) with the pre-clamp T', r = -2 on an
+    occupied or off-map target, -1 on a free non-goal cell; laterals are the ring neighbours (R3)."""
+    m = O.Model.grid(open3x3(goal=8))
+    # corner 0, action 0 (up-left): intended and both laterals (1 up, 3 left) leave the map
+    assert m.R(0, 0) == pytest.approx(0.8 * -2 + 0.1 * -1 + 0.05 * -2 + 0.05 * -2, abs=1e-15)
+    m = O.Model.grid(open3x3(goal=8, blocked=(4,)))
+    # cell 1, action 7 (down) into the occupied centre; laterals 8 -> cell 5, 6 -> cell 3 are free
+    assert m.R(1, 7) == pytest.approx(0.8 * -2 + 0.1 * -1 + 0.05 * -1 + 0.05 * -1, abs=1e-15)
+    # cell 7, action 5 (right) onto the goal 8: laterals 2 -> cell 5 (free), 8 -> off the map
+    assert m.R(7, 5) == pytest.approx(0.8 * 0 + 0.1 * -1 + 0.05 * -1 + 0.05 * -2, abs=1e-15)
+
+
 # ---- P3 / P4 / P11 Eq. 3 -------------------------------------------------------------------
 def test_bayes_two_state_example():
     T = np.zeros((2, 1, 2)); T[0, 0, 0] = 1; T[1, 0, 1] = 1
@@ -481,10 +494,11 @@ def test_ancestral_sampler_in_plan_matches_alg4_and_marginal():
 
 
 # ---- NEXT-2 (part A): PBVI lower bound (§IV-B) --------------------------------------------------
-def _chain(nx=5, gamma=0.9):
+def _chain(nx=5, gamma=0.9, left_cost=-1.0):
     """Deterministic left/right chain, perfectly observed (O = identity), goal at the right end."""
     T = np.zeros((nx, 2, nx))
     R = np.full((nx, 2), -1.0)
+    R[:, 0] = left_cost
     for x in range(nx):
         T[x, 0, max(0, x - 1)] = 1
         T[x, 1, min(nx - 1, x + 1)] = 1
@@ -511,6 +525,21 @@ def test_pbvi_perfect_observation_chain_reaches_mdp_values():
         x = int(np.argmax(b))
         assert b[x] == 1.0
         assert max(a @ b for a in al) == pytest.approx(V[x], abs=1e-9)
+
+
+def test_pbvi_backup_uses_the_chosen_actions_reward():
+    """Action-dependent rewards on the perfectly observed chain (left costs -2): PBVI's point
+    backups still reach V*(x) at the point masses, which requires R(., a*) of the chosen a*."""
+    m = _chain(left_cost=-2.0)
+    b0 = np.eye(5)[0]
+    pts, al, act = m.pbvi(b0, expansions=6, max_points=8, seed=3, sweeps=400)
+    _, V, Q, _, _ = m.value_iteration(1e-12)
+    for b in pts:
+        x = int(np.argmax(b))
+        assert max(a @ b for a in al) == pytest.approx(V[x], abs=1e-9)
+    for b, a in zip(pts, act):                    # moving right is optimal everywhere but the goal
+        if int(np.argmax(b)) != 4:
+            assert a == 1
 
 
 def test_pbvi_sandwich_and_monotone_sweeps():
