@@ -13,7 +13,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# QVTS_ORACLE_LIB: load a prebuilt oracle library instead (tools/oracle_mutations.py runs the pins
+# QVTS_ORACLE_LIB: load a prebuilt oracle library instead (tests/oracle_mutations.py runs the pins
 # against deliberately broken copies to show they catch plausible mistakes)
 _LIB_PATH = os.environ.get("QVTS_ORACLE_LIB") or os.path.join(_HERE, "liboracle.so")
 

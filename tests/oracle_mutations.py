@@ -8,7 +8,7 @@ import subprocess
 import sys
 import tempfile
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))   # repo root (this file: tests/)
 SRC = open(os.path.join(ROOT, "oracle", "qvts_oracle.c")).read()
 
 MUTANTS = [
