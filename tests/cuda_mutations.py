@@ -1,0 +1,80 @@
+"""Mutation check of the GPU parity tests: one-line mutants of the CUDA sources, each built into
+variants/mut_<k>.so; `--run` (on a B200) loads each through QVTS_LIB and runs a fast subset of the
+`-m gpu` parity tests, which must fail.  `python tests/cuda_mutations.py --build` here (nvcc
+cross-compiles), then `python tests/cuda_mutations.py --run` on the GPU box.  Prints JSON."""
+import json
+import os
+import shutil
+import subprocess
+import sys
+import tempfile
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))   # repo root (this file: tests/)
+CSRC = os.path.join(ROOT, "paper_1810_00204_b200", "csrc")
+OUT = os.path.join(ROOT, "variants")
+
+MUTANTS = [
+    ("S4: correct without the 1/P(z) normaliser", "plan.cu",
+     "s_w[u][sg] = (float)(a.O64[sg * 16 + z] / a.P[q * 16 + z]);", "s_w[u][sg] = (float)(a.O64[sg * 16 + z]);"),
+    ("S3: Philox key halves swapped", "plan.cu", "make_uint2(a.seed, ep));", "make_uint2(ep, a.seed));"),
+    ("S6: gamma dropped in the backup", "plan.cu", "const double qv = R[q] + gamma * acc;", "const double qv = R[q] + acc;"),
+    ("S1: lateral ring neighbour off by one", "stencil.cuh", "return ring_at((ring_pos(k) + 7) % 8);",
+     "return ring_at((ring_pos(k) + 6) % 8);"),
+    ("S1/S2: diagonal blocked mass not kept at y", "plan.cu", "                h += b0;\n", "\n"),
+    ("NEXT-1: gamma dropped in the FIB sweep", "model.cu", "out = R64[(size_t)j * HW + x] + gamma * s;",
+     "out = R64[(size_t)j * HW + x] + s;"),
+    ("S7: gamma dropped in value iteration", "model.cu", "    return R64[(size_t)j * HW + x] + gamma * s;\n}",
+     "    return R64[(size_t)j * HW + x] + s;\n}"),
+    ("NEXT-2: PBVI alpha* by the first instead of the best vector", "pbvi.cu", "if (k == 0 || pb_beats(v, bz)) { bz = v; bk = k; }",
+     "if (k == 0) { bz = v; bk = k; }"),
+    ("S2: R(b,a) identity with p_stay instead of p_stay - 1", "plan.cu", "R = (a.p_stay - 1.0) * mass - Rp;",
+     "R = a.p_stay * mass - Rp;"),
+    ("S5: leaf offset qbar not added back", "plan.cu", "Vz = a.qbar + Vz / Pexact;", "Vz = Vz / Pexact;"),
+    ("best-first Alg. 7: heuristic child by H instead of U", "bestfirst.cu", "if (U[j] > U[bq]) bq = j;",
+     "if (H[j] > H[bq]) bq = j;"),
+]
+SUBSET = ("test_tables_and_value_iteration or test_belief_update or test_plan_C1_full_tree or "
+          "test_plan_ragged_depth3 or test_best_first_against_oracle or test_pbvi_against_oracle")
+
+
+def build():
+    os.makedirs(OUT, exist_ok=True)
+    res = []
+    for k, (name, fname, old, new) in enumerate(MUTANTS):
+        with tempfile.TemporaryDirectory() as tmp:
+            d = os.path.join(tmp, "pkg", "csrc")          # csrc/../../include -> tmp/include
+            shutil.copytree(CSRC, d, ignore=shutil.ignore_patterns("*.o", "*.log"))
+            shutil.copytree(os.path.join(ROOT, "include"), os.path.join(tmp, "include"))
+            path = os.path.join(d, fname)
+            src = open(path).read()
+            if src.count(old) != 1:
+                res.append({"mutant": name, "status": f"pattern count {src.count(old)}"})
+                continue
+            open(path, "w").write(src.replace(old, new))
+            lib = os.path.join(OUT, f"mut_{k}.so")
+            r = subprocess.run(["make", "-s", "-j4", "-C", d, f"LIB={lib}"], capture_output=True, text=True)
+            res.append({"mutant": name, "lib": os.path.basename(lib), "built": r.returncode == 0,
+                        "err": r.stderr[-300:] if r.returncode else ""})
+        print(json.dumps(res[-1]), flush=True)
+    json.dump(res, open(os.path.join(OUT, "mutants.json"), "w"))
+
+
+def run():
+    res = json.load(open(os.path.join(OUT, "mutants.json")))
+    caught = 0
+    for r in res:
+        if not r.get("built"):
+            continue
+        env = dict(os.environ, QVTS_LIB=os.path.join(OUT, r["lib"]))
+        p = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                            "-k", SUBSET, os.path.join(ROOT, "tests", "test_gpu_parity.py")], cwd=ROOT, env=env,
+                           capture_output=True, text=True, timeout=900)
+        r["caught"] = p.returncode != 0
+        r["first_failing"] = [l.split("::")[-1][:80] for l in p.stdout.splitlines() if l.startswith("FAILED")][:1]
+        caught += r["caught"]
+        print(json.dumps(r), flush=True)
+    print(json.dumps({"caught": caught, "total": len(res), "mutants": res}))
+
+
+if __name__ == "__main__":
+    build() if "--build" in sys.argv else run()
