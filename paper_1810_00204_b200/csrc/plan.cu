@@ -547,11 +547,9 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_hist(HistArgs a) {
     // after the tile (m8 = 0, Q' = 0), so they need no branch.
     const uint32_t tbase = (uint32_t)__cvta_generic_to_shared(smem + p * a.tstride);
     const uint32_t TP4 = 4u * (uint32_t)TP;
-    auto cell = [&](uint32_t e, const float4 (&qv)[LEAF ? NAP / 4 : 1]) {
+    auto load_nb = [&](uint32_t e, float (&nb)[9]) {
         const uint32_t c0 = tbase + ((e & 0xFFFFu) << 2);
-        const uint32_t m8 = e >> 16;
         const uint32_t cu = c0 - TP4, cd = c0 + TP4;
-        float nb[9];
         asm volatile("ld.shared.f32 %0, [%1+-4];" : "=f"(nb[0]) : "r"(cu));
         asm volatile("ld.shared.f32 %0, [%1];" : "=f"(nb[1]) : "r"(cu));
         asm volatile("ld.shared.f32 %0, [%1+4];" : "=f"(nb[2]) : "r"(cu));
@@ -561,6 +559,9 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_hist(HistArgs a) {
         asm volatile("ld.shared.f32 %0, [%1+-4];" : "=f"(nb[6]) : "r"(cd));
         asm volatile("ld.shared.f32 %0, [%1];" : "=f"(nb[7]) : "r"(cd));
         asm volatile("ld.shared.f32 %0, [%1+4];" : "=f"(nb[8]) : "r"(cd));
+    };
+    auto cell = [&](uint32_t e, const float (&nb)[9], const float4 (&qv)[LEAF ? NAP / 4 : 1]) {
+        const uint32_t m8 = e >> 16;
         float q[LEAF ? NAP : 1];
         if (LEAF) {
 #pragma unroll
@@ -592,7 +593,8 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_hist(HistArgs a) {
         }
     };
     // Slot streams are padded on the host by >= 4 steps (pads = the zero cell), so the loads
-    // below never need a bound check.  Entries run two slots ahead, Q' rows one (ping-pong).
+    // below never need a bound check.  Entries run two slots ahead, Q' rows one (ping-pong), the
+    // next cell's neighbourhood is loaded before the current cell is accumulated.
     const uint32_t *ep = a.entries + soff + st;
     const float4 *qp = a.qlist + (soff + st) * (NAP / 4);
     constexpr int QSTEP = T * (NAP / 4);
@@ -602,19 +604,23 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_hist(HistArgs a) {
 #pragma unroll
         for (int h = 0; h < (LEAF ? NAP / 4 : 0); ++h) qA[h] = __ldg(qp + h);
     }
+    float nbA[9], nbB[9];
+    load_nb(eA, nbA);
     for (int i = 0; i < L; i += 2) {
         eC = __ldg(ep + 2 * T);
         if (LEAF) {
 #pragma unroll
             for (int h = 0; h < (LEAF ? NAP / 4 : 0); ++h) qB[h] = __ldg(qp + QSTEP + h);
         }
-        cell(eA, qA);
+        load_nb(eB, nbB);
+        cell(eA, nbA, qA);
         eD = __ldg(ep + 3 * T);
         if (LEAF) {
 #pragma unroll
             for (int h = 0; h < (LEAF ? NAP / 4 : 0); ++h) qA[h] = __ldg(qp + 2 * QSTEP + h);
         }
-        cell(eB, qB);
+        load_nb(eC, nbA);
+        cell(eB, nbB, qB);
         eA = eC;
         eB = eD;
         ep += 2 * T;

@@ -1,6 +1,6 @@
 #!/bin/bash
 # A/B timing of library variants (variants/libqvts_*.so): bench.py kernel times per variant, twice.
-for rep in 1 2; do
+for rep in 1 2 3; do
   for f in variants/libqvts_*.so; do
     n=$(basename $f .so)
     QVTS_LIB=$PWD/$f timeout 600 python bench.py --steps 4 --warmup 2 --no-cpu-baseline > gpurun_out/ab_$n.log 2>&1
