@@ -344,8 +344,15 @@ __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int
     __syncthreads();   // rsm may be reused by the caller
 }
 
+// k_reduce is latency-bound on its band-partial loads: ~1536 resident threads per SM beat the
+// registers that cost (measured at A8: 6 blocks of 256 -> leaf launch 7.4 -> 4.5 ms)
+template <uint32_t MASK>
+__host__ __device__ constexpr int reduce_min_blocks() {
+    return 1536 / (mask_count(MASK) * 32) > 8 ? 8 : 1536 / (mask_count(MASK) * 32);
+}
+
 template <uint32_t MASK, bool LEAF>
-__global__ void __launch_bounds__(mask_count(MASK) * 32) k_reduce(ReduceArgs a) {
+__global__ void __launch_bounds__(mask_count(MASK) * 32, reduce_min_blocks<MASK>()) k_reduce(ReduceArgs a) {
     extern __shared__ double rsm[];
     if (a.skip && *a.skip) return;
     reduce_parent<MASK, LEAF>(a, blockIdx.x, rsm, mask_count(MASK) * 32);
