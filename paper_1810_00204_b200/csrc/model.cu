@@ -486,6 +486,16 @@ extern "C" qvts_status qvts_model_create(const qvts_model_desc *d, qvts_model **
             }
     }
     m->ngc = (int)gc_cell.size();
+    // fused leaf level: the distinct cells whose belief R(b,a) reads (goal first), and for every
+    // goal term the index of its cell in that list
+    std::vector<int32_t> fcells{m->goal}, gc_fidx;
+    for (int32_t x : gc_cell) {
+        int f = -1;
+        for (size_t i = 0; i < fcells.size(); ++i) if (fcells[i] == x) f = (int)i;
+        if (f < 0) { f = (int)fcells.size(); fcells.push_back(x); }
+        gc_fidx.push_back(f);
+    }
+    m->nfcells = (int)fcells.size();
     m->n_free = 0;
     for (int x = 0; x < HW; ++x) m->n_free += m->occ[x] ? 0 : 1;
     std::vector<uint8_t> freev(HW), cell(HW);
@@ -505,6 +515,8 @@ extern "C" qvts_status qvts_model_create(const qvts_model_desc *d, qvts_model **
         if ((st = upload(m->d_O64, O64)) != QVTS_OK) break;
         if ((st = upload(m->d_O32, O32)) != QVTS_OK) break;
         if ((st = upload(m->d_gc_cell, gc_cell)) != QVTS_OK) break;
+        if ((st = upload(m->d_fcells, fcells)) != QVTS_OK) break;
+        if (!gc_fidx.empty() && (st = upload(m->d_gc_fidx, gc_fidx)) != QVTS_OK) break;
         if ((st = upload(m->d_gc_act, gc_act)) != QVTS_OK) break;
         if ((st = upload(m->d_gc_val, gc_val)) != QVTS_OK) break;
         // band sets: ~16K cells per band for many parents, ~2K for few (more CTAs per parent)
@@ -530,7 +542,7 @@ extern "C" void qvts_model_destroy(qvts_model *m) {
     if (!m) return;
     cudaSetDevice(m->device);
     DevBuf *bufs[] = {&m->d_m8, &m->d_sig, &m->d_cell, &m->bu_R, &m->bu_P, &m->bu_cnt, &m->bu_umask,
-                      &m->bu_U, &m->bu_off, &m->bu_path, &m->bu_root, &m->bu_key, &m->d_ctab, &m->d_R64, &m->d_O64, &m->d_O32, &m->d_gc_cell,
+                      &m->bu_U, &m->bu_off, &m->bu_path, &m->bu_root, &m->bu_key, &m->d_ctab, &m->d_R64, &m->d_O64, &m->d_O32, &m->d_gc_cell, &m->d_fcells, &m->d_gc_fidx, &m->fl_goalv,
                       &m->d_gc_act, &m->d_gc_val, &m->d_free, &m->d_V[0], &m->d_V[1], &m->d_A[0], &m->d_A[1], &m->d_alpha64, &m->d_resid,
                       &m->d_Q64, &m->part, &m->tickets, &m->xs, &m->scan_tmp, &m->total, &m->counters, &m->vshard,
                       &m->ep_b[0], &m->ep_b[1], &m->ep_state, &m->ep_root_step, &m->ep_root_ep,

@@ -82,6 +82,10 @@ struct ReduceArgs {
     int W;
     double acc;
     const int32_t *skip = nullptr;  // device flag: non-zero -> the launch does nothing (best-first)
+    // fused leaf level: the leaf parents' beliefs at the goal-term cells [v][nf] (k_child_meta)
+    const float *goalv = nullptr;
+    int nf = 0;
+    const int32_t *gc_fidx = nullptr;
 };
 
 // tree level of a V-node path: one non-zero byte per action level (low nibble a+1 >= 1)
@@ -216,12 +220,13 @@ __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int
     double R = 0.0;
     if (lane == 0) {
         if (k == 4) {
-            R = -2.0 * mass + 2.0 * (double)bp[a.goal];
+            R = -2.0 * mass + 2.0 * (double)(a.goalv ? a.goalv[v * a.nf] : bp[a.goal]);
         } else {
             const double Rp = a.p_stay * mass + a.p_int * sE[da] + a.p_lat * (sE[d1] + sE[d2]);
             R = (a.p_stay - 1.0) * mass - Rp;
             for (int g = 0; g < a.ngc; ++g)
-                if (a.gc_act[g] == j) R += a.gc_val[g] * (double)bp[a.gc_cell[g]];
+                if (a.gc_act[g] == j)
+                    R += a.gc_val[g] * (double)(a.goalv ? a.goalv[v * a.nf + a.gc_fidx[g]] : bp[a.gc_cell[g]]);
         }
     }
     // P(z|b,a) = sum_s O[s][z] M[s]  (fixed s order)
@@ -442,6 +447,134 @@ __global__ void __launch_bounds__(256) k_ancestral_x(const float *__restrict__ b
 // the two half-warps so the static per-slot loads (entry, Q') are shared.  The CTAs of the bands
 // of one parent pair form a thread-block cluster and sum their class totals through DSMEM, so a
 // single fp64 partial per parent reaches HBM.
+// ---- S4: Bayes correction of every unique z of a Q-node ----------------------------------------
+// One CTA = one Q-node x 1024 cells (4 consecutive cells of one row per thread).  The thread
+// predicts bbar_a for its 4 cells once (linear form of k_hist) and writes every child
+// b'_z = O(y,z) bbar_a(y) / P(z|b,a) (Eq. 3) with float4 stores; w_z[s] = O[s][z] / P(z) is
+// formed in fp64 and staged in shared memory.
+struct CorrectArgs {
+    const float *beliefs;
+    long long bstride;
+    const int32_t *vmap;
+    const uint8_t *m8, *cell;
+    const double *O64;
+    const double *P;
+    const uint16_t *cnt, *umask;
+    const int32_t *off;
+    const uint64_t *vpath;
+    const int32_t *vroot;
+    int level;
+    float *child;
+    long long cstride;
+    uint64_t *cpath;
+    int32_t *cparent, *cz, *cf, *croot;
+    int H, W, G, ntiles, rows_cta;
+    float p_int, p_stay, p_lat;
+    long long qsel;   // >= 0: only this Q-node (belief_update)
+    const int32_t *sel_q, *sel_z, *sel_out;   // optional per-block-group selection (episodes)
+    const int32_t *skip = nullptr;             // device flag (best-first)
+    const long long *cbase_dev = nullptr;      // device child-index base (best-first pool)
+};
+
+// bbar_a for 4 consecutive cells (r, c0..c0+3): bbar = p_stay b + p_int h_a + p_lat (h_l1 + h_l2),
+// h_k = b(y - d_k) + occ(y + d_k) b(y); stay: bbar = b.  nbh holds rows r-1..r+1, cols c0-1..c0+4.
+template <int K>
+__device__ __forceinline__ void correct_predict(const CorrectArgs &a, int r, int c0, const float (&nbh)[3][6],
+                                                float (&bb)[4], int (&sg)[4]) {
+#pragma unroll
+    // cell info of the 4 cells in one 32-bit load each when the row is 4-aligned
+    const int x0 = r * a.W + c0;
+    uint32_t info4 = 0, m84 = 0;
+    const bool al = ((a.W & 3) == 0) && (c0 + 3 < a.W);
+    if (al) {
+        info4 = __ldg(reinterpret_cast<const unsigned int *>(a.cell + x0));
+        if (K != 4) m84 = __ldg(reinterpret_cast<const unsigned int *>(a.m8 + x0));
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int c = c0 + i;
+        bb[i] = 0.f;
+        sg[i] = 0;
+        if (c >= a.W) continue;
+        const int x = x0 + i;
+        const int info = al ? (int)((info4 >> (8 * i)) & 0xFFu) : (int)__ldg(a.cell + x);
+        sg[i] = info & 15;
+        if (info & 16) continue;                      // occupied: no mass
+        const float b0 = nbh[1][1 + i];
+        if (K == 4) {
+            bb[i] = b0;
+        } else {
+            const int m8 = al ? (int)((m84 >> (8 * i)) & 0xFFu) : (int)__ldg(a.m8 + x);
+            constexpr int L1 = lat1(K), L2 = lat2(K);
+            const float sa = nbh[1 - st_dr(K)][1 + i - st_dc(K)];
+            const float s1 = nbh[1 - st_dr(L1)][1 + i - st_dc(L1)];
+            const float s2 = nbh[1 - st_dr(L2)][1 + i - st_dc(L2)];
+            const float ha = ((m8 >> nbit(K)) & 1) ? sa + b0 : sa;
+            const float h1 = ((m8 >> nbit(L1)) & 1) ? s1 + b0 : s1;
+            const float h2 = ((m8 >> nbit(L2)) & 1) ? s2 + b0 : s2;
+            bb[i] = fmaf(a.p_lat, h1 + h2, fmaf(a.p_int, ha, a.p_stay * b0));
+        }
+    }
+}
+
+// Fused leaf level (SURVEY d.3 "K5-vs-fused"): the leaf parents' beliefs are never written.  Each
+// is rebuilt inside the leaf k_hist's staging from its own parent (the grandparent of the
+// leaves) with k_correct's arithmetic, b_v(y) = O[sig(y)][z_v] bbar_a(y) / P(z_v), so the
+// staged tiles -- and every result -- are bit-identical to the materialised path.
+struct FusedLeaf {
+    const int32_t *parent_q, *z;       // per leaf-parent V-node: parent Q-node (work index), z
+    const double *P;                   // the parent level's P(z|b,a) [nq][16]
+    const float *gbel;                 // grandparent beliefs
+    long long gstride;
+    const int32_t *gvmap;              // the parent level's work -> V-node map (or NULL)
+    CorrectArgs c;                     // geometry + motion model for correct_predict
+};
+
+template <uint32_t MASK, int K>
+__device__ void fused_stage(const FusedLeaf &f, const float *__restrict__ gb, const float (&w16)[16], float *tile,
+                            int TP, int row0, int TH, int t) {
+    const int W = f.c.W, G = (W + 3) >> 2;
+    const bool vec = (W & 3) == 0;
+    for (int i = t; i < TH * G; i += kPairThreads) {
+        const int tr = i / G, c0 = 4 * (i - tr * G);
+        const int r = row0 - 1 + tr;
+        float o[4] = {0.f, 0.f, 0.f, 0.f};
+        if (r >= 0 && r < f.c.H) {
+            float nbh[3][6];
+#pragma unroll
+            for (int dr = 0; dr < 3; ++dr) {
+                const int rr = r + dr - 1;
+                const bool rok = rr >= 0 && rr < f.c.H;
+                const float *row = gb + (long long)rr * W;
+                if (vec) {
+                    const float4 m4 = rok ? __ldg(reinterpret_cast<const float4 *>(row + c0)) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    nbh[dr][0] = (rok && c0 > 0) ? __ldg(row + c0 - 1) : 0.f;
+                    nbh[dr][1] = m4.x; nbh[dr][2] = m4.y; nbh[dr][3] = m4.z; nbh[dr][4] = m4.w;
+                    nbh[dr][5] = (rok && c0 + 4 < W) ? __ldg(row + c0 + 4) : 0.f;
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 6; ++j) {
+                        const int cc = c0 - 1 + j;
+                        nbh[dr][j] = (rok && cc >= 0 && cc < W) ? __ldg(row + cc) : 0.f;
+                    }
+                }
+            }
+            float bb[4];
+            int sg[4];
+            correct_predict<K>(f.c, r, c0, nbh, bb, sg);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) o[j] = w16[sg[j]] * bb[j];
+        }
+        if (vec) {
+            *reinterpret_cast<float4 *>(tile + tr * TP + 4 + c0) = make_float4(o[0], o[1], o[2], o[3]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (c0 + j < W) tile[tr * TP + 4 + c0 + j] = o[j];
+        }
+    }
+}
+
 struct HistArgs {
     const float *beliefs;
     long long bstride;
@@ -460,9 +593,11 @@ struct HistArgs {
     int *tickets;
     ReduceArgs red;
     const int32_t *skip = nullptr;  // device flag (best-first)
+    int fused_leaf = 0;             // 1: stage the leaf parents from their parents (FusedLeaf)
+    FusedLeaf fl;
 };
 
-template <uint32_t MASK, bool LEAF>
+template <uint32_t MASK, bool LEAF, bool FUSED = false>
 __global__ void __launch_bounds__(kPairThreads, 2) k_hist(HistArgs a) {
     constexpr int NA = mask_count(MASK);
     constexpr int NAP = (NA + 3) & ~3;
@@ -495,7 +630,34 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_hist(HistArgs a) {
         const float *__restrict__ b = a.beliefs + vv * a.bstride;
         float *tile = smem + pp * a.tstride;
         const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tile);
-        if (a.vec16) {
+        if (FUSED) {
+            if (vp) {
+                const int q = a.fl.parent_q[vv], z = a.fl.z[vv];
+                const int ww = q / NA, j = q - ww * NA;
+                const long long gw = a.fl.gvmap ? (long long)a.fl.gvmap[ww] : ww;
+                const float *__restrict__ gb = a.fl.gbel + gw * a.fl.gstride;
+                __shared__ float s_w16[2][16];
+                if (t < 16) s_w16[pp][t] = (float)(a.fl.c.O64[t * 16 + z] / a.fl.P[(long long)q * 16 + z]);
+                __syncthreads();
+                const float (&w16)[16] = s_w16[pp];
+                switch (action_of<MASK>(j)) {   // CTA-half uniform: compile-time tap geometry
+                    case 0: fused_stage<MASK, 0>(a.fl, gb, w16, tile, TP, row0, TH, t); break;
+                    case 1: fused_stage<MASK, 1>(a.fl, gb, w16, tile, TP, row0, TH, t); break;
+                    case 2: fused_stage<MASK, 2>(a.fl, gb, w16, tile, TP, row0, TH, t); break;
+                    case 3: fused_stage<MASK, 3>(a.fl, gb, w16, tile, TP, row0, TH, t); break;
+                    case 4: fused_stage<MASK, 4>(a.fl, gb, w16, tile, TP, row0, TH, t); break;
+                    case 5: fused_stage<MASK, 5>(a.fl, gb, w16, tile, TP, row0, TH, t); break;
+                    case 6: fused_stage<MASK, 6>(a.fl, gb, w16, tile, TP, row0, TH, t); break;
+                    case 7: fused_stage<MASK, 7>(a.fl, gb, w16, tile, TP, row0, TH, t); break;
+                    default: fused_stage<MASK, 8>(a.fl, gb, w16, tile, TP, row0, TH, t); break;
+                }
+            } else {
+                for (int i = t; i < TH * a.W; i += kPairThreads) {
+                    const int tr = i / a.W, c = i - tr * a.W;
+                    tile[tr * TP + 4 + c] = 0.f;
+                }
+            }
+        } else if (a.vec16) {
             const int W4 = a.W >> 2;
             for (int i = t; i < TH * W4; i += kPairThreads) {
                 const int tr = i / W4, c4 = i - tr * W4;
@@ -754,76 +916,6 @@ __global__ void __launch_bounds__(1024) k_scan(const int32_t *__restrict__ U, in
     if (t == 0) *total = carry_s;
 }
 
-// ---- S4: Bayes correction of every unique z of a Q-node ----------------------------------------
-// One CTA = one Q-node x 1024 cells (4 consecutive cells of one row per thread).  The thread
-// predicts bbar_a for its 4 cells once (linear form of k_hist) and writes every child
-// b'_z = O(y,z) bbar_a(y) / P(z|b,a) (Eq. 3) with float4 stores; w_z[s] = O[s][z] / P(z) is
-// formed in fp64 and staged in shared memory.
-struct CorrectArgs {
-    const float *beliefs;
-    long long bstride;
-    const int32_t *vmap;
-    const uint8_t *m8, *cell;
-    const double *O64;
-    const double *P;
-    const uint16_t *cnt, *umask;
-    const int32_t *off;
-    const uint64_t *vpath;
-    const int32_t *vroot;
-    int level;
-    float *child;
-    long long cstride;
-    uint64_t *cpath;
-    int32_t *cparent, *cz, *cf, *croot;
-    int H, W, G, ntiles, rows_cta;
-    float p_int, p_stay, p_lat;
-    long long qsel;   // >= 0: only this Q-node (belief_update)
-    const int32_t *sel_q, *sel_z, *sel_out;   // optional per-block-group selection (episodes)
-    const int32_t *skip = nullptr;             // device flag (best-first)
-    const long long *cbase_dev = nullptr;      // device child-index base (best-first pool)
-};
-
-// bbar_a for 4 consecutive cells (r, c0..c0+3): bbar = p_stay b + p_int h_a + p_lat (h_l1 + h_l2),
-// h_k = b(y - d_k) + occ(y + d_k) b(y); stay: bbar = b.  nbh holds rows r-1..r+1, cols c0-1..c0+4.
-template <int K>
-__device__ __forceinline__ void correct_predict(const CorrectArgs &a, int r, int c0, const float (&nbh)[3][6],
-                                                float (&bb)[4], int (&sg)[4]) {
-#pragma unroll
-    // cell info of the 4 cells in one 32-bit load each when the row is 4-aligned
-    const int x0 = r * a.W + c0;
-    uint32_t info4 = 0, m84 = 0;
-    const bool al = ((a.W & 3) == 0) && (c0 + 3 < a.W);
-    if (al) {
-        info4 = __ldg(reinterpret_cast<const unsigned int *>(a.cell + x0));
-        if (K != 4) m84 = __ldg(reinterpret_cast<const unsigned int *>(a.m8 + x0));
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int c = c0 + i;
-        bb[i] = 0.f;
-        sg[i] = 0;
-        if (c >= a.W) continue;
-        const int x = x0 + i;
-        const int info = al ? (int)((info4 >> (8 * i)) & 0xFFu) : (int)__ldg(a.cell + x);
-        sg[i] = info & 15;
-        if (info & 16) continue;                      // occupied: no mass
-        const float b0 = nbh[1][1 + i];
-        if (K == 4) {
-            bb[i] = b0;
-        } else {
-            const int m8 = al ? (int)((m84 >> (8 * i)) & 0xFFu) : (int)__ldg(a.m8 + x);
-            constexpr int L1 = lat1(K), L2 = lat2(K);
-            const float sa = nbh[1 - st_dr(K)][1 + i - st_dc(K)];
-            const float s1 = nbh[1 - st_dr(L1)][1 + i - st_dc(L1)];
-            const float s2 = nbh[1 - st_dr(L2)][1 + i - st_dc(L2)];
-            const float ha = ((m8 >> nbit(K)) & 1) ? sa + b0 : sa;
-            const float h1 = ((m8 >> nbit(L1)) & 1) ? s1 + b0 : s1;
-            const float h2 = ((m8 >> nbit(L2)) & 1) ? s2 + b0 : s2;
-            bb[i] = fmaf(a.p_lat, h1 + h2, fmaf(a.p_int, ha, a.p_stay * b0));
-        }
-    }
-}
-
 template <uint32_t MASK>
 __global__ void __launch_bounds__(256) k_correct(CorrectArgs a) {
     constexpr int NA = mask_count(MASK);
@@ -919,6 +1011,62 @@ __global__ void __launch_bounds__(256) k_correct(CorrectArgs a) {
     }
 }
 
+// Fused leaf level: the leaf parents' metadata (what k_correct writes from its tile-0 blocks) and
+// their beliefs at the goal-term cells, with k_correct's arithmetic; no belief is written.
+template <uint32_t MASK>
+__global__ void __launch_bounds__(256) k_child_meta(CorrectArgs a, long long nq, const int32_t *__restrict__ fcells,
+                                                   int nf, float *__restrict__ goalv) {
+    constexpr int NA = mask_count(MASK);
+    const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (idx >= nq * 16) return;
+    const long long q = idx >> 4;
+    const int u = (int)(idx & 15);
+    const unsigned um = a.umask[q];
+    if (u >= __popc(um)) return;
+    unsigned rem = um;
+    for (int i = 0; i < u; ++i) rem &= rem - 1;
+    const int z = __ffs(rem) - 1;
+    const long long w = q / NA;
+    const int j = (int)(q % NA);
+    const int k = action_of<MASK>(j);
+    const long long v = a.vmap ? (long long)a.vmap[w] : w;
+    const long long c = a.off[q] + u;
+    a.cpath[c] = a.vpath[v] | ((uint64_t)(k + 1) << (8 * a.level)) | ((uint64_t)z << (8 * a.level + 4));
+    a.cparent[c] = (int32_t)q;
+    a.cz[c] = z;
+    a.cf[c] = a.cnt[q * 16 + z];
+    a.croot[c] = a.vroot[v];
+    const float *__restrict__ b = a.beliefs + v * a.bstride;
+    for (int f = 0; f < nf; ++f) {
+        const int x = fcells[f], r = x / a.W, cx = x % a.W, c0 = cx & ~3;
+        float nbh[3][6];
+        for (int dr = 0; dr < 3; ++dr) {
+            const int rr = r + dr - 1;
+            const bool rok = rr >= 0 && rr < a.H;
+            for (int jj = 0; jj < 6; ++jj) {
+                const int cc = c0 - 1 + jj;
+                nbh[dr][jj] = (rok && cc >= 0 && cc < a.W) ? __ldg(b + (long long)rr * a.W + cc) : 0.f;
+            }
+        }
+        float bb[4];
+        int sg[4];
+        switch (k) {
+            case 0: correct_predict<0>(a, r, c0, nbh, bb, sg); break;
+            case 1: correct_predict<1>(a, r, c0, nbh, bb, sg); break;
+            case 2: correct_predict<2>(a, r, c0, nbh, bb, sg); break;
+            case 3: correct_predict<3>(a, r, c0, nbh, bb, sg); break;
+            case 4: correct_predict<4>(a, r, c0, nbh, bb, sg); break;
+            case 5: correct_predict<5>(a, r, c0, nbh, bb, sg); break;
+            case 6: correct_predict<6>(a, r, c0, nbh, bb, sg); break;
+            case 7: correct_predict<7>(a, r, c0, nbh, bb, sg); break;
+            default: correct_predict<8>(a, r, c0, nbh, bb, sg); break;
+        }
+        const int i = cx - c0;
+        const float ws = (float)(a.O64[sg[i] * 16 + z] / a.P[q * 16 + z]);
+        goalv[c * nf + f] = ws * bb[i];
+    }
+}
+
 // ---- S6 backup ---------------------------------------------------------------------------------
 template <int NA>
 __global__ void k_vmax(const double *__restrict__ Q, double *__restrict__ V, long long nwork, const int32_t *vmap) {
@@ -984,10 +1132,12 @@ template <uint32_t MASK, bool LEAF>
 static qvts_status launch_hist(Model &m, const BandSet &bs, const float *beliefs, long long bstride,
                                const int32_t *vmap, long long nwork, int pstride, cudaStream_t st, int *nb_eff,
                                const ReduceArgs *red = nullptr, bool *fused_out = nullptr,
-                               const int32_t *skip = nullptr) {
+                               const int32_t *skip = nullptr, const FusedLeaf *fl = nullptr) {
     constexpr int NOUT = 16 * hist_cb<MASK, LEAF>() + 8;
     HistArgs a;
     a.skip = skip;
+    a.fused_leaf = fl ? 1 : 0;
+    if (fl) a.fl = *fl;
     a.beliefs = beliefs; a.bstride = bstride; a.vmap = vmap; a.nwork = nwork;
     a.bands = bs.bands.as<BandInfo>(); a.nb = bs.nb;
     a.entries = bs.entries.as<uint32_t>();
@@ -1026,7 +1176,8 @@ static qvts_status launch_hist(Model &m, const BandSet &bs, const float *beliefs
     if (fused_out) *fused_out = a.fused != 0;
     const size_t smem = (size_t)std::max<size_t>((size_t)region * sizeof(float),
                                                  a.fused ? sizeof(double) * reduce_smem_doubles<MASK, LEAF>(pstride) : 0);
-    QVTS_CUDA(cudaFuncSetAttribute(k_hist<MASK, LEAF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    auto kfn = (LEAF && fl) ? k_hist<MASK, LEAF, LEAF> : k_hist<MASK, LEAF, false>;
+    QVTS_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const long long nblocks = ((nwork + 1) / 2) * bs.nb;
     if (nblocks > 0x7FFFFFFFLL) { set_error("too many hist blocks"); return QVTS_ERR_INVALID_ARG; }
     cudaLaunchConfig_t cfg = {};
@@ -1041,7 +1192,7 @@ static qvts_status launch_hist(Model &m, const BandSet &bs, const float *beliefs
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    QVTS_PROF(LEAF ? 0 : 1, QVTS_CUDA(cudaLaunchKernelEx(&cfg, k_hist<MASK, LEAF>, a)));
+    QVTS_PROF(LEAF ? 0 : 1, QVTS_CUDA(cudaLaunchKernelEx(&cfg, kfn, a)));
     (LEAF ? m.pstat.leaf_cells : m.pstat.hist_cells) += nwork * m.n_free;
     *nb_eff = a.cluster ? 1 : bs.nb;
     return QVTS_OK;
@@ -1086,6 +1237,12 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
     QVTS_CUDA(cudaMemsetAsync(m.counters.p, 0, sizeof(unsigned long long) * 4, st));
     QVTS_TRY(m.total.ensure(sizeof(long long)));
     nv_out[0] = roots.n;
+    // fused leaf level (FusedLeaf): measured slower than materialising the leaf parents (DESIGN
+    // §7: the in-kernel rebuild costs more than k_correct's HBM writes), so off unless
+    // QVTS_FUSED_LEAF=1; never with a trace or the ancestral sampler (they need the beliefs)
+    const char *ev_fused = std::getenv("QVTS_FUSED_LEAF");
+    const int env_fused = ev_fused ? std::atoi(ev_fused) : 0;
+    const bool fuse = env_fused && D >= 2 && !trace && cfg.sampler == QVTS_SAMPLER_MARGINAL;
 
     for (int d = 0; d < D; ++d) {
         const bool leaf = (d == D - 1);
@@ -1157,8 +1314,23 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
                 r.xs = m.xs.as<int32_t>();
             }
             bool fused = false;
+            FusedLeaf fl;
+            if (leaf && fuse) {
+                const int dg = D - 2;                       // the leaf parents' parents
+                fl.parent_q = vl.parent_q.as<int32_t>(); fl.z = vl.z.as<int32_t>();
+                fl.P = m.ql[dg].P.as<double>();
+                fl.gbel = dg == 0 ? roots.beliefs : m.vl[dg].belief.as<float>();
+                fl.gstride = dg == 0 ? roots.stride : m.HWp;
+                fl.gvmap = m.ql[dg].vmap_ptr;
+                std::memset(&fl.c, 0, sizeof(fl.c));
+                fl.c.m8 = m.d_m8.as<uint8_t>(); fl.c.cell = m.d_cell.as<uint8_t>(); fl.c.O64 = m.d_O64.as<double>();
+                fl.c.H = m.H; fl.c.W = m.W; fl.c.G = (m.W + 3) / 4;
+                fl.c.p_int = (float)m.p_int; fl.c.p_stay = (float)m.p_stay; fl.c.p_lat = (float)m.p_lat;
+                r.goalv = m.fl_goalv.as<float>(); r.nf = m.nfcells; r.gc_fidx = m.d_gc_fidx.as<int32_t>();
+            }
             const ReduceArgs *rf = r.xs ? nullptr : &r;   // the fused reduce has no x draws
-            if (leaf) QVTS_TRY((launch_hist<MASK, true>(m, bs, bel, bstride, vmap, nwork, pstride, st, &nb_eff, rf, &fused)));
+            if (leaf) QVTS_TRY((launch_hist<MASK, true>(m, bs, bel, bstride, vmap, nwork, pstride, st, &nb_eff, rf, &fused,
+                                                        nullptr, fuse ? &fl : nullptr)));
             else QVTS_TRY((launch_hist<MASK, false>(m, bs, bel, bstride, vmap, nwork, pstride, st, &nb_eff, rf, &fused)));
             r.nb = nb_eff;
             if (!fused) {
@@ -1186,7 +1358,9 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
         QVTS_TRY(vc.f.ensure(sizeof(int32_t) * tn));
         QVTS_TRY(vc.root.ensure(sizeof(int32_t) * tn));
         QVTS_TRY(vc.V.ensure(sizeof(double) * tn));
-        QVTS_TRY(vc.belief.ensure(sizeof(float) * (size_t)tn * m.HWp));
+        const bool meta_only = fuse && d + 1 == D - 1;   // leaf parents: metadata + goal-term cells only
+        if (meta_only) QVTS_TRY(m.fl_goalv.ensure(sizeof(float) * (size_t)tn * std::max(1, m.nfcells)));
+        else QVTS_TRY(vc.belief.ensure(sizeof(float) * (size_t)tn * m.HWp));
         if (nq > 0) {
             CorrectArgs c;
             c.beliefs = bel; c.bstride = bstride; c.vmap = vmap;
@@ -1204,9 +1378,14 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
             c.sel_q = c.sel_z = c.sel_out = nullptr;
             const long long nblocks = nq * c.ntiles;
             if (nblocks > 0x7FFFFFFFLL) { set_error("too many correct blocks"); return QVTS_ERR_INVALID_ARG; }
-            QVTS_PROF(5, k_correct<MASK><<<(unsigned)nblocks, 256, 0, st>>>(c));
+            if (meta_only) {
+                QVTS_PROF(5, k_child_meta<MASK><<<nblk(nq * 16, 256), 256, 0, st>>>(c, nq, m.d_fcells.as<int32_t>(),
+                                                                                 m.nfcells, m.fl_goalv.as<float>()));
+            } else {
+                QVTS_PROF(5, k_correct<MASK><<<(unsigned)nblocks, 256, 0, st>>>(c));
+                m.pstat.correct_cells_written += total * (long long)m.HW;
+            }
             QVTS_CUDA(cudaGetLastError());
-            m.pstat.correct_cells_written += total * (long long)m.HW;
         }
     }
     // S6 backup, bottom-up

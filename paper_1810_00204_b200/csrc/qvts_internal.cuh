@@ -82,6 +82,8 @@ struct Model {
     // device tables
     DevBuf d_m8, d_sig, d_cell /* sig | occ<<4 */, d_ctab, d_R64, d_O64, d_O32, d_gc_cell, d_gc_act, d_gc_val, d_free;
     int ngc = 0;
+    DevBuf d_fcells, d_gc_fidx, fl_goalv;   // fused leaf level: goal-term cells, their values
+    int nfcells = 0;
     BandSet band_big, band_small;
     // value iteration
     bool have_q = false;

@@ -477,3 +477,36 @@ def test_plan_point_mass_root_and_max_n(Q):
     b[int(np.flatnonzero(gm.occupancy == 0)[0])] = 1.0
     run_parity(Q, gm, W.A8, 3, 8, b)
     run_parity(Q, gm, W.A8, 1, 4096, W.random_belief(gm, 4))
+
+
+@pytest.mark.parametrize("name,depth,n", [("C1", 2, 4), ("ragged", 3, 8), ("paper", 3, 16), ("C3", 3, 8)])
+def test_fused_leaf_level_is_bit_identical(Q, name, depth, n, monkeypatch):
+    """SURVEY d.3 "K5-vs-fused": rebuilding the leaf parents inside the leaf kernel (never writing
+    them) gives the same root Q bits, counts and action as materialising them with k_correct;
+    and the root Q matches the oracle."""
+    gm = W.CONFIGS["C3"]["map"]() if name == "C3" else MAPS[name][0]()
+    mask = W.A8 if name == "C3" else MAPS[name][1]
+    g, o, Qo, _, _ = pair(Q, gm, mask)
+    b32 = np.asarray(W.random_belief(gm, 7), np.float32)
+    out = {}
+    for fused in ("1", "0"):
+        monkeypatch.setenv("QVTS_FUSED_LEAF", fused)
+        r = g.plan_step(dev(b32), depth, n, seed=5, step=2)
+        out[fused] = (np.array(r.q_root[:g.n_actions]), list(r.n_vnodes[:depth + 1]), r.action)
+    assert np.array_equal(out["1"][0], out["0"][0]) and out["1"][1] == out["0"][1] and out["1"][2] == out["0"][2]
+    ro = o.plan(Qo, b32.astype(np.float64), depth, n, seed=5, step=2)
+    assert np.max(np.abs(out["1"][0] - ro.qroot)) <= PT.TOL * 10
+
+
+def test_fused_leaf_episodes_identical(Q, monkeypatch):
+    gm, mask = MAPS["paper"][0](), MAPS["paper"][1]
+    g = Q.Model(gm, action_mask=mask)
+    g.value_iteration()
+    recs = {}
+    for fused in ("1", "0"):
+        monkeypatch.setenv("QVTS_FUSED_LEAF", fused)
+        rec, _ = g.run_episodes(6, max_steps=30, planner=Q.QVTS_PLANNER_QVTS, depth=3, n_samples=8, seed=3)
+        recs[fused] = rec
+    for k in recs["1"]:
+        assert np.array_equal(recs["1"][k], recs["0"][k]), k
+    g.close()
