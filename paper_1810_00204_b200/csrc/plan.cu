@@ -1078,26 +1078,29 @@ __global__ void k_vmax(const double *__restrict__ Q, double *__restrict__ V, lon
     V[vmap ? vmap[w] : w] = best + 0.0;   // +0.0 canonicalises -0 for the exact zero-padded sum
 }
 
+// one warp per parent V-node: lane j < NA backs up Q-node j over its children (ascending z, the
+// oracle's order), then V = max over the lanes (exact in any order)
 template <int NA>
-__global__ void k_backup(long long nwork, const int32_t *vmap, const double *__restrict__ R,
-                         const uint16_t *__restrict__ umask, const int32_t *__restrict__ off,
-                         const double *__restrict__ Vc, const int32_t *__restrict__ fc, int n, double gamma,
-                         double *__restrict__ Q, double *__restrict__ V) {
-    const long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(256) k_backup(long long nwork, const int32_t *vmap, const double *__restrict__ R,
+                                                const uint16_t *__restrict__ umask, const int32_t *__restrict__ off,
+                                                const double *__restrict__ Vc, const int32_t *__restrict__ fc, int n,
+                                                double gamma, double *__restrict__ Q, double *__restrict__ V) {
+    const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (w >= nwork) return;
-    double best = -INFINITY;
-#pragma unroll
-    for (int j = 0; j < NA; ++j) {
-        const long long q = w * NA + j;
+    double qv = -INFINITY;
+    if (lane < NA) {
+        const long long q = w * NA + lane;
         const int U = __popc((unsigned)umask[q]);
         const long long c0 = off[q];
         double acc = 0.0;
         for (int u = 0; u < U; ++u) acc += ((double)fc[c0 + u] / (double)n) * Vc[c0 + u];
-        const double qv = R[q] + gamma * acc;   // Alg. 6 with gamma (R13)
+        qv = R[q] + gamma * acc;                   // Alg. 6 with gamma (R13)
         Q[q] = qv;
-        best = fmax(best, qv);                  // Alg. 7
     }
-    V[vmap ? vmap[w] : w] = best + 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) qv = fmax(qv, __shfl_xor_sync(0xffffffffu, qv, o));   // Alg. 7
+    if (lane == 0) V[vmap ? vmap[w] : w] = qv + 0.0;
 }
 
 __global__ void k_init_roots(long long n, uint64_t *path, int32_t *root) {
@@ -1399,7 +1402,7 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
                 QVTS_PROF(6, k_vmax<NA><<<nblk(ql.nwork, 256), 256, 0, st>>>(ql.Q.as<double>(), vl.V.as<double>(), ql.nwork, vmap));
             } else {
                 VLevel &vc = m.vl[d + 1];
-                QVTS_PROF(6, k_backup<NA><<<nblk(ql.nwork, 256), 256, 0, st>>>(ql.nwork, vmap, ql.R.as<double>(),
+                QVTS_PROF(6, k_backup<NA><<<nblk(ql.nwork * 32, 256), 256, 0, st>>>(ql.nwork, vmap, ql.R.as<double>(),
                                                                   ql.umask.as<uint16_t>(), ql.off.as<int32_t>(),
                                                                   vc.V.as<double>(), vc.f.as<int32_t>(), n, m.gamma,
                                                                   ql.Q.as<double>(), vl.V.as<double>()));
