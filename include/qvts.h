@@ -132,6 +132,16 @@ QVTS_API qvts_status qvts_get_pbvi(const qvts_model *model, double *points_host,
 QVTS_API qvts_status qvts_belief_update(qvts_model *model, const float *b_dev, int32_t action, int32_t z,
                                float *out_dev, double *p_obs_out, void *stream);
 
+/* Batched Eq. 3 (SURVEY d.3 K9 at HBM scale): out_g = Phi(b_g, actions[g], zs[g]) for g < n.
+ * b_dev: device fp32 [n][b_stride] (b_stride >= H*W floats), out_dev: device fp32 [n][out_stride]
+ * (may not alias b_dev); actions (stencil ids) and zs: host int32 [n]; p_obs_out: host fp64 [n]
+ * or NULL.  Two passes over each belief: the selected action's class sums of bbar (then P(z)),
+ * and the correction (k_correct).  QVTS_ERR_ZERO_LIKELIHOOD if any P(z_g|b_g,a_g) <= 1e-30 (those
+ * outputs unspecified, the rest valid).  Synchronises `stream`. */
+QVTS_API qvts_status qvts_belief_update_batch(qvts_model *model, const float *b_dev, int64_t b_stride, int32_t n,
+                                              const int32_t *actions, const int32_t *zs, float *out_dev,
+                                              int64_t out_stride, double *p_obs_out, void *stream);
+
 /* ---- (4) plan step: level-batched QV-tree expansion (Alg. 1-7) --------
  * Expands every V-node of a level at once, for depth levels 0..depth-1: predict through T,
  * marginal P(z|b,a) and R(b,a), n forward-sampled observations per Q-node from Philox4x32-10

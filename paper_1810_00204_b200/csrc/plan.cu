@@ -1821,6 +1821,169 @@ extern "C" qvts_status qvts_belief_update(qvts_model *m, const float *b_dev, int
     return QVTS_OK;
 }
 
+// Batched Eq. 3, pass 1: M_g[s] = sum over class-s cells of bbar_{a_g}(y) for the selected action
+// only (correct_predict's 4-cell groups, k_correct's tiling), one fp64 partial per (belief, tile,
+// class); pass 2 (k_bu_p) sums the tiles in order and forms P(z|b,a) = sum_s O[s][z] M[s].
+template <uint32_t MASK>
+__global__ void __launch_bounds__(256) k_bu_marg(CorrectArgs a, double *__restrict__ part) {
+    constexpr int NA = mask_count(MASK);
+    const long long grp = blockIdx.x / a.ntiles;
+    const int tile = blockIdx.x % a.ntiles;
+    const long long q = a.sel_q[grp];
+    const int j = (int)(q % NA), k = action_of<MASK>(j);
+    const float *__restrict__ b = a.beliefs + (q / NA) * a.bstride;
+    const int W = a.W;
+    const bool vec = ((W & 3) == 0) && ((a.bstride & 3) == 0);
+    float acc[16];
+#pragma unroll
+    for (int s2 = 0; s2 < 16; ++s2) acc[s2] = 0.f;
+    const int r_end = min(a.H, (tile + 1) * a.rows_cta);
+    for (int idx = threadIdx.x; idx < a.rows_cta * a.G; idx += 256) {
+        const int r = tile * a.rows_cta + idx / a.G, c0 = 4 * (idx % a.G);
+        if (r >= r_end) break;
+        float nbh[3][6];
+#pragma unroll
+        for (int dr = 0; dr < 3; ++dr) {
+            const int rr = r + dr - 1;
+            const bool rok = rr >= 0 && rr < a.H;
+            const float *row = b + (long long)rr * W;
+            if (vec) {
+                const float4 m4 = rok ? __ldg(reinterpret_cast<const float4 *>(row + c0)) : make_float4(0.f, 0.f, 0.f, 0.f);
+                nbh[dr][0] = (rok && c0 > 0) ? __ldg(row + c0 - 1) : 0.f;
+                nbh[dr][1] = m4.x; nbh[dr][2] = m4.y; nbh[dr][3] = m4.z; nbh[dr][4] = m4.w;
+                nbh[dr][5] = (rok && c0 + 4 < W) ? __ldg(row + c0 + 4) : 0.f;
+            } else {
+#pragma unroll
+                for (int i = 0; i < 6; ++i) {
+                    const int cc = c0 - 1 + i;
+                    nbh[dr][i] = (rok && cc >= 0 && cc < W) ? __ldg(row + cc) : 0.f;
+                }
+            }
+        }
+        float bb[4];
+        int sg[4];
+        switch (k) {
+            case 0: correct_predict<0>(a, r, c0, nbh, bb, sg); break;
+            case 1: correct_predict<1>(a, r, c0, nbh, bb, sg); break;
+            case 2: correct_predict<2>(a, r, c0, nbh, bb, sg); break;
+            case 3: correct_predict<3>(a, r, c0, nbh, bb, sg); break;
+            case 4: correct_predict<4>(a, r, c0, nbh, bb, sg); break;
+            case 5: correct_predict<5>(a, r, c0, nbh, bb, sg); break;
+            case 6: correct_predict<6>(a, r, c0, nbh, bb, sg); break;
+            case 7: correct_predict<7>(a, r, c0, nbh, bb, sg); break;
+            default: correct_predict<8>(a, r, c0, nbh, bb, sg); break;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int s2 = 0; s2 < 16; ++s2) acc[s2] += (sg[i] == s2) ? bb[i] : 0.f;
+    }
+    // fixed-order reduction: butterfly within each warp, then the 8 warp sums in warp order (fp64)
+    __shared__ double wsum[8][16];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int s2 = 0; s2 < 16; ++s2) {
+        float v = acc[s2];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) wsum[warp][s2] = (double)v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 16) {
+        double sm = 0.0;
+#pragma unroll
+        for (int w2 = 0; w2 < 8; ++w2) sm += wsum[w2][threadIdx.x];
+        part[(grp * a.ntiles + tile) * 16 + threadIdx.x] = sm;
+    }
+}
+
+__global__ void k_bu_p(const double *__restrict__ part, int ntiles, const int32_t *__restrict__ sel_q, int n,
+                       const double *__restrict__ O64, double *__restrict__ P) {
+    const int g = blockIdx.x;
+    const int z = threadIdx.x;                       // 16 threads: P(z) for every z
+    __shared__ double M[16];
+    double m = 0.0;
+    for (int t2 = 0; t2 < ntiles; ++t2) m += part[((long long)g * ntiles + t2) * 16 + z];
+    M[z] = m;
+    __syncthreads();
+    double pz = 0.0;
+    for (int s2 = 0; s2 < 16; ++s2) pz += O64[s2 * 16 + z] * M[s2];
+    P[(long long)sel_q[g] * 16 + z] = pz;
+}
+
+// P(z_g | b_g, a_g) of the selected (Q-node, z) pairs, for the zero-likelihood check
+__global__ void k_gather_p(const double *__restrict__ P, const int32_t *__restrict__ sel_q,
+                           const int32_t *__restrict__ sel_z, int n, double *__restrict__ out) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < n) out[g] = P[(long long)sel_q[g] * 16 + sel_z[g]];
+}
+
+extern "C" qvts_status qvts_belief_update_batch(qvts_model *m, const float *b_dev, int64_t b_stride, int32_t n,
+                                                const int32_t *actions, const int32_t *zs, float *out_dev,
+                                                int64_t out_stride, double *p_obs_out, void *stream) {
+    if (!m || (n > 0 && (!b_dev || !actions || !zs || !out_dev))) { set_error("NULL argument"); return QVTS_ERR_INVALID_ARG; }
+    if (n < 0 || b_stride < m->HW || out_stride < m->HW) { set_error("bad n or stride"); return QVTS_ERR_INVALID_ARG; }
+    if (n == 0) return QVTS_OK;
+    QVTS_CUDA(cudaSetDevice(m->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const int NA = m->NA;
+    std::vector<int32_t> sel(3 * (size_t)n);
+    for (int g = 0; g < n; ++g) {
+        int j = -1;
+        for (int i = 0; i < NA; ++i) if (m->action_id[i] == actions[g]) j = i;
+        if (j < 0 || zs[g] < 0 || zs[g] > 15) { set_error("action not in the action set or z out of range"); return QVTS_ERR_INVALID_ARG; }
+        sel[g] = g * NA + j;
+        sel[n + g] = zs[g];
+        sel[2 * n + g] = g;
+    }
+    QVTS_TRY(m->bu_key.ensure(sizeof(uint32_t) * 2 * (size_t)n));
+    QVTS_TRY(m->bu_off.ensure(sizeof(int32_t) * 3 * (size_t)n));
+    QVTS_TRY(m->bu_P.ensure(sizeof(double) * (size_t)n));
+    QVTS_CUDA(cudaMemsetAsync(m->bu_key.p, 0, sizeof(uint32_t) * 2 * (size_t)n, st));
+    QVTS_CUDA(cudaMemcpyAsync(m->bu_off.p, sel.data(), sizeof(int32_t) * sel.size(), cudaMemcpyHostToDevice, st));
+    const int32_t *d_sel = m->bu_off.as<int32_t>();
+    CorrectArgs c;
+    std::memset(&c, 0, sizeof(c));
+    c.beliefs = b_dev; c.bstride = b_stride; c.m8 = m->d_m8.as<uint8_t>(); c.cell = m->d_cell.as<uint8_t>();
+    c.O64 = m->d_O64.as<double>(); c.H = m->H; c.W = m->W; c.G = (m->W + 3) / 4;
+    // CTAs of ~BU_GROUPS groups of 4 cells (the plan's 1024 leave the one-child case latency-bound)
+    static const int bu_groups = [] {
+        const char *ev = std::getenv("QVTS_BU_GROUPS");
+        return ev ? std::max(256, std::atoi(ev)) : 4096;
+    }();
+    c.rows_cta = std::min(m->H, std::max(1, bu_groups / std::max(1, c.G)));
+    c.ntiles = (m->H + c.rows_cta - 1) / c.rows_cta;
+    c.p_int = (float)m->p_int; c.p_stay = (float)m->p_stay; c.p_lat = (float)m->p_lat; c.qsel = -1;
+    c.sel_q = d_sel; c.sel_z = d_sel + n; c.sel_out = d_sel + 2 * n;
+    c.child = out_dev; c.cstride = out_stride;
+    QVTS_TRY(m->part.ensure(sizeof(double) * (size_t)n * c.ntiles * 16));
+    QVTS_TRY(m->bu_R.ensure(sizeof(double) * (size_t)n * NA * 16));     // P in the Q-node layout
+    c.P = m->bu_R.as<double>();
+    const long long nblocks = (long long)n * c.ntiles;
+    if (nblocks > 0x7FFFFFFFLL) { set_error("batch too large"); return QVTS_ERR_INVALID_ARG; }
+#define QVTS_BUB(MASK)                                                                                          \
+    {                                                                                                           \
+        k_bu_marg<MASK><<<(unsigned)nblocks, 256, 0, st>>>(c, m->part.as<double>());                            \
+        k_bu_p<<<n, 16, 0, st>>>(m->part.as<double>(), c.ntiles, d_sel, n, m->d_O64.as<double>(),               \
+                                 m->bu_R.as<double>());                                                          \
+        k_correct<MASK><<<(unsigned)nblocks, 256, 0, st>>>(c);                                                  \
+    }
+    QVTS_DISPATCH_MASK(m->mask, QVTS_BUB);
+#undef QVTS_BUB
+    k_gather_p<<<nblk(n, 256), 256, 0, st>>>(m->bu_R.as<double>(), d_sel, d_sel + n, n, m->bu_P.as<double>());
+    QVTS_CUDA(cudaGetLastError());
+    std::vector<double> p(n);
+    QVTS_CUDA(cudaMemcpyAsync(p.data(), m->bu_P.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    QVTS_CUDA(cudaStreamSynchronize(st));
+    bool zero = false;
+    for (int g = 0; g < n; ++g) {
+        if (p_obs_out) p_obs_out[g] = p[g];
+        if (!(p[g] > 1e-30)) zero = true;
+    }
+    if (zero) { set_error("zero-likelihood observation in the batch"); return QVTS_ERR_ZERO_LIKELIHOOD; }
+    return QVTS_OK;
+}
+
 // ---- trace accessors ----------------------------------------------------------------------------
 static qvts_status check_level(const qvts_model *m, int level, bool qlevel) {
     if (!m) { set_error("model is NULL"); return QVTS_ERR_INVALID_ARG; }

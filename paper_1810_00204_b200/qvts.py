@@ -24,7 +24,7 @@ EXPORTS = [
     "qvts_value_iteration", "qvts_get_q", "qvts_belief_update", "qvts_plan_step", "qvts_trace_qnodes",
     "qvts_trace_vnodes", "qvts_trace_leaf_values", "qvts_trace_belief", "qvts_run_episodes",
     "qvts_trace_counts", "qvts_set_profiling", "qvts_get_profile", "qvts_fib_iteration", "qvts_get_alpha",
-    "qvts_pbvi", "qvts_get_pbvi", "qvts_plan_best_first", "qvts_trace_best_first", "qvts_bf_advance",
+    "qvts_pbvi", "qvts_get_pbvi", "qvts_plan_best_first", "qvts_trace_best_first", "qvts_bf_advance", "qvts_belief_update_batch",
 ]
 QVTS_BF_BUDGET, QVTS_BF_GAP, QVTS_BF_TERMINAL, QVTS_BF_POOL, QVTS_BF_TIME = 0, 1, 2, 3, 4
 QVTS_LEAF_QMDP, QVTS_LEAF_FIB = 0, 1
@@ -125,6 +125,7 @@ def lib() -> C.CDLL:
         L.qvts_trace_best_first.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int32)] + [vp] * 10
         L.qvts_bf_advance.argtypes = [vp, C.c_int32, C.c_int32, C.POINTER(C.c_int32), vp]
         L.qvts_belief_update.argtypes = [vp, vp, C.c_int32, C.c_int32, vp, C.POINTER(C.c_double), vp]
+        L.qvts_belief_update_batch.argtypes = [vp, vp, C.c_int64, C.c_int32, vp, vp, vp, C.c_int64, vp, vp]
         L.qvts_plan_step.argtypes = [vp, vp, C.POINTER(qvts_plan_cfg), C.POINTER(qvts_comm),
                                      C.POINTER(qvts_plan_result), vp]
         L.qvts_trace_qnodes.argtypes = [vp, C.c_int32, vp, vp, vp, vp, vp, vp]
@@ -224,6 +225,18 @@ def qvts_get_alpha(h, n_actions, n_cells):
     a = np.zeros((n_actions, n_cells), np.float64)
     _check(lib().qvts_get_alpha(h, a.ctypes.data), "qvts_get_alpha")
     return a
+
+
+def qvts_belief_update_batch(h, b_dev, actions, zs, out_dev, stream=None):
+    """Batched Eq. 3: b_dev / out_dev are [n][>= H*W] fp32 device tensors; returns P(z|b,a) [n]."""
+    acts = np.ascontiguousarray(actions, dtype=np.int32)
+    z = np.ascontiguousarray(zs, dtype=np.int32)
+    n = len(acts)
+    p = np.zeros(max(1, n))
+    _check(lib().qvts_belief_update_batch(h, _ptr(b_dev), int(b_dev.stride(0)) if n else 0, n, acts.ctypes.data,
+                                          z.ctypes.data, _ptr(out_dev), int(out_dev.stride(0)) if n else 0,
+                                          p.ctypes.data, _stream(stream)), "qvts_belief_update_batch")
+    return p[:n]
 
 
 def qvts_pbvi(h, b0_dev=None, expansions=3, max_points=16, seed=1, sweeps=30, stream=None):
@@ -446,6 +459,9 @@ class Model:
 
     def tables(self):
         return qvts_model_tables(self.h, self.n_actions, self.n_cells)
+
+    def belief_update_batch(self, b_dev, actions, zs, out_dev):
+        return qvts_belief_update_batch(self.h, b_dev, actions, zs, out_dev)
 
     def belief_update(self, b_dev, action, z, out_dev):
         return qvts_belief_update(self.h, b_dev, action, z, out_dev)

@@ -510,3 +510,29 @@ def test_fused_leaf_episodes_identical(Q, monkeypatch):
     for k in recs["1"]:
         assert np.array_equal(recs["1"][k], recs["0"][k]), k
     g.close()
+
+
+@pytest.mark.parametrize("name", ["C1", "ragged", "paper"])
+def test_belief_update_batch(Q, name):
+    """Batched Eq. 3 against the oracle element by element, mixed actions and observations."""
+    gm, mask = MAPS[name][0](), MAPS[name][1]
+    g = Q.Model(gm, action_mask=mask)
+    o = O.Model.grid(gm, action_mask=mask)
+    rng = np.random.default_rng(3)
+    nb = 37
+    B = np.stack([W.random_belief(gm, 100 + i) for i in range(nb)]).astype(np.float32)
+    acts = rng.choice(g.action_ids, size=nb)
+    zs = np.zeros(nb, np.int32)
+    for i in range(nb):                     # a z with non-negligible mass
+        P = o.marginal(o.predict(B[i].astype(np.float64), g.action_ids.index(acts[i])))
+        zs[i] = int(np.argsort(P)[-1 - (i % 3)])
+    out = torch.empty((nb, gm.occupancy.size), dtype=torch.float32, device="cuda")
+    p = g.belief_update_batch(dev(B), acts, zs, out)
+    res = out.cpu().numpy()
+    for i in range(nb):
+        ob, op = o.belief_update(B[i].astype(np.float64), g.action_ids.index(acts[i]), int(zs[i]))
+        assert abs(p[i] - op) <= 1e-7
+        assert np.max(np.abs(res[i] - ob)) <= PT.TOL
+        assert np.max(np.abs(res[i] - ob)) <= 1e-5 * max(1e-3, float(np.max(ob)))
+        assert np.all(res[i][gm.occupancy == 1] == 0.0)
+    g.close()
