@@ -425,11 +425,8 @@ static BfGeom bf_geom(const Model &m) {
 template <int KJ>
 static void bf_dots_launch(Model &m, const BfGeom &g, BfDev *S, cudaStream_t st) {
     const size_t smem = (size_t)(g.XS + 1) * (16 * KJ * 8 + 48 * 4);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(k_bf_dots<3, KJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr_set = true;
-    }
+    // per call (the attribute is per device; the call is cheap and legal during graph capture)
+    cudaFuncSetAttribute(k_bf_dots<3, KJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     k_bf_dots<3, KJ><<<dim3(g.nsplit, g.nkb, 3), 256, smem, st>>>(m.bf_bel.as<float>(), m.HWp, S, m.bf_VT.as<double>(),
                                                                   m.HW, g.XS, g.nsplit, m.bf_part.as<double>());
 }
