@@ -566,6 +566,11 @@ extern "C" void qvts_model_destroy(qvts_model *m) {
     }
     for (auto &q : m->ql) { q.vmap.release(); q.R.release(); q.P.release(); q.cnt.release(); q.umask.release(); q.U.release(); q.off.release(); q.Q.release(); q.zdraw.release(); q.leafV.release(); }
     if (m->bf_gexec) cudaGraphExecDestroy(m->bf_gexec);
+    if (m->pg_exec) cudaGraphExecDestroy(m->pg_exec);
+    if (m->pg_stream) cudaStreamDestroy(m->pg_stream);
+    if (m->pg_join) cudaEventDestroy(m->pg_join);
+    m->lvl_cnt.release();
+    m->root_buf.release();
     if (m->bf_stream) cudaStreamDestroy(m->bf_stream);
     if (m->bf_join) cudaEventDestroy(m->bf_join);
     if (m->ev0) cudaEventDestroy(m->ev0);

@@ -82,6 +82,7 @@ struct ReduceArgs {
     int W;
     double acc;
     const int32_t *skip = nullptr;  // device flag: non-zero -> the launch does nothing (best-first)
+    const long long *nwork_dev = nullptr;   // device-side parent count (graph-captured plan step)
     // fused leaf level: the leaf parents' beliefs at the goal-term cells [v][nf] (k_child_meta)
     const float *goalv = nullptr;
     int nf = 0;
@@ -360,6 +361,7 @@ template <uint32_t MASK, bool LEAF>
 __global__ void __launch_bounds__(mask_count(MASK) * 32, reduce_min_blocks<MASK>()) k_reduce(ReduceArgs a) {
     extern __shared__ double rsm[];
     if (a.skip && *a.skip) return;
+    if (a.nwork_dev && (long long)blockIdx.x >= *a.nwork_dev) return;
     reduce_parent<MASK, LEAF>(a, blockIdx.x, rsm, mask_count(MASK) * 32);
 }
 
@@ -474,6 +476,7 @@ struct CorrectArgs {
     const int32_t *sel_q, *sel_z, *sel_out;   // optional per-block-group selection (episodes)
     const int32_t *skip = nullptr;             // device flag (best-first)
     const long long *cbase_dev = nullptr;      // device child-index base (best-first pool)
+    const long long *nwork_dev = nullptr;      // device-side parent count (graph-captured plan step)
 };
 
 // bbar_a for 4 consecutive cells (r, c0..c0+3): bbar = p_stay b + p_int h_a + p_lat (h_l1 + h_l2),
@@ -593,11 +596,12 @@ struct HistArgs {
     int *tickets;
     ReduceArgs red;
     const int32_t *skip = nullptr;  // device flag (best-first)
+    const long long *nwork_dev = nullptr;   // device-side parent count (graph-captured plan step)
     int fused_leaf = 0;             // 1: stage the leaf parents from their parents (FusedLeaf)
     FusedLeaf fl;
 };
 
-template <uint32_t MASK, bool LEAF, bool FUSED = false>
+template <uint32_t MASK, bool LEAF, bool FUSED = false, bool DEV = false>
 __global__ void __launch_bounds__(kPairThreads, 2) k_hist(HistArgs a) {
     constexpr int NA = mask_count(MASK);
     constexpr int NAP = (NA + 3) & ~3;
@@ -614,6 +618,9 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_hist(HistArgs a) {
     const int st = warp * 16 + (lane & 15);        // slot-thread 0..T-1
     const int band = blockIdx.x % a.nb;
     const long long pair = blockIdx.x / a.nb;
+    // DEV (graph-captured step): the parent count lives on the device and the grid is worst-case
+    const long long nwork = DEV ? *a.nwork_dev : a.nwork;
+    if (DEV && 2 * pair >= nwork) return;
     const BandInfo *bi = a.bands + band;
     const int row0 = bi->row0, nrows = bi->nrows, L = bi->L;
     const long long soff = bi->slot_off;
@@ -625,7 +632,7 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_hist(HistArgs a) {
 #pragma unroll
     for (int pp = 0; pp < 2; ++pp) {
         const long long wp = 2 * pair + pp;
-        const bool vp = wp < a.nwork;
+        const bool vp = wp < nwork;
         const long long vv = vp ? (a.vmap ? (long long)a.vmap[wp] : wp) : 0;
         const float *__restrict__ b = a.beliefs + vv * a.bstride;
         float *tile = smem + pp * a.tstride;
@@ -701,7 +708,7 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_hist(HistArgs a) {
             for (int o = t; o < 2 * NOUT0; o += kPairThreads) {
                 const int pp = o / NOUT0, oo = o % NOUT0;
                 const long long wp = 2 * pair + pp;
-                if (wp < a.nwork) a.part[(wp * a.nb + band) * (long long)a.pstride + oo] = 0.0;
+                if (wp < nwork) a.part[(wp * a.nb + band) * (long long)a.pstride + oo] = 0.0;
             }
             if (!a.cluster) return;
         }
@@ -850,14 +857,14 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_hist(HistArgs a) {
             const long long wp = 2 * pair + pp;
             double sm = 0.0;
             for (int rr = 0; rr < nr; ++rr) sm += cl.map_shared_rank(sums, rr)[o];
-            if (wp < a.nwork) a.part[wp * (long long)a.pstride + oo] = sm;
+            if (wp < nwork) a.part[wp * (long long)a.pstride + oo] = sm;
         }
         cl.sync();
     } else {
         for (int o = t; o < 2 * NOUT; o += kPairThreads) {
             const int pp = o / NOUT, oo = o % NOUT;
             const long long wp = 2 * pair + pp;
-            if (wp < a.nwork) a.part[(wp * a.nb + band) * (long long)a.pstride + oo] = sums[o];
+            if (wp < nwork) a.part[(wp * a.nb + band) * (long long)a.pstride + oo] = sums[o];
         }
         if (a.fused) {
             // the last band CTA of this parent pair runs the pair's reduce/sample (k_reduce's
@@ -872,7 +879,7 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_hist(HistArgs a) {
                 __threadfence();
                 double *rsm = reinterpret_cast<double *>(smem);
                 for (int pp = 0; pp < 2; ++pp)
-                    if (2 * pair + pp < a.nwork) reduce_parent<MASK, LEAF>(a.red, 2 * pair + pp, rsm, kPairThreads);
+                    if (2 * pair + pp < nwork) reduce_parent<MASK, LEAF>(a.red, 2 * pair + pp, rsm, kPairThreads);
             }
         }
     }
@@ -880,10 +887,12 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_hist(HistArgs a) {
 
 // ---- child offsets: single-CTA exclusive scan -------------------------------------------------
 __global__ void __launch_bounds__(1024) k_scan(const int32_t *__restrict__ U, int32_t *__restrict__ off, long long n,
-                                               long long *total, const int32_t *skip = nullptr) {
+                                               long long *total, const int32_t *skip = nullptr,
+                                               const long long *nwork_dev = nullptr, int na = 1) {
     __shared__ long long wsum[32];
     __shared__ long long carry_s;
     if (skip && *skip) return;
+    if (nwork_dev) n = *nwork_dev * na;                // Q-nodes of the level, from the device count
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     if (t == 0) carry_s = 0;
     __syncthreads();
@@ -921,6 +930,7 @@ __global__ void __launch_bounds__(256) k_correct(CorrectArgs a) {
     constexpr int NA = mask_count(MASK);
     if (a.skip && *a.skip) return;
     const long long grp = blockIdx.x / a.ntiles;
+    if (a.nwork_dev && !a.sel_q && grp >= *a.nwork_dev * NA) return;
     const long long q = a.sel_q ? (long long)a.sel_q[grp] : (a.qsel >= 0 ? a.qsel : grp);
     const int tile = blockIdx.x % a.ntiles;
     const long long w = q / NA;
@@ -1069,9 +1079,10 @@ __global__ void __launch_bounds__(256) k_child_meta(CorrectArgs a, long long nq,
 
 // ---- S6 backup ---------------------------------------------------------------------------------
 template <int NA>
-__global__ void k_vmax(const double *__restrict__ Q, double *__restrict__ V, long long nwork, const int32_t *vmap) {
+__global__ void k_vmax(const double *__restrict__ Q, double *__restrict__ V, long long nwork, const int32_t *vmap,
+                       const long long *nwork_dev = nullptr) {
     const long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (w >= nwork) return;
+    if (w >= nwork || (nwork_dev && w >= *nwork_dev)) return;
     double best = Q[w * NA];
 #pragma unroll
     for (int j = 1; j < NA; ++j) best = fmax(best, Q[w * NA + j]);
@@ -1084,10 +1095,11 @@ template <int NA>
 __global__ void __launch_bounds__(256) k_backup(long long nwork, const int32_t *vmap, const double *__restrict__ R,
                                                 const uint16_t *__restrict__ umask, const int32_t *__restrict__ off,
                                                 const double *__restrict__ Vc, const int32_t *__restrict__ fc, int n,
-                                                double gamma, double *__restrict__ Q, double *__restrict__ V) {
+                                                double gamma, double *__restrict__ Q, double *__restrict__ V,
+                                                const long long *nwork_dev = nullptr) {
     const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (w >= nwork) return;
+    if (w >= nwork || (nwork_dev && w >= *nwork_dev)) return;
     double qv = -INFINITY;
     if (lane < NA) {
         const long long q = w * NA + lane;
@@ -1135,10 +1147,12 @@ template <uint32_t MASK, bool LEAF>
 static qvts_status launch_hist(Model &m, const BandSet &bs, const float *beliefs, long long bstride,
                                const int32_t *vmap, long long nwork, int pstride, cudaStream_t st, int *nb_eff,
                                const ReduceArgs *red = nullptr, bool *fused_out = nullptr,
-                               const int32_t *skip = nullptr, const FusedLeaf *fl = nullptr) {
+                               const int32_t *skip = nullptr, const FusedLeaf *fl = nullptr,
+                               const long long *nwork_dev = nullptr) {
     constexpr int NOUT = 16 * hist_cb<MASK, LEAF>() + 8;
     HistArgs a;
     a.skip = skip;
+    a.nwork_dev = nwork_dev;
     a.fused_leaf = fl ? 1 : 0;
     if (fl) a.fl = *fl;
     a.beliefs = beliefs; a.bstride = bstride; a.vmap = vmap; a.nwork = nwork;
@@ -1158,7 +1172,7 @@ static qvts_status launch_hist(Model &m, const BandSet &bs, const float *beliefs
         const char *ev = std::getenv("QVTS_HIST_CLUSTER");
         return ev ? std::atoi(ev) : 0;
     }();
-    a.cluster = (use_cluster && bs.nb <= 8) ? 1 : 0;
+    a.cluster = (use_cluster && bs.nb <= 8 && !nwork_dev) ? 1 : 0;
     a.part = m.part.as<double>(); a.pstride = pstride;
     // fused reduce (the last band CTA of each pair runs reduce_parent): measured slower than a
     // separate k_reduce launch, so off unless QVTS_FUSED_REDUCE=1
@@ -1179,7 +1193,8 @@ static qvts_status launch_hist(Model &m, const BandSet &bs, const float *beliefs
     if (fused_out) *fused_out = a.fused != 0;
     const size_t smem = (size_t)std::max<size_t>((size_t)region * sizeof(float),
                                                  a.fused ? sizeof(double) * reduce_smem_doubles<MASK, LEAF>(pstride) : 0);
-    auto kfn = (LEAF && fl) ? k_hist<MASK, LEAF, LEAF> : k_hist<MASK, LEAF, false>;
+    auto kfn = (LEAF && fl) ? k_hist<MASK, LEAF, LEAF, false>
+                            : (nwork_dev ? k_hist<MASK, LEAF, false, true> : k_hist<MASK, LEAF, false, false>);
     QVTS_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const long long nblocks = ((nwork + 1) / 2) * bs.nb;
     if (nblocks > 0x7FFFFFFFLL) { set_error("too many hist blocks"); return QVTS_ERR_INVALID_ARG; }
@@ -1427,6 +1442,163 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
     m.last_shard_level = shard_level;
     m.last_n = n;
     m.last_trace = trace;
+    return QVTS_OK;
+}
+
+// ---- graph-captured plan step (small trees) ------------------------------------------------------
+// The same kernels as plan_levels_t, with every level's V-node count kept on the device
+// (m.lvl_cnt[d], written by k_scan) and grids sized for the worst case Vmax[d] (children per
+// Q-node <= min(n, 16)), so one plan step is a fixed launch sequence that a CUDA graph replays
+// with no host synchronisation between levels.  Used for single-root plan steps whose worst-case
+// tree fits kGraphBudget; results are bit-identical to plan_levels_t (same kernels, same order).
+constexpr double kGraphBudget = 2.0e9;    // bytes of worst-case materialised beliefs
+
+__global__ void k_set_count(long long *cnt, long long v) { cnt[0] = v; }
+
+static bool graph_eligible(const Model &m, const qvts_plan_cfg &cfg, long long *vmax) {
+    vmax[0] = 1;
+    double bytes = 0.0;
+    for (int d = 0; d < cfg.depth; ++d) {
+        vmax[d + 1] = vmax[d] * m.NA * std::min(cfg.n_samples, 16);
+        if (d + 1 < cfg.depth) bytes += (double)vmax[d + 1] * m.HWp * 4.0;
+        if (vmax[d + 1] > (1LL << 26)) return false;
+    }
+    return bytes <= kGraphBudget;
+}
+
+template <uint32_t MASK>
+static qvts_status plan_levels_dev_t(Model &m, const float *root, const qvts_plan_cfg &cfg, const long long *vmax,
+                                     cudaStream_t st) {
+    constexpr int NA = mask_count(MASK);
+    const int D = cfg.depth, n = cfg.n_samples;
+    long long *cnt = m.lvl_cnt.as<long long>();           // [D+1] V-node counts per level
+    VLevel &v0 = m.vl[0];
+    QVTS_PROF(7, k_init_roots<<<1, 256, 0, st>>>(1, v0.path.as<uint64_t>(), v0.root.as<int32_t>()));
+    QVTS_PROF(7, k_set_count<<<1, 1, 0, st>>>(cnt, 1));
+    QVTS_CUDA(cudaMemsetAsync(m.counters.p, 0, sizeof(unsigned long long) * 4, st));
+    for (int d = 0; d < D; ++d) {
+        const bool leaf = (d == D - 1);
+        VLevel &vl = m.vl[d];
+        QLevel &ql = m.ql[d];
+        ql.nwork = vmax[d];
+        ql.mapped = false;
+        ql.vmap_ptr = nullptr;
+        const float *bel = d == 0 ? root : vl.belief.as<float>();
+        const long long bstride = d == 0 ? m.HW : m.HWp;
+        const long long nwork = vmax[d], nq = nwork * NA;
+        double expect = 1.0;
+        for (int i = 0; i < d; ++i) expect *= 10.0;
+        const BandSet &bs = expect < 100.0 ? m.band_small : m.band_big;
+        const int pstride = pstride_of<MASK>(leaf);
+        ReduceArgs r;
+        r.part = m.part.as<double>(); r.pstride = pstride; r.nb = bs.nb; r.nwork = nwork; r.vmap = nullptr;
+        r.beliefs = bel; r.bstride = bstride; r.vpath = vl.path.as<uint64_t>(); r.vroot = vl.root.as<int32_t>();
+        r.root_step = m.ep_root_step.as<uint32_t>(); r.root_ep = m.ep_root_ep.as<uint32_t>(); r.seed = cfg.seed;
+        r.level = d; r.n = n; r.O64 = m.d_O64.as<double>();
+        r.ngc = m.ngc; r.gc_cell = m.d_gc_cell.as<int32_t>(); r.gc_act = m.d_gc_act.as<int32_t>();
+        r.gc_val = m.d_gc_val.as<double>(); r.goal = m.goal;
+        r.p_stay = m.p_stay; r.p_int = m.p_int; r.p_lat = m.p_lat; r.gamma = m.gamma;
+        r.qbar = m.cur_leaf == QVTS_LEAF_FIB ? m.qbar_fib : m.qbar;
+        r.R = ql.R.as<double>(); r.P = ql.P.as<double>(); r.cnt = ql.cnt.as<uint16_t>();
+        r.umask = ql.umask.as<uint16_t>(); r.U = ql.U.as<int32_t>(); r.zdraw = nullptr;
+        r.Q = ql.Q.as<double>(); r.leafV = nullptr;
+        r.counters = m.counters.as<unsigned long long>();
+        r.xs = nullptr; r.m8 = m.d_m8.as<uint8_t>(); r.sig = m.d_sig.as<uint8_t>(); r.W = m.W; r.acc = m.acc;
+        r.nwork_dev = cnt + d;
+        if (cfg.sampler == QVTS_SAMPLER_ANCESTRAL) {
+            const int nch = (m.HW + 255) / 256;
+            QVTS_PROF(7, k_ancestral_x<MASK><<<(unsigned)nwork, 256, sizeof(double) * (2 * nch + 1), st>>>(
+                             bel, bstride, nullptr, nwork, m.HW, vl.path.as<uint64_t>(), vl.root.as<int32_t>(),
+                             r.root_step, r.root_ep, cfg.seed, d, n, m.xs.as<int32_t>()));
+            r.xs = m.xs.as<int32_t>();
+        }
+        int nb_eff = bs.nb;
+        if (leaf) QVTS_TRY((launch_hist<MASK, true>(m, bs, bel, bstride, nullptr, nwork, pstride, st, &nb_eff, nullptr,
+                                                    nullptr, nullptr, nullptr, cnt + d)));
+        else QVTS_TRY((launch_hist<MASK, false>(m, bs, bel, bstride, nullptr, nwork, pstride, st, &nb_eff, nullptr,
+                                                 nullptr, nullptr, nullptr, cnt + d)));
+        r.nb = nb_eff;
+        if (leaf) QVTS_TRY((launch_reduce<MASK, true>(m, r, st)));
+        else QVTS_TRY((launch_reduce<MASK, false>(m, r, st)));
+        if (leaf) break;
+        QVTS_PROF(4, k_scan<<<1, 1024, 0, st>>>(ql.U.as<int32_t>(), ql.off.as<int32_t>(), nq, cnt + d + 1, nullptr,
+                                               cnt + d, NA));
+        VLevel &vc = m.vl[d + 1];
+        CorrectArgs c;
+        c.beliefs = bel; c.bstride = bstride; c.vmap = nullptr;
+        c.m8 = m.d_m8.as<uint8_t>(); c.cell = m.d_cell.as<uint8_t>();
+        c.O64 = m.d_O64.as<double>(); c.P = ql.P.as<double>(); c.cnt = ql.cnt.as<uint16_t>();
+        c.umask = ql.umask.as<uint16_t>(); c.off = ql.off.as<int32_t>();
+        c.vpath = vl.path.as<uint64_t>(); c.vroot = vl.root.as<int32_t>(); c.level = d;
+        c.child = vc.belief.as<float>(); c.cstride = m.HWp;
+        c.cpath = vc.path.as<uint64_t>(); c.cparent = vc.parent_q.as<int32_t>(); c.cz = vc.z.as<int32_t>();
+        c.cf = vc.f.as<int32_t>(); c.croot = vc.root.as<int32_t>();
+        c.H = m.H; c.W = m.W; c.G = (m.W + 3) / 4;
+        c.rows_cta = correct_rows_per_cta(m.H, c.G);
+        c.ntiles = (m.H + c.rows_cta - 1) / c.rows_cta;
+        c.p_int = (float)m.p_int; c.p_stay = (float)m.p_stay; c.p_lat = (float)m.p_lat; c.qsel = -1;
+        c.sel_q = c.sel_z = c.sel_out = nullptr;
+        c.nwork_dev = cnt + d;
+        QVTS_PROF(5, k_correct<MASK><<<(unsigned)(nq * c.ntiles), 256, 0, st>>>(c));
+    }
+    for (int d = D - 1; d >= 0; --d) {
+        QLevel &ql = m.ql[d];
+        VLevel &vl = m.vl[d];
+        if (d == D - 1) {
+            QVTS_PROF(6, k_vmax<NA><<<nblk(vmax[d], 256), 256, 0, st>>>(ql.Q.as<double>(), vl.V.as<double>(), vmax[d],
+                                                                        nullptr, cnt + d));
+        } else {
+            VLevel &vc = m.vl[d + 1];
+            QVTS_PROF(6, k_backup<NA><<<nblk(vmax[d] * 32, 256), 256, 0, st>>>(
+                             vmax[d], nullptr, ql.R.as<double>(), ql.umask.as<uint16_t>(), ql.off.as<int32_t>(),
+                             vc.V.as<double>(), vc.f.as<int32_t>(), n, m.gamma, ql.Q.as<double>(), vl.V.as<double>(),
+                             cnt + d));
+        }
+    }
+    QVTS_CUDA(cudaGetLastError());
+    return QVTS_OK;
+}
+
+// workspace for the worst-case tree (outside any capture: ensure() may allocate)
+template <uint32_t MASK>
+static qvts_status plan_dev_prepare_t(Model &m, const qvts_plan_cfg &cfg, const long long *vmax) {
+    constexpr int NA = mask_count(MASK);
+    const int D = cfg.depth;
+    QVTS_TRY(m.lvl_cnt.ensure(sizeof(long long) * (kMaxLevels + 1)));
+    QVTS_TRY(m.counters.ensure(sizeof(unsigned long long) * 4));
+    QVTS_TRY(m.total.ensure(sizeof(long long)));
+    size_t part = 0;
+    for (int d = 0; d <= D; ++d) {
+        VLevel &vl = m.vl[d];
+        const long long tn = std::max(1LL, vmax[d]);
+        QVTS_TRY(vl.path.ensure(sizeof(uint64_t) * tn));
+        QVTS_TRY(vl.root.ensure(sizeof(int32_t) * tn));
+        QVTS_TRY(vl.V.ensure(sizeof(double) * tn));
+        if (d >= 1) {
+            QVTS_TRY(vl.parent_q.ensure(sizeof(int32_t) * tn));
+            QVTS_TRY(vl.z.ensure(sizeof(int32_t) * tn));
+            QVTS_TRY(vl.f.ensure(sizeof(int32_t) * tn));
+            if (d < D) QVTS_TRY(vl.belief.ensure(sizeof(float) * (size_t)tn * m.HWp));
+        }
+        if (d < D) {
+            QLevel &ql = m.ql[d];
+            const long long nq = tn * NA;
+            QVTS_TRY(ql.R.ensure(sizeof(double) * nq));
+            QVTS_TRY(ql.P.ensure(sizeof(double) * 16 * nq));
+            QVTS_TRY(ql.cnt.ensure(sizeof(uint16_t) * 16 * nq));
+            QVTS_TRY(ql.umask.ensure(sizeof(uint16_t) * nq));
+            QVTS_TRY(ql.U.ensure(sizeof(int32_t) * nq));
+            QVTS_TRY(ql.off.ensure(sizeof(int32_t) * nq));
+            QVTS_TRY(ql.Q.ensure(sizeof(double) * nq));
+            double expect = 1.0;
+            for (int i = 0; i < d; ++i) expect *= 10.0;
+            const BandSet &bs = expect < 100.0 ? m.band_small : m.band_big;
+            part = std::max(part, sizeof(double) * (size_t)(tn + 1) * bs.nb * pstride_of<MASK>(d == D - 1));
+            if (cfg.sampler == QVTS_SAMPLER_ANCESTRAL)
+                QVTS_TRY(m.xs.ensure(sizeof(int32_t) * (size_t)nq * cfg.n_samples));
+        }
+    }
+    QVTS_TRY(m.part.ensure(part));
     return QVTS_OK;
 }
 
@@ -1682,6 +1854,86 @@ qvts_status correct_selected(Model &m, const RootBatch &roots, const int32_t *se
     return s;
 }
 
+static qvts_status plan_dev_prepare(Model &m, const qvts_plan_cfg &cfg, const long long *vmax) {
+    qvts_status s = QVTS_ERR_INVALID_ARG;
+#define QVTS_PDP(MASK) s = plan_dev_prepare_t<MASK>(m, cfg, vmax)
+    QVTS_DISPATCH_MASK(m.mask, QVTS_PDP);
+#undef QVTS_PDP
+    return s;
+}
+
+static qvts_status plan_levels_dev(Model &m, const float *root, const qvts_plan_cfg &cfg, const long long *vmax,
+                                   cudaStream_t st) {
+    qvts_status s = QVTS_ERR_INVALID_ARG;
+#define QVTS_PLD(MASK) s = plan_levels_dev_t<MASK>(m, root, cfg, vmax, st)
+    QVTS_DISPATCH_MASK(m.mask, QVTS_PLD);
+#undef QVTS_PLD
+    return s;
+}
+
+// One graph-captured plan step (see plan_levels_dev_t): root copied into a private buffer, keys
+// uploaded, the cached graph replayed (re-captured when the configuration or a buffer changed), then
+// Q(root, .), the level counts and the counters read back with one synchronisation.
+static qvts_status plan_step_graph(Model &m, const float *root_dev, const qvts_plan_cfg &cfg, const long long *vmax,
+                                   cudaStream_t cst, double *q, long long *nv) {
+    if (!m.pg_stream) QVTS_CUDA(cudaStreamCreateWithFlags(&m.pg_stream, cudaStreamNonBlocking));
+    if (!m.pg_join) QVTS_CUDA(cudaEventCreateWithFlags(&m.pg_join, cudaEventDisableTiming));
+    cudaStream_t st = m.pg_stream;
+    QVTS_CUDA(cudaEventRecord(m.pg_join, cst));
+    QVTS_CUDA(cudaStreamWaitEvent(st, m.pg_join, 0));
+    m.cur_leaf = cfg.leaf_bound;
+    QVTS_TRY(plan_dev_prepare(m, cfg, vmax));
+    QVTS_TRY(m.root_buf.ensure(sizeof(float) * (size_t)m.HWp));
+    QVTS_CUDA(cudaMemcpyAsync(m.root_buf.p, root_dev, sizeof(float) * m.HW, cudaMemcpyDeviceToDevice, st));
+    uint32_t keys[2] = {cfg.step, cfg.episode};
+    QVTS_CUDA(cudaMemcpyAsync(m.ep_root_step.p, &keys[0], sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+    QVTS_CUDA(cudaMemcpyAsync(m.ep_root_ep.p, &keys[1], sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+    std::vector<uintptr_t> key = {(uintptr_t)cfg.depth, (uintptr_t)cfg.n_samples, (uintptr_t)cfg.seed,
+                                  (uintptr_t)cfg.sampler, (uintptr_t)cfg.leaf_bound, (uintptr_t)m.part.p,
+                                  (uintptr_t)m.lvl_cnt.p, (uintptr_t)m.counters.p, (uintptr_t)m.root_buf.p,
+                                  (uintptr_t)m.xs.p, (uintptr_t)m.ep_root_step.p, (uintptr_t)m.ep_root_ep.p};
+    for (int d = 0; d <= cfg.depth; ++d) {
+        const VLevel &vl = m.vl[d];
+        for (const DevBuf *b : {&vl.path, &vl.parent_q, &vl.z, &vl.f, &vl.root, &vl.V, &vl.belief}) key.push_back((uintptr_t)b->p);
+        if (d < cfg.depth) {
+            const QLevel &ql = m.ql[d];
+            for (const DevBuf *b : {&ql.R, &ql.P, &ql.cnt, &ql.umask, &ql.U, &ql.off, &ql.Q}) key.push_back((uintptr_t)b->p);
+        }
+    }
+    if (!m.pg_exec || key != m.pg_key) {
+        if (m.pg_exec) { cudaGraphExecDestroy(m.pg_exec); m.pg_exec = nullptr; }
+        cudaGraph_t graph;
+        QVTS_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+        const qvts_status s2 = plan_levels_dev(m, m.root_buf.as<float>(), cfg, vmax, st);
+        const cudaError_t e = cudaStreamEndCapture(st, &graph);
+        QVTS_TRY(s2);
+        QVTS_CUDA(e);
+        const cudaError_t e2 = cudaGraphInstantiate(&m.pg_exec, graph, 0);
+        cudaGraphDestroy(graph);
+        QVTS_CUDA(e2);
+        m.pg_key = key;
+    }
+    QVTS_CUDA(cudaEventRecord(m.ev0, st));
+    QVTS_CUDA(cudaGraphLaunch(m.pg_exec, st));
+    QVTS_CUDA(cudaEventRecord(m.ev1, st));
+    long long cnt[kMaxLevels + 1];
+    unsigned long long ctr[2];
+    QVTS_CUDA(cudaMemcpyAsync(q, m.ql[0].Q.p, sizeof(double) * m.NA, cudaMemcpyDeviceToHost, st));
+    QVTS_CUDA(cudaMemcpyAsync(cnt, m.lvl_cnt.p, sizeof(long long) * cfg.depth, cudaMemcpyDeviceToHost, st));
+    QVTS_CUDA(cudaMemcpyAsync(ctr, m.counters.p, sizeof(ctr), cudaMemcpyDeviceToHost, st));
+    QVTS_CUDA(cudaStreamSynchronize(st));
+    QVTS_CUDA(cudaEventRecord(m.pg_join, st));
+    QVTS_CUDA(cudaStreamWaitEvent(cst, m.pg_join, 0));
+    for (int d = 0; d < cfg.depth; ++d) { nv[d] = cnt[d]; m.vl[d].n = cnt[d]; m.ql[d].nwork = cnt[d]; }
+    nv[cfg.depth] = (long long)ctr[1];
+    m.last_flagged = (long long)ctr[0];
+    m.last_depth = cfg.depth;
+    m.last_shard_level = -1;
+    m.last_n = cfg.n_samples;
+    m.last_trace = false;
+    return QVTS_OK;
+}
+
 qvts_status plan_levels(Model &m, const RootBatch &roots, const qvts_plan_cfg &cfg, const qvts_comm *comm,
                         cudaStream_t st, long long *nv_out) {
     qvts_status s = QVTS_ERR_INVALID_ARG;
@@ -1718,12 +1970,21 @@ extern "C" qvts_status qvts_plan_step(qvts_model *m, const float *root_dev, cons
     QVTS_CUDA(cudaMemcpyAsync(m->ep_root_ep.p, &keys[1], sizeof(uint32_t), cudaMemcpyHostToDevice, st));
     RootBatch rb{root_dev, (long long)m->HW, 1, m->ep_root_step.as<uint32_t>(), m->ep_root_ep.as<uint32_t>()};
     long long nv[kMaxLevels + 1] = {0};
-    QVTS_CUDA(cudaEventRecord(m->ev0, st));
-    QVTS_TRY(plan_levels(*m, rb, *cfg, comm, st, nv));
-    QVTS_CUDA(cudaEventRecord(m->ev1, st));
     double q[9];
-    QVTS_CUDA(cudaMemcpyAsync(q, m->ql[0].Q.p, sizeof(double) * m->NA, cudaMemcpyDeviceToHost, st));
-    QVTS_CUDA(cudaStreamSynchronize(st));
+    // small single-GPU trees: the graph-captured step (QVTS_PLAN_GRAPH=0 keeps the level-synchronous one)
+    long long vmax[kMaxLevels + 1];
+    const char *ev_graph = std::getenv("QVTS_PLAN_GRAPH");
+    const bool use_graph = (!ev_graph || std::atoi(ev_graph) != 0) && (!comm || comm->nranks == 1) &&
+                           !cfg->want_trace && !m->prof && graph_eligible(*m, *cfg, vmax);
+    if (use_graph) {
+        QVTS_TRY(plan_step_graph(*m, root_dev, *cfg, vmax, st, q, nv));
+    } else {
+        QVTS_CUDA(cudaEventRecord(m->ev0, st));
+        QVTS_TRY(plan_levels(*m, rb, *cfg, comm, st, nv));
+        QVTS_CUDA(cudaEventRecord(m->ev1, st));
+        QVTS_CUDA(cudaMemcpyAsync(q, m->ql[0].Q.p, sizeof(double) * m->NA, cudaMemcpyDeviceToHost, st));
+        QVTS_CUDA(cudaStreamSynchronize(st));
+    }
     float ms = 0.f;
     QVTS_CUDA(cudaEventElapsedTime(&ms, m->ev0, m->ev1));
     prof_collect(*m);

@@ -102,6 +102,12 @@ struct Model {
     long long last_flagged = 0;
     bool last_trace = false;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // graph-captured plan step (small trees): device level counts, private stream, cached graph
+    DevBuf lvl_cnt, root_buf;
+    cudaStream_t pg_stream = nullptr;
+    cudaEvent_t pg_join = nullptr;
+    cudaGraphExec_t pg_exec = nullptr;
+    std::vector<uintptr_t> pg_key;
     // instrumentation
     bool prof = false;
     qvts_profile pstat{};

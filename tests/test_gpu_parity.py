@@ -536,3 +536,24 @@ def test_belief_update_batch(Q, name):
         assert np.max(np.abs(res[i] - ob)) <= 1e-5 * max(1e-3, float(np.max(ob)))
         assert np.all(res[i][gm.occupancy == 1] == 0.0)
     g.close()
+
+
+@pytest.mark.parametrize("name,depth,n", [("C1", 2, 4), ("ragged", 3, 8), ("paper", 3, 16), ("C3", 3, 8),
+                                          ("ragged", 1, 300), ("C1", 4, 2)])
+def test_graph_plan_step_is_bit_identical(Q, name, depth, n, monkeypatch):
+    """Small single-GPU plan steps run as one captured CUDA graph with device-side level counts:
+    the same root Q bits, level counts and action as the level-synchronous path, across repeated
+    (cached-graph) calls with different step keys; and the root Q matches the oracle."""
+    gm = W.CONFIGS["C3"]["map"]() if name == "C3" else MAPS[name][0]()
+    mask = W.A8 if name == "C3" else MAPS[name][1]
+    g, o, Qo, _, _ = pair(Q, gm, mask)
+    b32 = np.asarray(W.random_belief(gm, 11), np.float32)
+    for step in (0, 1, 2):
+        out = {}
+        for flag in ("1", "0"):
+            monkeypatch.setenv("QVTS_PLAN_GRAPH", flag)
+            r = g.plan_step(dev(b32), depth, n, seed=9, step=step)
+            out[flag] = (np.array(r.q_root[:g.n_actions]), list(r.n_vnodes[:depth + 1]), r.action)
+        assert np.array_equal(out["1"][0], out["0"][0]) and out["1"][1] == out["0"][1] and out["1"][2] == out["0"][2]
+    ro = o.plan(Qo, b32.astype(np.float64), depth, n, seed=9, step=2)
+    assert np.max(np.abs(out["1"][0] - ro.qroot)) <= PT.TOL * 10
