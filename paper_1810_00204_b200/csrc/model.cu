@@ -41,12 +41,6 @@ void DevBuf::release() {
     cap = 0;
 }
 
-template <class T>
-static qvts_status upload(DevBuf &b, const std::vector<T> &v) {
-    QVTS_TRY(b.ensure(sizeof(T) * std::max<size_t>(v.size(), 1)));
-    if (!v.empty()) QVTS_CUDA(cudaMemcpy(b.p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
-    return QVTS_OK;
-}
 
 // ---- instrumentation -----------------------------------------------------------------------------
 static cudaEvent_t next_event(Model &m) {
@@ -219,7 +213,7 @@ qvts_status build_qlists(Model &m, const double *src64, double qbar, bool fib, c
                                                             qbar, dst.as<float>());
         QVTS_CUDA(cudaGetLastError());
     }
-    return QVTS_OK;
+    return build_leaf_qfrag(m, src64, qbar, fib, st);
 }
 
 // ---- Fast Informed Bound (Eq. 7), fp64 -----------------------------------------
@@ -529,6 +523,7 @@ extern "C" qvts_status qvts_model_create(const qvts_model_desc *d, qvts_model **
         if (const char *ev = std::getenv("QVTS_BAND_ROWS")) big_rows = std::max(1, std::atoi(ev));
         if ((st = build_bands(*m, m->band_big, big_rows)) != QVTS_OK) break;
         if ((st = build_bands(*m, m->band_small, std::max(1, 1024 / W))) != QVTS_OK) break;
+        if ((st = build_leaf_mma(*m)) != QVTS_OK) break;
         if (cudaEventCreate(&m->ev0) != cudaSuccess || cudaEventCreate(&m->ev1) != cudaSuccess) {
             set_error("cudaEventCreate failed"); st = QVTS_ERR_CUDA; break;
         }
@@ -549,6 +544,9 @@ extern "C" void qvts_model_destroy(qvts_model *m) {
                       &m->pb_b0, &m->pb_B, &m->pb_G, &m->pb_Gn, &m->pb_GT, &m->pb_Bbar, &m->pb_Sc, &m->pb_Rb,
                       &m->pb_sel, &m->pb_astar, &m->pb_cand, &m->pb_misc, &m->pb_cls, &m->pb_chunks, &m->pb_part};
     for (DevBuf *b : bufs) b->release();
+    for (DevBuf *b : {&m->lm.cs, &m->lm.offs, &m->lm.m8w, &m->lm.cells, &m->lm.qfr, &m->lm.qfr8, &m->lm.qfr_fib,
+                      &m->lm.qfr8_fib})
+        b->release();
     for (BandSet *bs : {&m->band_big, &m->band_small}) {
         bs->bands.release(); bs->entries.release(); bs->slot_cell.release(); bs->qlist.release(); bs->qlist_fib.release();
     }

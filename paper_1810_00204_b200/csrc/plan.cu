@@ -1216,6 +1216,15 @@ static qvts_status launch_hist(Model &m, const BandSet &bs, const float *beliefs
     return QVTS_OK;
 }
 
+// leaf level on the tensor cores (leafmma.cu): one fp64 record per parent (nb = 1)
+static qvts_status launch_leaf_mma_prof(Model &m, const float *beliefs, long long bstride, const int32_t *vmap,
+                                        long long nwork, int pstride, cudaStream_t st, const int32_t *skip,
+                                        const long long *nwork_dev) {
+    QVTS_PROF(0, QVTS_TRY(launch_leaf_mma(m, beliefs, bstride, vmap, nwork, pstride, st, skip, nwork_dev)));
+    m.pstat.leaf_cells += nwork * m.n_free;
+    return QVTS_OK;
+}
+
 template <uint32_t MASK, bool LEAF>
 static qvts_status launch_reduce(Model &m, const ReduceArgs &r, cudaStream_t st) {
     constexpr int NA = mask_count(MASK);
@@ -1305,7 +1314,7 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
             for (int i = 0; i < d; ++i) expect *= 10.0;
             const BandSet &bs = expect < 100.0 ? m.band_small : m.band_big;
             const int pstride = pstride_of<MASK>(leaf);
-            QVTS_TRY(m.part.ensure(sizeof(double) * (size_t)(nwork + 1) * bs.nb * pstride));
+            QVTS_TRY(m.part.ensure(sizeof(double) * (size_t)(nwork + 1) * std::max(bs.nb, leaf_mma_records()) * pstride));
             int nb_eff = bs.nb;
             ReduceArgs r;
             r.part = m.part.as<double>(); r.pstride = pstride; r.nb = bs.nb; r.nwork = nwork; r.vmap = vmap;
@@ -1347,7 +1356,10 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
                 r.goalv = m.fl_goalv.as<float>(); r.nf = m.nfcells; r.gc_fidx = m.d_gc_fidx.as<int32_t>();
             }
             const ReduceArgs *rf = r.xs ? nullptr : &r;   // the fused reduce has no x draws
-            if (leaf) QVTS_TRY((launch_hist<MASK, true>(m, bs, bel, bstride, vmap, nwork, pstride, st, &nb_eff, rf, &fused,
+            if (leaf && !fuse && leaf_mma_enabled(m, bstride, bel)) {
+                QVTS_TRY(launch_leaf_mma_prof(m, bel, bstride, vmap, nwork, pstride, st, nullptr, nullptr));
+                nb_eff = leaf_mma_records();
+            } else if (leaf) QVTS_TRY((launch_hist<MASK, true>(m, bs, bel, bstride, vmap, nwork, pstride, st, &nb_eff, rf, &fused,
                                                         nullptr, fuse ? &fl : nullptr)));
             else QVTS_TRY((launch_hist<MASK, false>(m, bs, bel, bstride, vmap, nwork, pstride, st, &nb_eff, rf, &fused)));
             r.nb = nb_eff;
@@ -1513,7 +1525,10 @@ static qvts_status plan_levels_dev_t(Model &m, const float *root, const qvts_pla
             r.xs = m.xs.as<int32_t>();
         }
         int nb_eff = bs.nb;
-        if (leaf) QVTS_TRY((launch_hist<MASK, true>(m, bs, bel, bstride, nullptr, nwork, pstride, st, &nb_eff, nullptr,
+        if (leaf && leaf_mma_enabled(m, bstride, bel)) {
+            QVTS_TRY(launch_leaf_mma_prof(m, bel, bstride, nullptr, nwork, pstride, st, nullptr, cnt + d));
+            nb_eff = leaf_mma_records();
+        } else if (leaf) QVTS_TRY((launch_hist<MASK, true>(m, bs, bel, bstride, nullptr, nwork, pstride, st, &nb_eff, nullptr,
                                                     nullptr, nullptr, nullptr, cnt + d)));
         else QVTS_TRY((launch_hist<MASK, false>(m, bs, bel, bstride, nullptr, nwork, pstride, st, &nb_eff, nullptr,
                                                  nullptr, nullptr, nullptr, cnt + d)));
@@ -1593,7 +1608,8 @@ static qvts_status plan_dev_prepare_t(Model &m, const qvts_plan_cfg &cfg, const 
             double expect = 1.0;
             for (int i = 0; i < d; ++i) expect *= 10.0;
             const BandSet &bs = expect < 100.0 ? m.band_small : m.band_big;
-            part = std::max(part, sizeof(double) * (size_t)(tn + 1) * bs.nb * pstride_of<MASK>(d == D - 1));
+            part = std::max(part, sizeof(double) * (size_t)(tn + 1) * std::max(bs.nb, leaf_mma_records()) *
+                                      pstride_of<MASK>(d == D - 1));
             if (cfg.sampler == QVTS_SAMPLER_ANCESTRAL)
                 QVTS_TRY(m.xs.ensure(sizeof(int32_t) * (size_t)nq * cfg.n_samples));
         }

@@ -58,6 +58,16 @@ struct BandSet {
     DevBuf bands, entries, slot_cell, qlist, qlist_fib;
 };
 
+// Tensor-core leaf level (leafmma.cu): per row band, the free cells sorted by wall-signature class
+// and cut into chunks of 16 (the MMA's K); per (chunk, lane) the Q' B fragments.
+struct LeafMma {
+    int R = 0, nb = 0, TP = 0, tile_words = 0, ptile = 0;   // nb = 0: not available (scalar leaf kernel)
+    long long nchunks = 0;
+    std::vector<int32_t> h_cs;       // [nb][17] chunk ranges per class (host only)
+    std::vector<int32_t> h_cells;    // [nchunks][16] cell of each K position (-1 = padding)
+    DevBuf cs /* [nb][5] warp chunk ranges */, offs, m8w /* diagonal masks */, cells, qfr, qfr8, qfr_fib, qfr8_fib;
+};
+
 // Per-level node arrays of the level-batched tree (SoA).
 struct VLevel {
     long long n = 0;                  // V-nodes at this level
@@ -85,6 +95,7 @@ struct Model {
     DevBuf d_fcells, d_gc_fidx, fl_goalv;   // fused leaf level: goal-term cells, their values
     int nfcells = 0;
     BandSet band_big, band_small;
+    LeafMma lm;
     // value iteration
     bool have_q = false;
     double qbar = 0.0;
@@ -144,6 +155,21 @@ struct Model {
 void prof_begin(Model &m, int cat, cudaStream_t st, cudaEvent_t *out);
 void prof_end(Model &m, int cat, cudaStream_t st, cudaEvent_t a);
 void prof_collect(Model &m);   // after a stream sync: fold recorded event pairs into pstat
+
+template <class T>
+static qvts_status upload(DevBuf &b, const std::vector<T> &v) {
+    QVTS_TRY(b.ensure(sizeof(T) * (v.size() > 1 ? v.size() : 1)));
+    if (!v.empty()) QVTS_CUDA(cudaMemcpy(b.p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+    return QVTS_OK;
+}
+
+// leafmma.cu
+qvts_status build_leaf_mma(Model &m);
+qvts_status build_leaf_qfrag(Model &m, const double *src64, double qbar, bool fib, cudaStream_t st);
+bool leaf_mma_enabled(const Model &m, long long bstride, const float *beliefs);
+int leaf_mma_records();              // fp64 records per parent written by the leaf kernel (one per warp)
+qvts_status launch_leaf_mma(Model &m, const float *beliefs, long long bstride, const int32_t *vmap, long long nwork,
+                            int pstride, cudaStream_t st, const int32_t *skip, const long long *nwork_dev);
 
 // model.cu
 qvts_status build_bands(Model &m, BandSet &bs, int rows);

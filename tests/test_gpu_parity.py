@@ -384,6 +384,7 @@ def test_best_first_stop_rules(Q):
     res = g.plan_best_first(dev(b32), 8, 10000, max_depth=1)
     assert res.n_expansions == 1 and res.stop_reason == Q.QVTS_BF_TERMINAL
     import time
+    g.plan_best_first(dev(b32), 8, 100000, max_depth=8, time_budget_ms=20.0)   # warm: graphs, pool
     t0 = time.perf_counter()
     res = g.plan_best_first(dev(b32), 8, 100000, max_depth=8, time_budget_ms=20.0)
     dt = (time.perf_counter() - t0) * 1e3
@@ -489,6 +490,7 @@ def test_fused_leaf_level_is_bit_identical(Q, name, depth, n, monkeypatch):
     g, o, Qo, _, _ = pair(Q, gm, mask)
     b32 = np.asarray(W.random_belief(gm, 7), np.float32)
     out = {}
+    monkeypatch.setenv("QVTS_LEAF_MMA", "0")    # the fused rebuild lives in the scalar leaf kernel
     for fused in ("1", "0"):
         monkeypatch.setenv("QVTS_FUSED_LEAF", fused)
         r = g.plan_step(dev(b32), depth, n, seed=5, step=2)
@@ -503,6 +505,7 @@ def test_fused_leaf_episodes_identical(Q, monkeypatch):
     g = Q.Model(gm, action_mask=mask)
     g.value_iteration()
     recs = {}
+    monkeypatch.setenv("QVTS_LEAF_MMA", "0")
     for fused in ("1", "0"):
         monkeypatch.setenv("QVTS_FUSED_LEAF", fused)
         rec, _ = g.run_episodes(6, max_steps=30, planner=Q.QVTS_PLANNER_QVTS, depth=3, n_samples=8, seed=3)
@@ -556,4 +559,32 @@ def test_graph_plan_step_is_bit_identical(Q, name, depth, n, monkeypatch):
             out[flag] = (np.array(r.q_root[:g.n_actions]), list(r.n_vnodes[:depth + 1]), r.action)
         assert np.array_equal(out["1"][0], out["0"][0]) and out["1"][1] == out["0"][1] and out["1"][2] == out["0"][2]
     ro = o.plan(Qo, b32.astype(np.float64), depth, n, seed=9, step=2)
+    assert np.max(np.abs(out["1"][0] - ro.qroot)) <= PT.TOL * 10
+
+
+@pytest.mark.parametrize("name,depth,n", [("C1", 2, 4), ("ragged", 3, 8), ("paper", 3, 16), ("C3", 3, 8),
+                                          ("ragged", 1, 300)])
+def test_leaf_mma_matches_scalar_leaf_and_oracle(Q, name, depth, n, monkeypatch):
+    """The tensor-core leaf kernel (fp16 hi/lo split products, leafmma.cu) against the scalar fp32
+    leaf kernel and the oracle: identical tree (counts, draws come from the non-leaf levels),
+    every sampled leaf value and root Q within the north-star 1e-5."""
+    gm = W.CONFIGS["C3"]["map"]() if name == "C3" else MAPS[name][0]()
+    mask = W.A8 if name == "C3" else MAPS[name][1]
+    g, o, Qo, _, _ = pair(Q, gm, mask)
+    b32 = np.asarray(W.random_belief(gm, 13), np.float32)
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("QVTS_LEAF_MMA", flag)
+        r = g.plan_step(dev(b32), depth, n, seed=4, step=1, want_trace=True)
+        t = g.trace(with_draws=True, n_samples=n)
+        lq = t["levels"][depth - 1]["q"]
+        lv = np.array(t["leafV"]).reshape(-1, 16)
+        sampled = np.array(lq["cnt"]) > 0
+        out[flag] = (np.array(r.q_root[:g.n_actions]), list(r.n_vnodes[:depth + 1]), r.action,
+                     np.where(sampled, lv, 0.0), np.array(lq["Q"]))
+    assert out["1"][1] == out["0"][1]
+    assert np.max(np.abs(out["1"][3] - out["0"][3])) <= PT.TOL      # every sampled leaf value
+    assert np.max(np.abs(out["1"][4] - out["0"][4])) <= PT.TOL      # every leaf-level Q-node
+    assert np.max(np.abs(out["1"][0] - out["0"][0])) <= PT.TOL
+    ro = o.plan(Qo, b32.astype(np.float64), depth, n, seed=4, step=1)
     assert np.max(np.abs(out["1"][0] - ro.qroot)) <= PT.TOL * 10
