@@ -665,23 +665,26 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_hist(HistArgs a) {
                 }
             }
         } else if (a.vec16) {
+            // warp per tile row, lanes over the row's 16-byte groups (no index division)
             const int W4 = a.W >> 2;
-            for (int i = t; i < TH * W4; i += kPairThreads) {
-                const int tr = i / W4, c4 = i - tr * W4;
+            for (int tr = warp; tr < TH; tr += kPairThreads / 32) {
                 const int r = row0 - 1 + tr;
                 const bool ok = vp && r >= 0 && r < a.H;
-                const float *src = ok ? b + (long long)r * a.W + 4 * c4 : b;
-                const uint32_t dst = sbase + 4u * (uint32_t)(tr * TP + 4 + 4 * c4);
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0));
+                const float *src = ok ? b + (long long)r * a.W : b;
+                const uint32_t dst = sbase + 4u * (uint32_t)(tr * TP + 4);
+                for (int c4 = lane; c4 < W4; c4 += 32)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst + 16u * c4),
+                                 "l"(ok ? src + 4 * c4 : src), "r"(ok ? 16 : 0));
             }
         } else {
-            for (int i = t; i < TH * a.W; i += kPairThreads) {
-                const int tr = i / a.W, c = i - tr * a.W;
+            for (int tr = warp; tr < TH; tr += kPairThreads / 32) {
                 const int r = row0 - 1 + tr;
                 const bool ok = vp && r >= 0 && r < a.H;
-                const float *src = ok ? b + (long long)r * a.W + c : b;
-                const uint32_t dst = sbase + 4u * (uint32_t)(tr * TP + 4 + c);
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 4 : 0));
+                const float *src = ok ? b + (long long)r * a.W : b;
+                const uint32_t dst = sbase + 4u * (uint32_t)(tr * TP + 4);
+                for (int c = lane; c < a.W; c += 32)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dst + 4u * c),
+                                 "l"(ok ? src + c : src), "r"(ok ? 4 : 0));
             }
         }
         for (int tr = t; tr < TH; tr += kPairThreads) {      // halo columns
