@@ -477,6 +477,8 @@ struct CorrectArgs {
     const int32_t *skip = nullptr;             // device flag (best-first)
     const long long *cbase_dev = nullptr;      // device child-index base (best-first pool)
     const long long *nwork_dev = nullptr;      // device-side parent count (graph-captured plan step)
+    int stage_tp = 0;                          // > 0: the CTA's parent rows (+ halo) are staged in shared
+                                               // memory with this row pitch (correct_stage)
 };
 
 // bbar_a for 4 consecutive cells (r, c0..c0+3): bbar = p_stay b + p_int h_a + p_lat (h_l1 + h_l2),
@@ -964,18 +966,52 @@ __global__ void __launch_bounds__(256) k_correct(CorrectArgs a) {
             }
         }
     }
-    __syncthreads();
     // this CTA covers rows [tile * rows_cta, +rows_cta): 4 consecutive cells per thread, rows_it
     // rows per pass
     const int W = a.W;
     const float *__restrict__ b = a.beliefs + v * a.bstride;
     const bool vec = ((W & 3) == 0) && ((a.cstride & 3) == 0) && ((a.bstride & 3) == 0);
     const int r_end = min(a.H, (tile + 1) * a.rows_cta);
+    // staged path: the parent's rows [r0 - 1, r_end + 1) land in shared memory in one cp.async
+    // burst (row pitch stage_tp, column c at c + 4, zero halo columns and off-map rows), so the
+    // neighbourhood loads below no longer wait on L2 one pass at a time
+    extern __shared__ float4 c_smem4[];
+    float *stile = reinterpret_cast<float *>(c_smem4);
+    const int r0 = tile * a.rows_cta;
+    if (a.stage_tp > 0) {
+        const int TPc = a.stage_tp, nr = r_end - r0 + 2, W4 = W >> 2;
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        for (int tr = warp; tr < nr; tr += 8) {
+            const int rr = r0 - 1 + tr;
+            const bool ok = rr >= 0 && rr < a.H;
+            const float *src = ok ? b + (long long)rr * W : b;
+            const uint32_t dst = (uint32_t)__cvta_generic_to_shared(stile + tr * TPc + 4);
+            for (int c4 = lane; c4 < W4; c4 += 32)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst + 16u * c4),
+                             "l"(ok ? src + 4 * c4 : src), "r"(ok ? 16 : 0));
+            if (lane == 0) {
+                stile[tr * TPc + 3] = 0.f;
+                stile[tr * TPc + 4 + W] = 0.f;
+            }
+        }
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();
     for (int idx = threadIdx.x; idx < a.rows_cta * a.G; idx += 256) {
         const int r = tile * a.rows_cta + idx / a.G, c0 = 4 * (idx % a.G);
         if (r >= r_end) break;
         // rows r-1..r+1, columns c0-1..c0+4 (zero off-map)
         float nbh[3][6];
+        if (a.stage_tp > 0) {
+#pragma unroll
+            for (int dr = 0; dr < 3; ++dr) {
+                const float *row = stile + (r - r0 + dr) * a.stage_tp + 4 + c0;
+                const float4 m4 = *reinterpret_cast<const float4 *>(row);
+                nbh[dr][0] = row[-1];
+                nbh[dr][1] = m4.x; nbh[dr][2] = m4.y; nbh[dr][3] = m4.z; nbh[dr][4] = m4.w;
+                nbh[dr][5] = row[4];
+            }
+        } else
 #pragma unroll
         for (int dr = 0; dr < 3; ++dr) {
             const int rr = r + dr - 1;
@@ -1132,6 +1168,20 @@ __global__ void k_iota_stride(int32_t *out, long long n, int r, int G) {
 
 // ---- host orchestration -------------------------------------------------------------------------
 static inline unsigned nblk(long long n, int b) { return (unsigned)((n + b - 1) / b); }
+// k_correct's shared-memory staging of the parent rows: on when the rows are 16-byte copyable and
+// the CTA's rows + halo fit the default 48 KB; returns the dynamic shared memory to launch with
+static size_t correct_stage(CorrectArgs &c) {
+    const bool vec = (c.W & 3) == 0 && (c.cstride & 3) == 0 && (c.bstride & 3) == 0 &&
+                     (reinterpret_cast<uintptr_t>(c.beliefs) & 15) == 0;
+    const int tp = c.W + 8;
+    const size_t bytes = sizeof(float) * (size_t)(c.rows_cta + 2) * tp;
+    static const int env = [] {
+        const char *ev = std::getenv("QVTS_CORRECT_STAGE");
+        return ev ? std::atoi(ev) : 1;
+    }();
+    c.stage_tp = (env && vec && bytes <= 48 * 1024) ? tp : 0;
+    return c.stage_tp ? bytes : 0;
+}
 // k_correct: a CTA covers ~1024 groups of 4 cells (4 passes of its 256 threads)
 static inline int correct_rows_per_cta(int H, int G) {
     return std::min(H, std::max(1, 1024 / std::max(1, G)));
@@ -1415,7 +1465,8 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
                 QVTS_PROF(5, k_child_meta<MASK><<<nblk(nq * 16, 256), 256, 0, st>>>(c, nq, m.d_fcells.as<int32_t>(),
                                                                                  m.nfcells, m.fl_goalv.as<float>()));
             } else {
-                QVTS_PROF(5, k_correct<MASK><<<(unsigned)nblocks, 256, 0, st>>>(c));
+                { const size_t csm_ = correct_stage(c);
+                QVTS_PROF(5, k_correct<MASK><<<(unsigned)nblocks, 256, csm_, st>>>(c)); }
                 m.pstat.correct_cells_written += total * (long long)m.HW;
             }
             QVTS_CUDA(cudaGetLastError());
@@ -1557,7 +1608,8 @@ static qvts_status plan_levels_dev_t(Model &m, const float *root, const qvts_pla
         c.p_int = (float)m.p_int; c.p_stay = (float)m.p_stay; c.p_lat = (float)m.p_lat; c.qsel = -1;
         c.sel_q = c.sel_z = c.sel_out = nullptr;
         c.nwork_dev = cnt + d;
-        QVTS_PROF(5, k_correct<MASK><<<(unsigned)(nq * c.ntiles), 256, 0, st>>>(c));
+        { const size_t csm_ = correct_stage(c);
+        QVTS_PROF(5, k_correct<MASK><<<(unsigned)(nq * c.ntiles), 256, csm_, st>>>(c)); }
     }
     for (int d = D - 1; d >= 0; --d) {
         QLevel &ql = m.ql[d];
@@ -1673,7 +1725,8 @@ static qvts_status correct_selected_t(Model &m, const RootBatch &roots, const in
     c.ntiles = (m.H + c.rows_cta - 1) / c.rows_cta;
     c.p_int = (float)m.p_int; c.p_stay = (float)m.p_stay; c.p_lat = (float)m.p_lat; c.qsel = -1;
     c.sel_q = sel_q; c.sel_z = sel_z; c.sel_out = sel_out;
-    QVTS_PROF(5, k_correct<MASK><<<(unsigned)(n * c.ntiles), 256, 0, st>>>(c));
+    { const size_t csm_ = correct_stage(c);
+    QVTS_PROF(5, k_correct<MASK><<<(unsigned)(n * c.ntiles), 256, csm_, st>>>(c)); }
     QVTS_CUDA(cudaGetLastError());
     return QVTS_OK;
 }
@@ -1752,7 +1805,8 @@ static qvts_status expand_children_t(Model &m, const ExpandSpec &e, const QLevel
     c.p_int = (float)m.p_int; c.p_stay = (float)m.p_stay; c.p_lat = (float)m.p_lat; c.qsel = -1;
     const long long nblocks = e.nwork * NA * c.ntiles;
     if (nblocks > 0x7FFFFFFFLL) { set_error("too many correct blocks"); return QVTS_ERR_INVALID_ARG; }
-    QVTS_PROF(5, k_correct<MASK><<<(unsigned)nblocks, 256, 0, st>>>(c));
+    { const size_t csm_ = correct_stage(c);
+    QVTS_PROF(5, k_correct<MASK><<<(unsigned)nblocks, 256, csm_, st>>>(c)); }
     QVTS_CUDA(cudaGetLastError());
     return QVTS_OK;
 }
@@ -1808,7 +1862,8 @@ static qvts_status bf_expand_launch_t(Model &m, const BfLaunch &L, QLevel &ql, c
     c.ntiles = (m.H + c.rows_cta - 1) / c.rows_cta;
     c.p_int = (float)m.p_int; c.p_stay = (float)m.p_stay; c.p_lat = (float)m.p_lat; c.qsel = -1;
     c.skip = L.skip; c.cbase_dev = L.cbase;
-    QVTS_PROF(5, k_correct<MASK><<<(unsigned)(NA * c.ntiles), 256, 0, st>>>(c));
+    { const size_t csm_ = correct_stage(c);
+    QVTS_PROF(5, k_correct<MASK><<<(unsigned)(NA * c.ntiles), 256, csm_, st>>>(c)); }
     QVTS_CUDA(cudaGetLastError());
     return QVTS_OK;
 }
@@ -2093,7 +2148,8 @@ extern "C" qvts_status qvts_belief_update(qvts_model *m, const float *b_dev, int
     c.ntiles = (m->H + c.rows_cta - 1) / c.rows_cta;
     c.p_int = (float)m->p_int; c.p_stay = (float)m->p_stay; c.p_lat = (float)m->p_lat; c.qsel = j;
     c.sel_q = c.sel_z = c.sel_out = nullptr;
-#define QVTS_BU_CORR(MASK) k_correct<MASK><<<c.ntiles, 256, 0, st>>>(c)
+    const size_t csm_ = correct_stage(c);
+#define QVTS_BU_CORR(MASK) k_correct<MASK><<<c.ntiles, 256, csm_, st>>>(c)
     QVTS_DISPATCH_MASK(m->mask, QVTS_BU_CORR);
 #undef QVTS_BU_CORR
     QVTS_CUDA(cudaGetLastError());
@@ -2246,7 +2302,8 @@ extern "C" qvts_status qvts_belief_update_batch(qvts_model *m, const float *b_de
         k_bu_marg<MASK><<<(unsigned)nblocks, 256, 0, st>>>(c, m->part.as<double>());                            \
         k_bu_p<<<n, 16, 0, st>>>(m->part.as<double>(), c.ntiles, d_sel, n, m->d_O64.as<double>(),               \
                                  m->bu_R.as<double>());                                                          \
-        k_correct<MASK><<<(unsigned)nblocks, 256, 0, st>>>(c);                                                  \
+        { const size_t csm_ = correct_stage(c); \
+        k_correct<MASK><<<(unsigned)nblocks, 256, csm_, st>>>(c); } \
     }
     QVTS_DISPATCH_MASK(m->mask, QVTS_BUB);
 #undef QVTS_BUB
