@@ -80,40 +80,83 @@ def _oracle_sample(O, gm, om, Qo, D, n, rng, seed=1, step=0):
     return updates
 
 
-def cpu_baseline(budget_s=15.0):
-    O, gm, om, Qo, D, n = _oracle_setup()
-    rng = np.random.default_rng(0)
+_ORACLE = None     # set before forking the all-core workers (they share the compiled model)
+
+
+def _oracle_worker(job):
+    """One worker process: bounded oracle samples for budget_s seconds (or `count` samples)."""
+    seed, budget_s, count = job
+    os.environ["OMP_NUM_THREADS"] = "1"
+    O, gm, om, Qo, D, n = _ORACLE
+    rng = np.random.default_rng(1000 + seed)
     t0 = time.perf_counter()
     upd, k = 0, 0
-    while time.perf_counter() - t0 < budget_s:
-        upd += _oracle_sample(O, gm, om, Qo, D, n, rng, step=k)
+    while (count and k < count) or (not count and time.perf_counter() - t0 < budget_s):
+        upd += _oracle_sample(O, gm, om, Qo, D, n, rng, step=seed * 100000 + k)
         k += 1
-    dt = time.perf_counter() - t0
-    return {"value": upd / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{k} level-3 subtrees of the C4 depth-4 tree (oracle's own random paths, all 8 actions "
-                      f"and sampled leaves each), {upd} belief-node updates in {dt:.1f} s, single thread, fp64"}
+    return upd, k
+
+
+def _oracle_pool():
+    import multiprocessing as mp
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    return mp.get_context("fork").Pool(cores), cores
+
+
+def cpu_baseline(budget_s=10.0):
+    """the oracle as it stands, single thread and on all of the host's cores
+    (one forked worker per core running independent bounded samples of the same workload)."""
+    global _ORACLE
+    _ORACLE = _oracle_setup()
+    t0 = time.perf_counter()
+    upd1, k1 = _oracle_worker((0, budget_s, 0))
+    dt1 = time.perf_counter() - t0
+    pool, cores = _oracle_pool()
+    try:
+        t0 = time.perf_counter()
+        res = pool.map(_oracle_worker, [(1 + i, budget_s, 0) for i in range(cores)])
+        dtc = time.perf_counter() - t0
+    finally:
+        pool.close()
+        pool.join()
+    updc, kc = sum(r[0] for r in res), sum(r[1] for r in res)
+    return {"value": updc / dtc, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{kc} level-3 subtrees of the C4 depth-4 tree (oracle's own random paths, all 8 actions and "
+                      f"sampled leaves each) on {cores} worker processes, {updc} belief-node updates in {dtc:.1f} s, "
+                      f"fp64",
+            "single_thread": {"value": upd1 / dt1, "cores": 1,
+                              "sample": f"{k1} subtrees, {upd1} updates in {dt1:.1f} s"}}
 
 
 def run_reference(args):
+    """--impl reference: the oracle on all host cores; each step = one bounded sample per core."""
+    global _ORACLE
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    O, gm, om, Qo, D, n = _oracle_setup()
-    rng = np.random.default_rng(1)
-    for i in range(args.warmup):
-        _oracle_sample(O, gm, om, Qo, D, n, rng, step=i)
-    t0 = time.perf_counter()
-    upd = 0
-    for i in range(args.steps):
-        upd += _oracle_sample(O, gm, om, Qo, D, n, rng, step=args.warmup + i)
-    dt = time.perf_counter() - t0
+    _ORACLE = _oracle_setup()
+    pool, cores = _oracle_pool()
+    try:
+        for i in range(args.warmup):
+            pool.map(_oracle_worker, [(10000 * (i + 1) + c, 0.0, 1) for c in range(cores)])
+        t0 = time.perf_counter()
+        upd = 0
+        for i in range(args.steps):
+            res = pool.map(_oracle_worker, [(10000 * (args.warmup + i + 1) + c, 0.0, 1) for c in range(cores)])
+            upd += sum(r[0] for r in res)
+        dt = time.perf_counter() - t0
+    finally:
+        pool.close()
+        pool.join()
     v = upd / dt
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * dt / max(1, args.steps), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": config_json(1, {"step": "one bounded sample: a random level-3 V-node subtree of the C4 tree"}),
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"{args.steps} level-3 subtrees of the C4 depth-4 tree, {upd} updates"},
+            "config": config_json(1, {"step": f"one bounded sample per host core: {cores} random level-3 V-node "
+                                              f"subtrees of the C4 tree"}),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{args.steps} steps x {cores} level-3 subtrees of the C4 depth-4 tree, "
+                                       f"{upd} updates"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
