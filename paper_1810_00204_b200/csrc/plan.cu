@@ -143,7 +143,8 @@ __device__ __forceinline__ int ancestral_tail(const ReduceArgs &a, int x, int k,
 // backup Q = R + gamma sum_z (f_z/n) V(z) in ascending z (Alg. 6 with gamma, R13).
 template <uint32_t MASK, bool LEAF>
 __host__ __device__ constexpr int reduce_smem_doubles(int pstride) {
-    return pstride + 8 + (LEAF ? mask_count(MASK) * 32 * mask_count(MASK) : 0);
+    // band sums, blocked-mass totals, per-warp S / numerators (leaf), per-warp CDF (16 warps max)
+    return pstride + 8 + (LEAF ? mask_count(MASK) * 32 * mask_count(MASK) : 0) + 16 * 16;
 }
 
 // Executed by a whole CTA of nthreads (a multiple of 32) for parent w; warp j handles actions
@@ -237,13 +238,17 @@ __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int
         const double m = __shfl_sync(0xffffffffu, Ms, s);
         if (lane < 16) Pz += a.O64[s * 16 + lane] * m;
     }
-    double C[16];
+    // ascending-z CDF in fp64, summed sequentially (A.5); kept in shared memory (16 doubles per
+    // warp) rather than 32 registers per lane, which spilled under the kernel's register bound
+    double *C = rsm + a.pstride + 8 + (LEAF ? NA * 32 * NA : 0) + 16 * warp;
     double acc = 0.0;
+    __syncwarp();                              // the previous action's draws are done with C
 #pragma unroll
     for (int z = 0; z < 16; ++z) {
         acc += __shfl_sync(0xffffffffu, Pz, z);
-        C[z] = acc;
+        if (lane == 0) C[z] = acc;
     }
+    __syncwarp();
     // S3: n draws keyed by the tree path (Appendix A.2-A.5)
     const int level = a.level >= 0 ? a.level : path_level(vpath);   // level < 0: from the path
     const uint64_t qpath = vpath | ((uint64_t)(k + 1) << (8 * level));
