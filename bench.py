@@ -341,6 +341,19 @@ def main():
     if os.path.exists(tpath) and CFG_NAME == "C4":
         t = json.load(open(tpath))
         traffic = t["dram_bytes_read"] + t["dram_bytes_write"]
+    # ---- the HBM-bound belief kernel (k_correct, S4: child beliefs written once; north star: >= 60%
+    # of HBM bandwidth in the belief kernels): algorithmic bytes = 4 * cells per child written
+    # (parent reads come through L2), all its launches in the timed region
+    corr_ms = prof["ms"]["correct"]
+    corr_bytes = 4.0 * prof["correct_cells_written"]
+    corr_gbs = corr_bytes / (corr_ms / 1e3) / 1e9 if corr_ms > 0 else 0.0
+    peaks = {}
+    ppath = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(ppath):
+        peaks = json.load(open(ppath))
+    copy_peak = float(peaks.get("hbm_gbs", 6549.1))
+    wpath = os.path.join(ROOT, "profiles", "r01_hbm_write_peak.json")
+    write_peak = json.load(open(wpath))["write_fill"]["GBps"] if os.path.exists(wpath) else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -355,6 +368,15 @@ def main():
                                     f"{prof['leaf_cells'] / leaf_launches:.3e} per launch; "
                                     "peak = 148 SM x 128 FP32 lanes x 2 x 1965 MHz (guide unit counts)",
                      "avg_launch_ms": leaf_ms / leaf_launches},
+        "roofline_hbm": {"bound": "hbm", "kernel": "k_correct (S4 Bayes correction, child beliefs written)",
+                         "achieved": corr_gbs, "peak": copy_peak, "unit": "GB/s",
+                         "frac": corr_gbs / copy_peak if copy_peak else None,
+                         "frac_of_write_peak": (corr_gbs / write_peak) if write_peak else None,
+                         "frac_of_8tbs": corr_gbs / 8000.0,
+                         "algorithmic": f"4 B x {prof['correct_cells_written'] / max(1, prof['launches']['correct']):.3e}"
+                                        " child cells written per launch (parents via L2); peak = MEASURED_PEAKS "
+                                        "hbm_gbs (copy), also vs the measured pure-write peak and 8 TB/s",
+                         "launches": prof["launches"]["correct"], "total_ms": corr_ms},
         "kernel_share": share,
         "kernel_ms": {k: round(v, 3) for k, v in prof["ms"].items()},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 4 * model.n_cells,
