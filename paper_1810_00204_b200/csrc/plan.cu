@@ -219,16 +219,23 @@ __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int
         Ms = (k == 4) ? c[0] : a.p_stay * c[0] + a.p_int * hma + a.p_lat * (hm1 + hm2);
     }
     // R(b,a) = (p_stay - 1) sum b - sum c_a b + goal terms, sum c_a b = p_stay mass + p_int E_a + p_lat (E_l1 + E_l2)
+    // goal terms G(x, a) b(x): the warp's lanes take the entries (all loads of a round in
+    // flight at once instead of one dependent chain per entry on lane 0), fixed-order tree sum
+    double gsum = 0.0;
+    if (k != 4) {
+        for (int g = lane; g < a.ngc; g += 32)
+            if (a.gc_act[g] == j)
+                gsum += a.gc_val[g] * (double)(a.goalv ? a.goalv[v * a.nf + a.gc_fidx[g]] : bp[a.gc_cell[g]]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) gsum += __shfl_xor_sync(0xffffffffu, gsum, o);
+    }
     double R = 0.0;
     if (lane == 0) {
         if (k == 4) {
             R = -2.0 * mass + 2.0 * (double)(a.goalv ? a.goalv[v * a.nf] : bp[a.goal]);
         } else {
             const double Rp = a.p_stay * mass + a.p_int * sE[da] + a.p_lat * (sE[d1] + sE[d2]);
-            R = (a.p_stay - 1.0) * mass - Rp;
-            for (int g = 0; g < a.ngc; ++g)
-                if (a.gc_act[g] == j)
-                    R += a.gc_val[g] * (double)(a.goalv ? a.goalv[v * a.nf + a.gc_fidx[g]] : bp[a.gc_cell[g]]);
+            R = (a.p_stay - 1.0) * mass - Rp + gsum;
         }
     }
     // P(z|b,a) = sum_s O[s][z] M[s]  (fixed s order)
