@@ -152,7 +152,7 @@ def test_plan_deterministic(Q):
     assert np.array_equal(t1["leafV"], t2["leafV"])
 
 
-@pytest.mark.parametrize("G", [2, 3])
+@pytest.mark.parametrize("G", [2, 3, 4, 8])
 def test_sharded_plan_matches_single_gpu_bitwise(Q, G):
     """Run the G ranks of a sharded plan step serially on one GPU: first pass collects each rank's
     zero-padded shard-level values, second pass feeds back their exact sum."""
