@@ -535,44 +535,32 @@ qvts_status build_leaf_mma(Model &m) {
         for (int w = 0; w <= kLmWarps; ++w) wr.push_back((int32_t)(band0 + nb_ch * w / kLmWarps));
     }
     L.nchunks = nch;
-    QVTS_TRY(upload(L.cs, wr));
+    QVTS_TRY(upload(L.wr, wr));
     QVTS_TRY(upload(L.offs, offs));
-    QVTS_TRY(upload(L.m8w, dmask));
+    QVTS_TRY(upload(L.dmask, dmask));
     QVTS_TRY(upload(L.cells, L.h_cells));
     return QVTS_OK;
 }
 
-// B fragments per (chunk, lane): column g = a' of Q'(y, a') = src(y, a') - qbar, hi/lo fp16 of
-// the fp64 value; the second tile (|A| = 9): column 0 = 1, column 1 = Q'(y, 8).
+// B fragments per (chunk, lane): column g = a' of Q'(y, a') = src(y, a') - qbar (|A| <= 8), as the
+// hi/lo fp16 split of the fp64 value; padding cells and columns g >= |A| are zero.
 __global__ void k_leaf_qfrag(const double *__restrict__ src64, const int32_t *__restrict__ cells, long long nchunks,
-                             int NA, int HW, double qbar, uint4 *__restrict__ qfr, uint4 *__restrict__ qfr8) {
+                             int NA, int HW, double qbar, uint4 *__restrict__ qfr) {
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= nchunks * 32) return;
     const long long ch = i >> 5;
     const int lane = (int)(i & 31), g = lane >> 2, t = lane & 3;
     const int pos[4] = {2 * t, 2 * t + 1, 2 * t + 8, 2 * t + 9};
-    uint16_t hi[4], lo[4], h8[4], l8[4];
+    uint16_t hi[4], lo[4];
     for (int e = 0; e < 4; ++e) {
         const int x = cells[ch * 16 + pos[e]];
-        double v = 0.0, v8 = 0.0;
-        if (x >= 0 && g < NA && g < 8) v = src64[(size_t)g * HW + x] - qbar;
-        if (x >= 0 && NA == 9) v8 = src64[(size_t)8 * HW + x] - qbar;
+        const double v = (x >= 0 && g < NA) ? src64[(size_t)g * HW + x] - qbar : 0.0;
         const __half h = __double2half(v);
         hi[e] = __half_as_ushort(h);
         lo[e] = __half_as_ushort(__double2half(v - (double)__half2float(h)));
-        if (g == 0) {
-            h8[e] = 0x3C00; l8[e] = 0;
-        } else if (g == 1) {
-            const __half hh = __double2half(v8);
-            h8[e] = __half_as_ushort(hh);
-            l8[e] = __half_as_ushort(__double2half(v8 - (double)__half2float(hh)));
-        } else {
-            h8[e] = 0; l8[e] = 0;
-        }
     }
     auto pk = [](uint16_t a, uint16_t b) { return (uint32_t)a | ((uint32_t)b << 16); };
     qfr[i] = make_uint4(pk(hi[0], hi[1]), pk(hi[2], hi[3]), pk(lo[0], lo[1]), pk(lo[2], lo[3]));
-    if (qfr8) qfr8[i] = make_uint4(pk(h8[0], h8[1]), pk(h8[2], h8[3]), pk(l8[0], l8[1]), pk(l8[2], l8[3]));
 }
 
 qvts_status build_leaf_qfrag(Model &m, const double *src64, double qbar, bool fib, cudaStream_t st) {
@@ -582,7 +570,7 @@ qvts_status build_leaf_qfrag(Model &m, const double *src64, double qbar, bool fi
     QVTS_TRY(q.ensure(sizeof(uint4) * 32 * L.nchunks));
     const long long n = L.nchunks * 32;
     k_leaf_qfrag<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(src64, L.cells.as<int32_t>(), L.nchunks, m.NA, m.HW, qbar,
-                                                             q.as<uint4>(), nullptr);
+                                                             q.as<uint4>());
     QVTS_CUDA(cudaGetLastError());
     return QVTS_OK;
 }
@@ -603,7 +591,7 @@ static qvts_status launch_leaf_mma_t(Model &m, const float *beliefs, long long b
     a.beliefs = beliefs; a.bstride = bstride; a.vmap = vmap; a.nwork = nwork; a.nwork_dev = nwork_dev; a.skip = skip;
     a.H = m.H; a.W = m.W; a.TP = L.TP; a.R = L.R; a.nb = L.nb; a.ptile = L.ptile;
     a.vec16 = ((m.W & 3) == 0 && (bstride & 3) == 0 && (reinterpret_cast<uintptr_t>(beliefs) & 15) == 0) ? 1 : 0;
-    a.wr = L.cs.as<int32_t>(); a.offs = L.offs.as<uint4>(); a.dmask = L.m8w.as<uint4>();
+    a.wr = L.wr.as<int32_t>(); a.offs = L.offs.as<uint4>(); a.dmask = L.dmask.as<uint4>();
     a.qfr = (m.cur_leaf == QVTS_LEAF_FIB ? L.qfr_fib : L.qfr).as<uint4>();
     a.part = m.part.as<double>(); a.pstride = pstride;
     int dev = 0, nsm = 148;

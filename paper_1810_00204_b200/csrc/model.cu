@@ -544,8 +544,7 @@ extern "C" void qvts_model_destroy(qvts_model *m) {
                       &m->pb_b0, &m->pb_B, &m->pb_G, &m->pb_Gn, &m->pb_GT, &m->pb_Bbar, &m->pb_Sc, &m->pb_Rb,
                       &m->pb_sel, &m->pb_astar, &m->pb_cand, &m->pb_misc, &m->pb_cls, &m->pb_chunks, &m->pb_part};
     for (DevBuf *b : bufs) b->release();
-    for (DevBuf *b : {&m->lm.cs, &m->lm.offs, &m->lm.m8w, &m->lm.cells, &m->lm.qfr, &m->lm.qfr8, &m->lm.qfr_fib,
-                      &m->lm.qfr8_fib})
+    for (DevBuf *b : {&m->lm.wr, &m->lm.offs, &m->lm.dmask, &m->lm.cells, &m->lm.qfr, &m->lm.qfr_fib})
         b->release();
     for (BandSet *bs : {&m->band_big, &m->band_small}) {
         bs->bands.release(); bs->entries.release(); bs->slot_cell.release(); bs->qlist.release(); bs->qlist_fib.release();

@@ -65,7 +65,11 @@ struct LeafMma {
     long long nchunks = 0;
     std::vector<int32_t> h_cs;       // [nb][17] chunk ranges per class (host only)
     std::vector<int32_t> h_cells;    // [nchunks][16] cell of each K position (-1 = padding)
-    DevBuf cs /* [nb][5] warp chunk ranges */, offs, m8w /* diagonal masks */, cells, qfr, qfr8, qfr_fib, qfr8_fib;
+    DevBuf wr;                       // [nb][5] chunk range of each warp quarter in the band
+    DevBuf offs;                     // [nchunks][4] uint4: byte offsets of a lane's 4 cells, class << 28
+    DevBuf dmask;                    // [nchunks][4] uint4: per diagonal, byte e = 0x80 if occ(cell e + d_k)
+    DevBuf cells;                    // [nchunks][16] (h_cells on the device, for the fragment build)
+    DevBuf qfr, qfr_fib;             // [nchunks][32] uint4 B fragments of Q' (Q_MDP / FIB leaves)
 };
 
 // Per-level node arrays of the level-batched tree (SoA).
