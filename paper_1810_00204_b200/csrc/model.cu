@@ -565,6 +565,10 @@ extern "C" void qvts_model_destroy(qvts_model *m) {
     if (m->bf_gexec) cudaGraphExecDestroy(m->bf_gexec);
     if (m->pg_exec) cudaGraphExecDestroy(m->pg_exec);
     if (m->pg_stream) cudaStreamDestroy(m->pg_stream);
+    if (m->ov_corr) cudaStreamDestroy(m->ov_corr);
+    if (m->ov_leaf) cudaStreamDestroy(m->ov_leaf);
+    for (cudaEvent_t e : m->ov_ev)
+        if (e) cudaEventDestroy(e);
     if (m->pg_join) cudaEventDestroy(m->pg_join);
     m->lvl_cnt.release();
     m->root_buf.release();

@@ -489,6 +489,7 @@ struct CorrectArgs {
     const int32_t *skip = nullptr;             // device flag (best-first)
     const long long *cbase_dev = nullptr;      // device child-index base (best-first pool)
     const long long *nwork_dev = nullptr;      // device-side parent count (graph-captured plan step)
+    long long q0 = 0;                          // first Q-node of this launch (chunked launches)
     int stage_tp = 0;                          // > 0: the CTA's parent rows (+ halo) are staged in shared
                                                // memory with this row pitch (correct_stage)
 };
@@ -948,7 +949,7 @@ __global__ void __launch_bounds__(256) k_correct(CorrectArgs a) {
     if (a.skip && *a.skip) return;
     const long long grp = blockIdx.x / a.ntiles;
     if (a.nwork_dev && !a.sel_q && grp >= *a.nwork_dev * NA) return;
-    const long long q = a.sel_q ? (long long)a.sel_q[grp] : (a.qsel >= 0 ? a.qsel : grp);
+    const long long q = a.sel_q ? (long long)a.sel_q[grp] : (a.qsel >= 0 ? a.qsel : a.q0 + grp);
     const int tile = blockIdx.x % a.ntiles;
     const long long w = q / NA;
     const int j = (int)(q % NA);
@@ -1213,7 +1214,7 @@ static qvts_status launch_hist(Model &m, const BandSet &bs, const float *beliefs
                                const int32_t *vmap, long long nwork, int pstride, cudaStream_t st, int *nb_eff,
                                const ReduceArgs *red = nullptr, bool *fused_out = nullptr,
                                const int32_t *skip = nullptr, const FusedLeaf *fl = nullptr,
-                               const long long *nwork_dev = nullptr) {
+                               const long long *nwork_dev = nullptr, long long part_off = 0) {
     constexpr int NOUT = 16 * hist_cb<MASK, LEAF>() + 8;
     HistArgs a;
     a.skip = skip;
@@ -1238,7 +1239,7 @@ static qvts_status launch_hist(Model &m, const BandSet &bs, const float *beliefs
         return ev ? std::atoi(ev) : 0;
     }();
     a.cluster = (use_cluster && bs.nb <= 8 && !nwork_dev) ? 1 : 0;
-    a.part = m.part.as<double>(); a.pstride = pstride;
+    a.part = m.part.as<double>() + part_off; a.pstride = pstride;
     // fused reduce (the last band CTA of each pair runs reduce_parent): measured slower than a
     // separate k_reduce launch, so off unless QVTS_FUSED_REDUCE=1
     static const int use_fused = [] {
@@ -1306,6 +1307,122 @@ static int pstride_of(bool leaf) {
     return 16 * (leaf ? hist_cb<MASK, true>() : hist_cb<MASK, false>()) + 8;
 }
 
+// The last transition of a plan step with the leaf level pipelined behind it: the Q-nodes of level
+// D-2 are cut into chunks of about equal child counts; chunk i's k_correct (HBM-write bound, on a
+// high-priority stream) overlaps the leaf k_hist + k_reduce of chunk i-1's children (FP32-ALU
+// bound, second stream).  Same kernels and arithmetic per parent, so every value is bit-identical
+// to the unchunked sequence.  Sets up m.ql[D-1] / m.vl[D-1] as the leaf iteration would.
+// Opt-in (QVTS_LEAF_OVERLAP=<chunks>): measured no gain at C4 (55.5 ms off; 55.7 / 56.0 / 56.4 ms with
+// 4 / 8 / 16 chunks) -- the leaf k_hist's two CTAs per SM hold the whole register file, so k_correct
+// CTAs cannot co-reside and the two only interleave.
+static int leaf_overlap_chunks(long long nleaf) {
+    static const int env = [] {
+        const char *ev = std::getenv("QVTS_LEAF_OVERLAP");
+        return ev ? std::atoi(ev) : 0;
+    }();
+    if (env <= 1 || nleaf < 64LL * env) return 0;
+    return env;
+}
+
+template <uint32_t MASK>
+static qvts_status leaf_overlap(Model &m, const CorrectArgs &c0, long long nq, long long total, int D, int n,
+                                const qvts_plan_cfg &cfg, const RootBatch &roots, bool trace, int nch,
+                                cudaStream_t st) {
+    constexpr int NA = mask_count(MASK);
+    const int dl = D - 1;
+    VLevel &vl = m.vl[dl];
+    QLevel &ql = m.ql[dl];
+    // child offsets on the host (the stream was synchronised for the child count)
+    std::vector<int32_t> off((size_t)nq);
+    QVTS_CUDA(cudaMemcpy(off.data(), m.ql[dl - 1].off.p, sizeof(int32_t) * nq, cudaMemcpyDeviceToHost));
+    std::vector<long long> qb{0}, wb{0};
+    for (int i = 1; i < nch; ++i) {
+        const long long target = total * i / nch;
+        long long q = qb.back();
+        while (q < nq && off[(size_t)q] < target) ++q;
+        if (q > qb.back() && q < nq) { qb.push_back(q); wb.push_back(off[(size_t)q]); }
+    }
+    qb.push_back(nq);
+    wb.push_back(total);
+    // the leaf level's arrays, as the leaf iteration of plan_levels_t allocates them
+    const long long nwork = total, nql = nwork * NA;
+    ql.nwork = nwork; ql.mapped = false; ql.vmap_ptr = nullptr;
+    QVTS_TRY(ql.R.ensure(sizeof(double) * std::max(1LL, nql)));
+    QVTS_TRY(ql.P.ensure(sizeof(double) * 16 * std::max(1LL, nql)));
+    QVTS_TRY(ql.cnt.ensure(sizeof(uint16_t) * 16 * std::max(1LL, nql)));
+    QVTS_TRY(ql.umask.ensure(sizeof(uint16_t) * std::max(1LL, nql)));
+    QVTS_TRY(ql.U.ensure(sizeof(int32_t) * std::max(1LL, nql)));
+    QVTS_TRY(ql.off.ensure(sizeof(int32_t) * std::max(1LL, nql)));
+    QVTS_TRY(ql.Q.ensure(sizeof(double) * std::max(1LL, nql)));
+    if (trace) {
+        QVTS_TRY(ql.zdraw.ensure((size_t)std::max(1LL, nql) * n));
+        QVTS_TRY(ql.leafV.ensure(sizeof(double) * 16 * std::max(1LL, nql)));
+    }
+    double expect = 1.0;
+    for (int i = 0; i < dl; ++i) expect *= 10.0;
+    const BandSet &bs = expect < 100.0 ? m.band_small : m.band_big;
+    const int pstride = pstride_of<MASK>(true);
+    QVTS_TRY(m.part.ensure(sizeof(double) * (size_t)(nwork + 1) * std::max(bs.nb, leaf_mma_records()) * pstride));
+    // streams: k_correct chunks at high priority, leaf chunks at normal priority, both after st
+    if (!m.ov_corr) {
+        int lo = 0, hi = 0;
+        QVTS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        QVTS_CUDA(cudaStreamCreateWithPriority(&m.ov_corr, cudaStreamNonBlocking, hi));
+        QVTS_CUDA(cudaStreamCreateWithFlags(&m.ov_leaf, cudaStreamNonBlocking));
+        for (auto &e : m.ov_ev) QVTS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const int nc = (int)qb.size() - 1;
+    if (nc + 2 > (int)(sizeof(m.ov_ev) / sizeof(m.ov_ev[0]))) { set_error("too many overlap chunks"); return QVTS_ERR_INVALID_ARG; }
+    QVTS_CUDA(cudaEventRecord(m.ov_ev[0], st));
+    QVTS_CUDA(cudaStreamWaitEvent(m.ov_corr, m.ov_ev[0], 0));
+    QVTS_CUDA(cudaStreamWaitEvent(m.ov_leaf, m.ov_ev[0], 0));
+    CorrectArgs c = c0;
+    const size_t csm = correct_stage(c);
+    for (int i = 0; i < nc; ++i) {
+        c.q0 = qb[i];
+        const long long nblocks = (qb[i + 1] - qb[i]) * c.ntiles;
+        cudaEvent_t e;
+        prof_begin(m, 5, m.ov_corr, &e);
+        k_correct<MASK><<<(unsigned)nblocks, 256, csm, m.ov_corr>>>(c);
+        prof_end(m, 5, m.ov_corr, e);
+        QVTS_CUDA(cudaGetLastError());
+        QVTS_CUDA(cudaEventRecord(m.ov_ev[2 + i], m.ov_corr));
+    }
+    m.pstat.correct_cells_written += total * (long long)m.HW;
+    for (int i = 0; i < nc; ++i) {
+        QVTS_CUDA(cudaStreamWaitEvent(m.ov_leaf, m.ov_ev[2 + i], 0));
+        const long long w0 = wb[i], cnt = wb[i + 1] - wb[i];
+        if (cnt <= 0) continue;
+        const float *bel = vl.belief.as<float>() + w0 * m.HWp;
+        int nb_eff = bs.nb;
+        QVTS_TRY((launch_hist<MASK, true>(m, bs, bel, m.HWp, nullptr, cnt, pstride, m.ov_leaf, &nb_eff, nullptr, nullptr,
+                                          nullptr, nullptr, nullptr, w0 * bs.nb * (long long)pstride)));
+        ReduceArgs r;
+        r.part = m.part.as<double>() + w0 * bs.nb * (long long)pstride; r.pstride = pstride; r.nb = nb_eff;
+        r.nwork = cnt; r.vmap = nullptr;
+        r.beliefs = bel; r.bstride = m.HWp; r.vpath = vl.path.as<uint64_t>() + w0; r.vroot = vl.root.as<int32_t>() + w0;
+        r.root_step = roots.step_dev; r.root_ep = roots.episode_dev; r.seed = cfg.seed;
+        r.level = dl; r.n = n; r.O64 = m.d_O64.as<double>();
+        r.ngc = m.ngc; r.gc_cell = m.d_gc_cell.as<int32_t>(); r.gc_act = m.d_gc_act.as<int32_t>();
+        r.gc_val = m.d_gc_val.as<double>(); r.goal = m.goal;
+        r.p_stay = m.p_stay; r.p_int = m.p_int; r.p_lat = m.p_lat; r.gamma = m.gamma;
+        r.qbar = m.cur_leaf == QVTS_LEAF_FIB ? m.qbar_fib : m.qbar;
+        const long long q0 = w0 * NA;
+        r.R = ql.R.as<double>() + q0; r.P = ql.P.as<double>() + 16 * q0; r.cnt = ql.cnt.as<uint16_t>() + 16 * q0;
+        r.umask = ql.umask.as<uint16_t>() + q0; r.U = ql.U.as<int32_t>() + q0;
+        r.zdraw = trace ? ql.zdraw.as<uint8_t>() + q0 * n : nullptr;
+        r.Q = ql.Q.as<double>() + q0; r.leafV = trace ? ql.leafV.as<double>() + 16 * q0 : nullptr;
+        r.counters = m.counters.as<unsigned long long>();
+        r.xs = nullptr; r.m8 = m.d_m8.as<uint8_t>(); r.sig = m.d_sig.as<uint8_t>(); r.W = m.W; r.acc = m.acc;
+        QVTS_TRY((launch_reduce<MASK, true>(m, r, m.ov_leaf)));
+    }
+    QVTS_CUDA(cudaEventRecord(m.ov_ev[1], m.ov_leaf));
+    QVTS_CUDA(cudaStreamWaitEvent(st, m.ov_ev[1], 0));
+    QVTS_CUDA(cudaEventRecord(m.ov_ev[0], m.ov_corr));
+    QVTS_CUDA(cudaStreamWaitEvent(st, m.ov_ev[0], 0));
+    return QVTS_OK;
+}
+
 template <uint32_t MASK>
 static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_plan_cfg &cfg, const qvts_comm *comm,
                                  cudaStream_t st, long long *nv_out) {
@@ -1335,6 +1452,7 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
     const char *ev_fused = std::getenv("QVTS_FUSED_LEAF");
     const int env_fused = ev_fused ? std::atoi(ev_fused) : 0;
     const bool fuse = env_fused && D >= 2 && !trace && cfg.sampler == QVTS_SAMPLER_MARGINAL;
+    bool leaf_done = false;                     // the leaf level ran inside leaf_overlap
 
     for (int d = 0; d < D; ++d) {
         const bool leaf = (d == D - 1);
@@ -1454,6 +1572,13 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
         QVTS_TRY(vc.root.ensure(sizeof(int32_t) * tn));
         QVTS_TRY(vc.V.ensure(sizeof(double) * tn));
         const bool meta_only = fuse && d + 1 == D - 1;   // leaf parents: metadata + goal-term cells only
+        // pipeline the leaf level behind this k_correct (leaf_overlap): not when the leaf level
+        // would become the shard level (its parents then need a rank map), nor for the options
+        // that need the whole level at once (ancestral draws, tensor-core leaf, fused leaf)
+        const bool leaf_sharded = G > 1 && shard_level < 0 && total >= shard_min;
+        const int overlap_nch = (d + 1 == D - 1 && !meta_only && !leaf_sharded &&
+                                 cfg.sampler == QVTS_SAMPLER_MARGINAL && !leaf_mma_enabled(m, m.HWp, nullptr))
+                                    ? leaf_overlap_chunks(total) : 0;
         if (meta_only) QVTS_TRY(m.fl_goalv.ensure(sizeof(float) * (size_t)tn * std::max(1, m.nfcells)));
         else QVTS_TRY(vc.belief.ensure(sizeof(float) * (size_t)tn * m.HWp));
         if (nq > 0) {
@@ -1476,6 +1601,9 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
             if (meta_only) {
                 QVTS_PROF(5, k_child_meta<MASK><<<nblk(nq * 16, 256), 256, 0, st>>>(c, nq, m.d_fcells.as<int32_t>(),
                                                                                  m.nfcells, m.fl_goalv.as<float>()));
+            } else if (overlap_nch) {
+                QVTS_TRY(leaf_overlap<MASK>(m, c, nq, total, D, n, cfg, roots, trace, overlap_nch, st));
+                leaf_done = true;
             } else {
                 { const size_t csm_ = correct_stage(c);
                 QVTS_PROF(5, k_correct<MASK><<<(unsigned)nblocks, 256, csm_, st>>>(c)); }
@@ -1483,6 +1611,7 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
             }
             QVTS_CUDA(cudaGetLastError());
         }
+        if (leaf_done) break;
     }
     // S6 backup, bottom-up
     for (int d = D - 1; d >= 0; --d) {

@@ -122,6 +122,9 @@ struct Model {
     cudaStream_t pg_stream = nullptr;
     cudaEvent_t pg_join = nullptr;
     cudaGraphExec_t pg_exec = nullptr;
+    // leaf level pipelined behind the last k_correct (plan.cu leaf_overlap)
+    cudaStream_t ov_corr = nullptr, ov_leaf = nullptr;
+    cudaEvent_t ov_ev[40] = {};
     std::vector<uintptr_t> pg_key;
     // instrumentation
     bool prof = false;

@@ -594,3 +594,29 @@ def test_leaf_mma_matches_scalar_leaf_and_oracle(Q, name, depth, n, monkeypatch)
     assert np.max(np.abs(out["1"][0] - out["0"][0])) <= PT.TOL
     ro = o.plan(Qo, b32.astype(np.float64), depth, n, seed=4, step=1)
     assert np.max(np.abs(out["1"][0] - ro.qroot)) <= PT.TOL * 10
+
+
+@pytest.mark.parametrize("nch", ["4", "16"])
+def test_leaf_overlap_chunks_bit_identical(Q, nch, monkeypatch):
+    """The leaf level pipelined behind the last k_correct in chunks (QVTS_LEAF_OVERLAP) gives the
+    same root Q bits, level counts and action as the unchunked level-synchronous path."""
+    gm = W.CONFIGS["C3"]["map"]()
+    g, o, Qo, _, _ = pair(Q, gm, W.A8)
+    b32 = np.asarray(W.random_belief(gm, 17), np.float32)
+    monkeypatch.setenv("QVTS_PLAN_GRAPH", "0")
+    ref = g.plan_step(dev(b32), 3, 8, seed=3, step=4)
+    import subprocess, sys, json, os
+    code = (
+        "import numpy as np, torch, json, sys; sys.path.insert(0, %r)\n"
+        "import workloads as W; from paper_1810_00204_b200 import qvts as Q\n"
+        "gm = W.CONFIGS['C3']['map'](); g = Q.Model(gm, action_mask=W.A8); g.value_iteration(1e-9)\n"
+        "b = torch.tensor(np.asarray(W.random_belief(gm, 17), np.float32), device='cuda')\n"
+        "r = g.plan_step(b, 3, 8, seed=3, step=4)\n"
+        "print(json.dumps([list(map(float.hex, r.q_root[:g.n_actions])), list(r.n_vnodes[:4]), r.action]))\n"
+    ) % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, QVTS_PLAN_GRAPH="0", QVTS_LEAF_OVERLAP=nch)
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    qh, nv, act = json.loads(out.stdout.strip().splitlines()[-1])
+    assert qh == [float(x).hex() for x in ref.q_root[:g.n_actions]]
+    assert nv == list(ref.n_vnodes[:4]) and act == ref.action
