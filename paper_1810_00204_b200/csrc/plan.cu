@@ -157,28 +157,23 @@ __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int
     double *sp = rsm;                          // [pstride] band-summed partials
     double *sE = rsm + a.pstride;              // [8] blocked-mass totals
     const double *pp = a.part + w * a.nb * (long long)a.pstride;
-    // band sum, fixed band order; two elements per pass with all their band loads in flight
-    for (int i0 = threadIdx.x; i0 < a.pstride; i0 += 2 * nthreads) {
-        const int i1 = i0 + nthreads;
-        const bool has1 = i1 < a.pstride;
+    // band sum, fixed band order (sequential over bands, as before); a thread takes two adjacent
+    // elements per pass as one 16-byte load per band (pstride is even), 4 bands in flight
+    const double2 *pp2 = reinterpret_cast<const double2 *>(pp);
+    const int half = a.pstride >> 1;
+    for (int i = threadIdx.x; i < half; i += nthreads) {
         double acc0 = 0.0, acc1 = 0.0;
-        int bd = 0;
-        for (; bd + 4 <= a.nb; bd += 4) {
-            double x[4], y[4];
+        for (int bd = 0; bd < a.nb; bd += 4) {
+            double2 x[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                x[u] = pp[(long long)(bd + u) * a.pstride + i0];
-                y[u] = has1 ? pp[(long long)(bd + u) * a.pstride + i1] : 0.0;
-            }
+            for (int u = 0; u < 4; ++u)
+                if (bd + u < a.nb) x[u] = pp2[(long long)(bd + u) * half + i];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) { acc0 += x[u]; acc1 += y[u]; }
+            for (int u = 0; u < 4; ++u)
+                if (bd + u < a.nb) { acc0 += x[u].x; acc1 += x[u].y; }
         }
-        for (; bd < a.nb; ++bd) {
-            acc0 += pp[(long long)bd * a.pstride + i0];
-            if (has1) acc1 += pp[(long long)bd * a.pstride + i1];
-        }
-        sp[i0] = acc0;
-        if (has1) sp[i1] = acc1;
+        sp[2 * i] = acc0;
+        sp[2 * i + 1] = acc1;
     }
     __syncthreads();
     // E[d] = sum_y occ(y + d) b(y); orthogonal directions come from the class masses (signature bit)
