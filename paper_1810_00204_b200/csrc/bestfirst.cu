@@ -507,6 +507,7 @@ using namespace qvts;
 
 extern "C" qvts_status qvts_plan_best_first(qvts_model *m, const float *root_dev, const qvts_bf_cfg *cfg,
                                             qvts_bf_result *res, void *stream) {
+    qvts::NvtxRange nvtx_range__("qvts_plan_best_first");
     if (!m || !cfg || !res) { set_error("NULL argument"); return QVTS_ERR_INVALID_ARG; }
     if (cfg->n_samples < 1 || cfg->n_samples > 4096 || cfg->max_expansions < 0 || cfg->max_depth < 1 ||
         cfg->max_depth > 8 || !(cfg->gap_tol >= 0.0) ||
@@ -740,6 +741,7 @@ extern "C" qvts_status qvts_trace_best_first(const qvts_model *m, int64_t *n_v, 
 }
 
 extern "C" qvts_status qvts_bf_advance(qvts_model *m, int32_t action, int32_t z, int32_t *reused, void *stream) {
+    qvts::NvtxRange nvtx_range__("qvts_bf_advance");
     if (!m || !reused) { set_error("NULL argument"); return QVTS_ERR_INVALID_ARG; }
     *reused = 0;
     if (!m->bf_valid) { set_error("qvts_plan_best_first has not run"); return QVTS_ERR_STATE; }

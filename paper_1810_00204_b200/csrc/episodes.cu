@@ -332,6 +332,7 @@ using namespace qvts;
 
 extern "C" qvts_status qvts_run_episodes(qvts_model *m, const qvts_episode_cfg *cfg, const qvts_comm *comm,
                                          qvts_episode_record *out_host, void *stream) {
+    qvts::NvtxRange nvtx_range__("qvts_run_episodes");
     if (!m || !cfg || !out_host || cfg->n_episodes < 0 || cfg->max_steps < 1 || cfg->stop_patience < 0 ||
         cfg->planner < 0 || cfg->planner > 2) {
         set_error("bad run_episodes arguments");

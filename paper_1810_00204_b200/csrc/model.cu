@@ -611,6 +611,7 @@ extern "C" qvts_status qvts_model_tables(const qvts_model *m, float *R_host, uin
 
 extern "C" qvts_status qvts_value_iteration(qvts_model *m, double eps, int32_t max_sweeps, int32_t *sweeps_out,
                                             double *residual_out, void *stream) {
+    qvts::NvtxRange nvtx_range__("qvts_value_iteration");
     if (!m || !(eps > 0) || max_sweeps <= 0) { set_error("bad value_iteration arguments"); return QVTS_ERR_INVALID_ARG; }
     QVTS_CUDA(cudaSetDevice(m->device));
     cudaStream_t st = (cudaStream_t)stream;
@@ -678,6 +679,7 @@ extern "C" qvts_status qvts_value_iteration(qvts_model *m, double eps, int32_t m
 
 extern "C" qvts_status qvts_fib_iteration(qvts_model *m, double eps, int32_t max_sweeps, int32_t *sweeps_out,
                                           double *residual_out, void *stream) {
+    qvts::NvtxRange nvtx_range__("qvts_fib_iteration");
     if (!m || !(eps > 0) || max_sweeps <= 0) { set_error("bad fib_iteration arguments"); return QVTS_ERR_INVALID_ARG; }
     QVTS_CUDA(cudaSetDevice(m->device));
     cudaStream_t st = (cudaStream_t)stream;

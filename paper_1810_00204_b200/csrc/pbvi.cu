@@ -498,6 +498,7 @@ using namespace qvts;
 
 extern "C" qvts_status qvts_pbvi(qvts_model *m, const float *b0_dev, int32_t expansions, int32_t max_points,
                                  uint32_t seed, int32_t sweeps, int32_t *n_points_out, void *stream) {
+    qvts::NvtxRange nvtx_range__("qvts_pbvi");
     if (!m || expansions < 0 || max_points < 1 || max_points > 1024 || sweeps < 0) {
         set_error("bad pbvi arguments");
         return QVTS_ERR_INVALID_ARG;

@@ -1449,7 +1449,11 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
     const bool fuse = env_fused && D >= 2 && !trace && cfg.sampler == QVTS_SAMPLER_MARGINAL;
     bool leaf_done = false;                     // the leaf level ran inside leaf_overlap
 
+    static const char *const kLevelNames[kMaxLevels] = {"qvts level 0", "qvts level 1", "qvts level 2",
+                                                         "qvts level 3", "qvts level 4", "qvts level 5",
+                                                         "qvts level 6", "qvts level 7", "qvts level 8"};
     for (int d = 0; d < D; ++d) {
+        NvtxRange nvtx_level(kLevelNames[d < kMaxLevels ? d : kMaxLevels - 1]);
         const bool leaf = (d == D - 1);
         VLevel &vl = m.vl[d];
         QLevel &ql = m.ql[d];
@@ -2159,6 +2163,7 @@ using namespace qvts;
 
 extern "C" qvts_status qvts_plan_step(qvts_model *m, const float *root_dev, const qvts_plan_cfg *cfg,
                                       const qvts_comm *comm, qvts_plan_result *res, void *stream) {
+    qvts::NvtxRange nvtx_range__("qvts_plan_step");
     if (!m || !root_dev || !cfg || !res) { set_error("NULL argument"); return QVTS_ERR_INVALID_ARG; }
     if (cfg->depth < 1 || cfg->depth > 8 || cfg->n_samples < 1 || cfg->n_samples > 4096) {
         set_error("depth must be 1..8 and n_samples 1..4096"); return QVTS_ERR_INVALID_ARG;
@@ -2219,6 +2224,7 @@ extern "C" qvts_status qvts_plan_step(qvts_model *m, const float *root_dev, cons
 
 extern "C" qvts_status qvts_belief_update(qvts_model *m, const float *b_dev, int32_t action, int32_t z,
                                           float *out_dev, double *p_obs_out, void *stream) {
+    qvts::NvtxRange nvtx_range__("qvts_belief_update");
     if (!m || !b_dev || !out_dev) { set_error("NULL argument"); return QVTS_ERR_INVALID_ARG; }
     int j = -1;
     for (int i = 0; i < m->NA; ++i) if (m->action_id[i] == action) j = i;
@@ -2393,6 +2399,7 @@ __global__ void k_gather_p(const double *__restrict__ P, const int32_t *__restri
 extern "C" qvts_status qvts_belief_update_batch(qvts_model *m, const float *b_dev, int64_t b_stride, int32_t n,
                                                 const int32_t *actions, const int32_t *zs, float *out_dev,
                                                 int64_t out_stride, double *p_obs_out, void *stream) {
+    qvts::NvtxRange nvtx_range__("qvts_belief_update_batch");
     if (!m || (n > 0 && (!b_dev || !actions || !zs || !out_dev))) { set_error("NULL argument"); return QVTS_ERR_INVALID_ARG; }
     if (n < 0 || b_stride < m->HW || out_stride < m->HW) { set_error("bad n or stride"); return QVTS_ERR_INVALID_ARG; }
     if (n == 0) return QVTS_OK;

@@ -8,7 +8,18 @@
 
 #include "../../include/qvts.h"
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace qvts {
+
+// NVTX range for the duration of a scope (ABI entry points, plan-step levels): visible in Nsight
+// Systems / Compute timelines, a no-op without an attached tool (SURVEY §5 tracing)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 constexpr int kHistThreads = 128;   // slot-threads per band list (one class stream per slot-thread)
 constexpr int kPairThreads = 256;   // hist CTA: 2 parents x 128 slot-threads
