@@ -17,7 +17,7 @@ MUTANTS = [
     ("S4: correct without the 1/P(z) normaliser", "plan.cu",
      "s_w[u][sg] = (float)(a.O64[sg * 16 + z] / a.P[q * 16 + z]);", "s_w[u][sg] = (float)(a.O64[sg * 16 + z]);"),
     ("S3: Philox key halves swapped", "plan.cu", "make_uint2(a.seed, ep));", "make_uint2(ep, a.seed));"),
-    ("S6: gamma dropped in the backup", "plan.cu", "const double qv = R[q] + gamma * acc;", "const double qv = R[q] + acc;"),
+    ("S6: gamma dropped in the backup", "plan.cu", "qv = R[q] + gamma * acc;", "qv = R[q] + acc;"),
     ("S1: lateral ring neighbour off by one", "stencil.cuh", "return ring_at((ring_pos(k) + 7) % 8);",
      "return ring_at((ring_pos(k) + 6) % 8);"),
     ("S1/S2: diagonal blocked mass not kept at y", "plan.cu", "                h += b0;\n", "\n"),
@@ -27,14 +27,19 @@ MUTANTS = [
      "    return R64[(size_t)j * HW + x] + s;\n}"),
     ("NEXT-2: PBVI alpha* by the first instead of the best vector", "pbvi.cu", "if (k == 0 || pb_beats(v, bz)) { bz = v; bk = k; }",
      "if (k == 0) { bz = v; bk = k; }"),
-    ("S2: R(b,a) identity with p_stay instead of p_stay - 1", "plan.cu", "R = (a.p_stay - 1.0) * mass - Rp;",
-     "R = a.p_stay * mass - Rp;"),
+    ("S2: R(b,a) identity with p_stay instead of p_stay - 1", "plan.cu", "R = (a.p_stay - 1.0) * mass - Rp + gsum;",
+     "R = a.p_stay * mass - Rp + gsum;"),
+    ("S4 (staged k_correct): left neighbour read from the cell itself", "plan.cu", "nbh[dr][0] = row[-1];",
+     "nbh[dr][0] = row[0];"),
+    ("S2 (k_reduce band sum): second element of a pair summed from the first", "plan.cu",
+     "if (bd + u < a.nb) { acc0 += x[u].x; acc1 += x[u].y; }", "if (bd + u < a.nb) { acc0 += x[u].x; acc1 += x[u].x; }"),
     ("S5: leaf offset qbar not added back", "plan.cu", "Vz = a.qbar + Vz / Pexact;", "Vz = Vz / Pexact;"),
     ("best-first Alg. 7: heuristic child by H instead of U", "bestfirst.cu", "if (U[j] > U[bq]) bq = j;",
      "if (H[j] > H[bq]) bq = j;"),
 ]
 SUBSET = ("test_tables_and_value_iteration or test_belief_update or test_plan_C1_full_tree or "
-          "test_plan_ragged_depth3 or test_best_first_against_oracle or test_pbvi_against_oracle")
+          "test_plan_ragged_depth3 or test_plan_C3_full or test_best_first_against_oracle or "
+          "test_pbvi_against_oracle")   # C3 (W = 128) runs the staged k_correct path
 
 
 def build():
