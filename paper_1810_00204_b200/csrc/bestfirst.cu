@@ -659,6 +659,15 @@ extern "C" qvts_status qvts_plan_best_first(qvts_model *m, const float *root_dev
             for (size_t i = 0; i < arrs.size(); ++i) key[i] = (uintptr_t)arrs[i].first->p;
             key[arrs.size()] = (uintptr_t)m->bf_bel.p;
             if (key != m->bf_gkey) gexec = nullptr;
+            // a growth (reallocation, copy) and the graph recapture it forces can take tens of
+            // milliseconds: re-check the wall-clock budget before spending them on another chunk
+            if (cfg->time_budget_ms > 0.0 &&
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count() >=
+                    cfg->time_budget_ms) {
+                hs.done = 1;
+                hs.stop = QVTS_BF_TIME;
+                break;
+            }
         }
         if (direct) {
             for (int i = 0; i < chunk; ++i) QVTS_TRY(bf_one_expansion(*m, g, S, *cfg, st));
