@@ -954,7 +954,9 @@ __global__ void __launch_bounds__(256) k_correct(CorrectArgs a) {
     const int U = __popc(um);
     const long long base = (a.sel_q ? (long long)a.sel_out[grp] : (a.qsel >= 0 ? 0 : a.off[q])) +
                            (a.cbase_dev ? *a.cbase_dev : 0);
-    __shared__ float s_w[16][16];   // [rank u][signature s] = O[s][z_u] / P(z_u)
+    // [signature s][rank u] = O[s][z_u] / P(z_u); row pitch 18 so the 16 rows sit in distinct
+    // bank pairs and a cell reads two children's weights with one 8-byte load
+    __shared__ __align__(16) float s_w[16][18];
     {
         const int t = threadIdx.x;
         const int u = t >> 4, sg = t & 15;
@@ -962,7 +964,7 @@ __global__ void __launch_bounds__(256) k_correct(CorrectArgs a) {
             unsigned rem = um;
             for (int i = 0; i < u; ++i) rem &= rem - 1;
             const int z = __ffs(rem) - 1;
-            s_w[u][sg] = (float)(a.O64[sg * 16 + z] / a.P[q * 16 + z]);
+            s_w[sg][u] = (float)(a.O64[sg * 16 + z] / a.P[q * 16 + z]);
             if (tile == 0 && sg == 0 && a.cpath) {
                 const long long c = base + u;
                 const int level = a.level >= 0 ? a.level : path_level(a.vpath[v]);
@@ -1052,10 +1054,7 @@ __global__ void __launch_bounds__(256) k_correct(CorrectArgs a) {
             default: correct_predict<8>(a, r, c0, nbh, bb, sg); break;
         }
         const long long x0 = (long long)r * W + c0;
-        for (int u = 0; u < U; ++u) {
-            float o[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) o[i] = s_w[u][sg[i]] * bb[i];
+        auto put = [&](int u, const float (&o)[4]) {
             float *dst = a.child + (base + u) * a.cstride + x0;
             if (vec) {
                 __stcs(reinterpret_cast<float4 *>(dst), make_float4(o[0], o[1], o[2], o[3]));   // streaming
@@ -1064,6 +1063,17 @@ __global__ void __launch_bounds__(256) k_correct(CorrectArgs a) {
                 for (int i = 0; i < 4; ++i)
                     if (c0 + i < W) dst[i] = o[i];
             }
+        };
+        for (int u = 0; u < U; u += 2) {     // two children per weight load
+            float o0[4], o1[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float2 w = *reinterpret_cast<const float2 *>(&s_w[sg[i]][u]);
+                o0[i] = w.x * bb[i];
+                o1[i] = w.y * bb[i];
+            }
+            put(u, o0);
+            if (u + 1 < U) put(u + 1, o1);
         }
     }
 }
