@@ -2313,6 +2313,9 @@ extern "C" qvts_status qvts_belief_update(qvts_model *m, const float *b_dev, int
 // only (correct_predict's 4-cell groups, k_correct's tiling), one fp64 partial per (belief, tile,
 // class); pass 2 (k_bu_p) sums the tiles in order and forms P(z|b,a) = sum_s O[s][z] M[s].
 template <uint32_t MASK>
+// Eq. 3's normaliser for the one selected (a, z) of each belief, per row tile:
+// part[g][tile] = sum_y O[sig(y)][z] bbar_a(y) (fp64 per thread, fixed-order block reduction).
+// Only P(z | b, a) at the selected z is needed (k_correct's weights and the caller's p_obs).
 __global__ void __launch_bounds__(256) k_bu_marg(CorrectArgs a, double *__restrict__ part) {
     constexpr int NA = mask_count(MASK);
     const long long grp = blockIdx.x / a.ntiles;
@@ -2322,9 +2325,10 @@ __global__ void __launch_bounds__(256) k_bu_marg(CorrectArgs a, double *__restri
     const float *__restrict__ b = a.beliefs + (q / NA) * a.bstride;
     const int W = a.W;
     const bool vec = ((W & 3) == 0) && ((a.bstride & 3) == 0);
-    float acc[16];
-#pragma unroll
-    for (int s2 = 0; s2 < 16; ++s2) acc[s2] = 0.f;
+    __shared__ float s_o[16];                       // O[s][z] of the selected z
+    if (threadIdx.x < 16) s_o[threadIdx.x] = (float)a.O64[threadIdx.x * 16 + a.sel_z[grp]];
+    __syncthreads();
+    double acc = 0.0;
     const int r_end = min(a.H, (tile + 1) * a.rows_cta);
     for (int idx = threadIdx.x; idx < a.rows_cta * a.G; idx += 256) {
         const int r = tile * a.rows_cta + idx / a.G, c0 = 4 * (idx % a.G);
@@ -2362,48 +2366,32 @@ __global__ void __launch_bounds__(256) k_bu_marg(CorrectArgs a, double *__restri
             default: correct_predict<8>(a, r, c0, nbh, bb, sg); break;
         }
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int s2 = 0; s2 < 16; ++s2) acc[s2] += (sg[i] == s2) ? bb[i] : 0.f;
+        for (int i = 0; i < 4; ++i) acc += (double)(s_o[sg[i]] * bb[i]);
     }
-    // fixed-order reduction: butterfly within each warp, then the 8 warp sums in warp order (fp64)
-    __shared__ double wsum[8][16];
+    // fixed-order reduction: butterfly within each warp, then the 8 warp sums in warp order
+    __shared__ double wsum[8];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-    for (int s2 = 0; s2 < 16; ++s2) {
-        float v = acc[s2];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) wsum[warp][s2] = (double)v;
-    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) wsum[warp] = acc;
     __syncthreads();
-    if (threadIdx.x < 16) {
+    if (threadIdx.x == 0) {
         double sm = 0.0;
 #pragma unroll
-        for (int w2 = 0; w2 < 8; ++w2) sm += wsum[w2][threadIdx.x];
-        part[(grp * a.ntiles + tile) * 16 + threadIdx.x] = sm;
+        for (int w2 = 0; w2 < 8; ++w2) sm += wsum[w2];
+        part[grp * a.ntiles + tile] = sm;
     }
 }
-
-__global__ void k_bu_p(const double *__restrict__ part, int ntiles, const int32_t *__restrict__ sel_q, int n,
-                       const double *__restrict__ O64, double *__restrict__ P) {
-    const int g = blockIdx.x;
-    const int z = threadIdx.x;                       // 16 threads: P(z) for every z
-    __shared__ double M[16];
-    double m = 0.0;
-    for (int t2 = 0; t2 < ntiles; ++t2) m += part[((long long)g * ntiles + t2) * 16 + z];
-    M[z] = m;
-    __syncthreads();
-    double pz = 0.0;
-    for (int s2 = 0; s2 < 16; ++s2) pz += O64[s2 * 16 + z] * M[s2];
-    P[(long long)sel_q[g] * 16 + z] = pz;
-}
-
-// P(z_g | b_g, a_g) of the selected (Q-node, z) pairs, for the zero-likelihood check
-__global__ void k_gather_p(const double *__restrict__ P, const int32_t *__restrict__ sel_q,
-                           const int32_t *__restrict__ sel_z, int n, double *__restrict__ out) {
+// P(z | b, a) of each selected pair: the tile partials summed in order, into the Q-node layout
+// k_correct reads (P[q][z]) and the caller's per-belief array
+__global__ void k_bu_p(const double *__restrict__ part, int ntiles, const int32_t *__restrict__ sel_q,
+                       const int32_t *__restrict__ sel_z, int n, double *__restrict__ P, double *__restrict__ pout) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g < n) out[g] = P[(long long)sel_q[g] * 16 + sel_z[g]];
+    if (g >= n) return;
+    double pz = 0.0;
+    for (int t2 = 0; t2 < ntiles; ++t2) pz += part[(long long)g * ntiles + t2];
+    P[(long long)sel_q[g] * 16 + sel_z[g]] = pz;
+    pout[g] = pz;
 }
 
 extern "C" qvts_status qvts_belief_update_batch(qvts_model *m, const float *b_dev, int64_t b_stride, int32_t n,
@@ -2438,14 +2426,14 @@ extern "C" qvts_status qvts_belief_update_batch(qvts_model *m, const float *b_de
     // CTAs of ~BU_GROUPS groups of 4 cells (the plan's 1024 leave the one-child case latency-bound)
     static const int bu_groups = [] {
         const char *ev = std::getenv("QVTS_BU_GROUPS");
-        return ev ? std::max(256, std::atoi(ev)) : 4096;
+        return ev ? std::max(256, std::atoi(ev)) : 2048;   // 32-row tiles at W = 256: k_correct stages them
     }();
     c.rows_cta = std::min(m->H, std::max(1, bu_groups / std::max(1, c.G)));
     c.ntiles = (m->H + c.rows_cta - 1) / c.rows_cta;
     c.p_int = (float)m->p_int; c.p_stay = (float)m->p_stay; c.p_lat = (float)m->p_lat; c.qsel = -1;
     c.sel_q = d_sel; c.sel_z = d_sel + n; c.sel_out = d_sel + 2 * n;
     c.child = out_dev; c.cstride = out_stride;
-    QVTS_TRY(m->part.ensure(sizeof(double) * (size_t)n * c.ntiles * 16));
+    QVTS_TRY(m->part.ensure(sizeof(double) * (size_t)n * c.ntiles));
     QVTS_TRY(m->bu_R.ensure(sizeof(double) * (size_t)n * NA * 16));     // P in the Q-node layout
     c.P = m->bu_R.as<double>();
     const long long nblocks = (long long)n * c.ntiles;
@@ -2453,14 +2441,13 @@ extern "C" qvts_status qvts_belief_update_batch(qvts_model *m, const float *b_de
 #define QVTS_BUB(MASK)                                                                                          \
     {                                                                                                           \
         k_bu_marg<MASK><<<(unsigned)nblocks, 256, 0, st>>>(c, m->part.as<double>());                            \
-        k_bu_p<<<n, 16, 0, st>>>(m->part.as<double>(), c.ntiles, d_sel, n, m->d_O64.as<double>(),               \
-                                 m->bu_R.as<double>());                                                          \
+        k_bu_p<<<nblk(n, 256), 256, 0, st>>>(m->part.as<double>(), c.ntiles, d_sel, d_sel + n, n,               \
+                                             m->bu_R.as<double>(), m->bu_P.as<double>());                        \
         { const size_t csm_ = correct_stage(c); \
         k_correct<MASK><<<(unsigned)nblocks, 256, csm_, st>>>(c); } \
     }
     QVTS_DISPATCH_MASK(m->mask, QVTS_BUB);
 #undef QVTS_BUB
-    k_gather_p<<<nblk(n, 256), 256, 0, st>>>(m->bu_R.as<double>(), d_sel, d_sel + n, n, m->bu_P.as<double>());
     QVTS_CUDA(cudaGetLastError());
     std::vector<double> p(n);
     QVTS_CUDA(cudaMemcpyAsync(p.data(), m->bu_P.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
