@@ -135,8 +135,8 @@ QVTS_API qvts_status qvts_belief_update(qvts_model *model, const float *b_dev, i
 /* Batched Eq. 3 (SURVEY d.3 K9 at HBM scale): out_g = Phi(b_g, actions[g], zs[g]) for g < n.
  * b_dev: device fp32 [n][b_stride] (b_stride >= H*W floats), out_dev: device fp32 [n][out_stride]
  * (may not alias b_dev); actions (stencil ids) and zs: host int32 [n]; p_obs_out: host fp64 [n]
- * or NULL.  Two passes over each belief: the selected action's class sums of bbar (then P(z)),
- * and the correction (k_correct).  QVTS_ERR_ZERO_LIKELIHOOD if any P(z_g|b_g,a_g) <= 1e-30 (those
+ * or NULL.  Two passes over each belief: P(z|b,a) = sum_x' O(x',z) bbar_a(x') for the selected
+ * (a, z) only, then the correction (k_correct).  QVTS_ERR_ZERO_LIKELIHOOD if any P(z_g|b_g,a_g) <= 1e-30 (those
  * outputs unspecified, the rest valid).  Synchronises `stream`. */
 QVTS_API qvts_status qvts_belief_update_batch(qvts_model *model, const float *b_dev, int64_t b_stride, int32_t n,
                                               const int32_t *actions, const int32_t *zs, float *out_dev,

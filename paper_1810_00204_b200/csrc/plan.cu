@@ -2236,77 +2236,8 @@ extern "C" qvts_status qvts_belief_update(qvts_model *m, const float *b_dev, int
                                           float *out_dev, double *p_obs_out, void *stream) {
     qvts::NvtxRange nvtx_range__("qvts_belief_update");
     if (!m || !b_dev || !out_dev) { set_error("NULL argument"); return QVTS_ERR_INVALID_ARG; }
-    int j = -1;
-    for (int i = 0; i < m->NA; ++i) if (m->action_id[i] == action) j = i;
-    if (j < 0 || z < 0 || z > 15) { set_error("action not in the action set or z out of range"); return QVTS_ERR_INVALID_ARG; }
-    QVTS_CUDA(cudaSetDevice(m->device));
-    cudaStream_t st = (cudaStream_t)stream;
-    const int NA = m->NA;
-    QVTS_TRY(m->bu_R.ensure(sizeof(double) * NA));
-    QVTS_TRY(m->bu_P.ensure(sizeof(double) * 16 * NA));
-    QVTS_TRY(m->bu_cnt.ensure(sizeof(uint16_t) * 16 * NA));
-    QVTS_TRY(m->bu_umask.ensure(sizeof(uint16_t) * NA));
-    QVTS_TRY(m->bu_U.ensure(sizeof(int32_t) * NA));
-    QVTS_TRY(m->bu_off.ensure(sizeof(int32_t) * NA));
-    QVTS_TRY(m->bu_path.ensure(sizeof(uint64_t)));
-    QVTS_TRY(m->bu_root.ensure(sizeof(int32_t)));
-    QVTS_TRY(m->bu_key.ensure(sizeof(uint32_t) * 2));
-    QVTS_CUDA(cudaMemsetAsync(m->bu_path.p, 0, sizeof(uint64_t), st));
-    QVTS_CUDA(cudaMemsetAsync(m->bu_root.p, 0, sizeof(int32_t), st));
-    QVTS_CUDA(cudaMemsetAsync(m->bu_key.p, 0, sizeof(uint32_t) * 2, st));
-    const BandSet &bs = m->band_small;
-    qvts_status s = QVTS_ERR_INVALID_ARG;
-#define QVTS_BU_HIST(MASK)                                                                                    \
-    {                                                                                                         \
-        const int ps = pstride_of<MASK>(false);                                                               \
-        int nb_eff = bs.nb;                                                                                   \
-        s = m->part.ensure(sizeof(double) * (size_t)2 * bs.nb * ps);                                          \
-        if (s == QVTS_OK) s = launch_hist<MASK, false>(*m, bs, b_dev, m->HW, nullptr, 1, ps, st, &nb_eff);    \
-        if (s == QVTS_OK) {                                                                                   \
-            ReduceArgs r;                                                                                     \
-            std::memset(&r, 0, sizeof(r));                                                                    \
-            r.part = m->part.as<double>(); r.pstride = ps; r.nb = nb_eff; r.nwork = 1;                         \
-            r.beliefs = b_dev; r.bstride = m->HW; r.vpath = m->bu_path.as<uint64_t>();                        \
-            r.vroot = m->bu_root.as<int32_t>(); r.root_step = m->bu_key.as<uint32_t>();                       \
-            r.root_ep = m->bu_key.as<uint32_t>() + 1; r.n = 1; r.O64 = m->d_O64.as<double>();                 \
-            r.ngc = m->ngc; r.gc_cell = m->d_gc_cell.as<int32_t>(); r.gc_act = m->d_gc_act.as<int32_t>();     \
-            r.gc_val = m->d_gc_val.as<double>(); r.goal = m->goal; r.p_stay = m->p_stay; r.p_int = m->p_int; r.p_lat = m->p_lat; r.gamma = m->gamma;  \
-            r.R = m->bu_R.as<double>(); r.P = m->bu_P.as<double>(); r.cnt = m->bu_cnt.as<uint16_t>();         \
-            r.umask = m->bu_umask.as<uint16_t>(); r.U = m->bu_U.as<int32_t>();                                \
-            s = launch_reduce<MASK, false>(*m, r, st);                                                        \
-        }                                                                                                     \
-    }
-    QVTS_DISPATCH_MASK(m->mask, QVTS_BU_HIST);
-#undef QVTS_BU_HIST
-    QVTS_TRY(s);
-    QVTS_CUDA(cudaGetLastError());
-    double P[16];
-    QVTS_CUDA(cudaMemcpyAsync(P, m->bu_P.as<double>() + 16 * j, sizeof(P), cudaMemcpyDeviceToHost, st));
-    QVTS_CUDA(cudaStreamSynchronize(st));
-    if (p_obs_out) *p_obs_out = P[z];
-    if (!(P[z] > 1e-30)) { set_error("zero-likelihood observation"); return QVTS_ERR_ZERO_LIKELIHOOD; }
-    uint16_t um = (uint16_t)(1u << z);
-    std::vector<uint16_t> ums(NA, 0);
-    ums[j] = um;
-    QVTS_CUDA(cudaMemcpyAsync(m->bu_umask.p, ums.data(), sizeof(uint16_t) * NA, cudaMemcpyHostToDevice, st));
-    CorrectArgs c;
-    std::memset(&c, 0, sizeof(c));
-    c.beliefs = b_dev; c.bstride = m->HW; c.m8 = m->d_m8.as<uint8_t>(); c.cell = m->d_cell.as<uint8_t>();
-    c.O64 = m->d_O64.as<double>(); c.P = m->bu_P.as<double>();
-    c.cnt = m->bu_cnt.as<uint16_t>(); c.umask = m->bu_umask.as<uint16_t>(); c.off = m->bu_off.as<int32_t>();
-    c.vpath = m->bu_path.as<uint64_t>(); c.vroot = m->bu_root.as<int32_t>();
-    c.child = out_dev; c.cstride = m->HW; c.H = m->H; c.W = m->W; c.G = (m->W + 3) / 4;
-    c.rows_cta = correct_rows_per_cta(m->H, c.G);
-    c.ntiles = (m->H + c.rows_cta - 1) / c.rows_cta;
-    c.p_int = (float)m->p_int; c.p_stay = (float)m->p_stay; c.p_lat = (float)m->p_lat; c.qsel = j;
-    c.sel_q = c.sel_z = c.sel_out = nullptr;
-    const size_t csm_ = correct_stage(c);
-#define QVTS_BU_CORR(MASK) k_correct<MASK><<<c.ntiles, 256, csm_, st>>>(c)
-    QVTS_DISPATCH_MASK(m->mask, QVTS_BU_CORR);
-#undef QVTS_BU_CORR
-    QVTS_CUDA(cudaGetLastError());
-    QVTS_CUDA(cudaStreamSynchronize(st));
-    return QVTS_OK;
+    // one (b, a, z): the batched kernels with n = 1 (selected-z normaliser, then the correction)
+    return qvts_belief_update_batch(m, b_dev, m->HW, 1, &action, &z, out_dev, m->HW, p_obs_out, stream);
 }
 
 // Batched Eq. 3, pass 1: M_g[s] = sum over class-s cells of bbar_{a_g}(y) for the selected action
