@@ -13,9 +13,10 @@
 // the shifted beliefs is ever materialised); B (Q') is a model constant.
 //
 // Precision: fp16 x fp16 products on the tensor core are exact, but its fp32 accumulation
-// truncates, so (measured, profiles/r01_mma_precision.json) each chunk's MMAs start from zero and
-// their result is added in fp32 (RN) into a per-class run, the run into a per-class total at the
-// end of each band, and the total converted to fp64 at the end.  Operands are split hi + lo:
+// truncates (measured, profiles/r01_mma_precision.json: 6e-6 relative over 256 chunks), so the
+// MMA accumulates at most kLmFold = 4 chunks before they are folded in fp32 (RN) into the current
+// class run; the run joins the class's fp32 total in tensor memory when the class changes, and
+// the totals become fp64 in the epilogue.  Operands are split hi + lo:
 // b 2^14 = hi + lo (fp16 each, exact to 2^-22 relative), Q' = hi + lo likewise, and the three
 // products hi*hi + hi*lo + lo*hi are formed (the lo*lo term is below 2^-22).
 //
