@@ -56,7 +56,7 @@ class PlanCfg(C.Structure):
     _fields_ = [("depth", C.c_int), ("n_samples", C.c_int), ("mode", C.c_int), ("threads", C.c_int),
                 ("seed", C.c_uint32), ("step", C.c_uint32), ("episode", C.c_uint32),
                 ("sampler", C.c_int), ("n_replay", C.c_int), ("replay_path", C.c_void_p),
-                ("replay_j", C.c_void_p), ("replay_z", C.c_void_p)]
+                ("replay_j", C.c_void_p), ("replay_z", C.c_void_p), ("replay_x", C.c_void_p)]
 
 
 class BfCfg(C.Structure):
@@ -450,17 +450,20 @@ class Model:
     # -- plan step --
     @staticmethod
     def _cfg(depth, n, seed, step, episode, mode, threads, replay, sampler=0):
-        cfg = PlanCfg(depth, n, mode, threads, seed, step, episode, sampler, 0, None, None, None)
+        cfg = PlanCfg(depth, n, mode, threads, seed, step, episode, sampler, 0, None, None, None, None)
         keep = None
         if replay:
+            # entries (qpath, sample j, GPU z[, GPU state index x]); the ancestral sampler replays x
             rp = np.array([r[0] for r in replay], dtype=np.uint64)
             rj = np.array([r[1] for r in replay], dtype=np.int32)
             rz = np.array([r[2] for r in replay], dtype=np.uint8)
-            keep = (rp, rj, rz)
+            rx = np.array([r[3] if len(r) > 3 else -1 for r in replay], dtype=np.int32)
+            keep = (rp, rj, rz, rx)
             cfg.n_replay = len(replay)
             cfg.replay_path = rp.ctypes.data
             cfg.replay_j = rj.ctypes.data
             cfg.replay_z = rz.ctypes.data
+            cfg.replay_x = rx.ctypes.data if any(len(r) > 3 for r in replay) else None
         return cfg, keep
 
     def plan(self, Q, b0, depth, n, seed=1, step=0, episode=0, mode=MODE_FREQ, trace=False,
@@ -504,16 +507,16 @@ class Model:
                      qz[:nq * ns].reshape(nq, ns), qf[:nq * ns].reshape(nq, ns),
                      vp, vl, vV, vz, vf, bel)
 
-    def qnode_sample(self, b, a, qpath, n, seed=1, step=0, episode=0, sampler=0):
-        cfg, _ = self._cfg(0, n, seed, step, episode, MODE_FREQ, 1, None, sampler)
+    def qnode_sample(self, b, a, qpath, n, seed=1, step=0, episode=0, sampler=0, replay=None):
+        cfg, _keep = self._cfg(0, n, seed, step, episode, MODE_FREQ, 1, replay, sampler)
         P = np.zeros(16); R = C.c_double(0)
         z = np.zeros(n, np.uint8); f = np.zeros(n, np.uint8); cnt = np.zeros(16, np.uint16)
         lib().or_qnode_sample(self._h, np.ascontiguousarray(b, dtype=np.float64), a, int(qpath),
                               C.byref(cfg), P, C.byref(R), z, f, cnt)
         return P, R.value, z, f.astype(bool), cnt
 
-    def vnode_value(self, Q, b, vpath, level, depth, n, seed=1, step=0, episode=0, mode=MODE_FREQ):
-        cfg, _ = self._cfg(depth, n, seed, step, episode, mode, 1, None)
+    def vnode_value(self, Q, b, vpath, level, depth, n, seed=1, step=0, episode=0, mode=MODE_FREQ, replay=None):
+        cfg, _keep = self._cfg(depth, n, seed, step, episode, mode, 1, replay)
         qv = np.zeros(self.na)
         v = lib().or_vnode_value(self._h, np.ascontiguousarray(Q, dtype=np.float64).reshape(-1),
                                  np.ascontiguousarray(b, dtype=np.float64), int(vpath), level,

@@ -644,33 +644,67 @@ static int replay_lookup(const or_plan_cfg *cfg, uint64_t qpath, int j, int *z) 
         if (cfg->replay_path[i] == qpath && cfg->replay_j[i] == j) { *z = cfg->replay_z[i]; return 1; }
     return 0;
 }
+static int replay_lookup_x(const or_plan_cfg *cfg, uint64_t qpath, int j, int *x) {
+    if (!cfg->replay_x) return 0;
+    for (int i = 0; i < cfg->n_replay; ++i)
+        if (cfg->replay_path[i] == qpath && cfg->replay_j[i] == j) { *x = cfg->replay_x[i]; return 1; }
+    return 0;
+}
+
+/* c.5 step 3: a replayed category r of the inverse CDF over p[0..K) (target t = u * C_last) is
+ * admissible only if it borders a boundary C_k within OR_FLAG_GAP of t: r is the first category
+ * whose cumulative reaches C_k, or the first whose cumulative exceeds it. */
+static int borders_near_boundary(const double *p, int K, double u, int r) {
+    double *C = (double *)malloc(sizeof(double) * K);
+    double s = 0.0;
+    for (int k = 0; k < K; ++k) { s += p[k]; C[k] = s; }
+    double t = u * C[K - 1];
+    int ok = 0;
+    for (int k = 0; k < K - 1 && !ok; ++k) {
+        if (fabs(t - C[k]) >= OR_FLAG_GAP) continue;
+        int lo = K - 1, hi = K - 1;
+        for (int i = 0; i < K; ++i) if (C[i] >= C[k]) { lo = i; break; }
+        for (int i = 0; i < K; ++i) if (C[i] > C[k]) { hi = i; break; }
+        ok = (r == lo || r == hi);
+    }
+    free(C);
+    return ok;
+}
 
 /* Draws of one Q-node (Appendix A.2-A.6); returns the draws, flags and counts. */
 /* Alg. 4 literal: x ~ b (word 1), x' ~ T(x,a,.) over the clamped row in its
  * stored order (word 2), z ~ O(x',.) (word 3).  Only the state draw can be near a CDF boundary
- * (the other two CDFs are exact model tables), so *flag reports that draw (A.6 rule). */
-static int ancestral_draw(const or_model *m, const double *b, int a, const uint32_t w[4], int *flag) {
-    int x = or_inverse_cdf(b, m->nx, or_uniform(w[1]), flag);
+ * (the other two CDFs are exact model tables), so the flag reports that draw (A.6 rule). */
+static int ancestral_state(const or_model *m, const double *b, const uint32_t w[4], int *flag) {
+    return or_inverse_cdf(b, m->nx, or_uniform(w[1]), flag);
+}
+static int ancestral_obs(const or_model *m, int x, int a, const uint32_t w[4]) {
     int e0 = m->t_start[x * m->na + a], e1 = m->t_start[x * m->na + a + 1];
     double p[9];
     for (int e = e0; e < e1; ++e) p[e - e0] = m->t_p[e];
     int xp = m->t_y[e0 + or_inverse_cdf(p, e1 - e0, or_uniform(w[2]), NULL)];
     return or_inverse_cdf(&m->O[xp * m->nz], m->nz, or_uniform(w[3]), NULL);
 }
+static int ancestral_draw(const or_model *m, const double *b, int a, const uint32_t w[4], int *flag) {
+    return ancestral_obs(m, ancestral_state(m, b, w, flag), a, w);
+}
 
 static void qnode_draws(const or_model *m, const double *b, int a, const or_plan_cfg *cfg, int nz,
                         const double *P, uint64_t qpath, uint8_t *zs, uint8_t *flags, uint16_t *cnt) {
-    double C[16];
-    double s = 0.0;
-    for (int k = 0; k < nz; ++k) { s += P[k]; C[k] = s; cnt[k] = 0; }
+    for (int k = 0; k < nz; ++k) cnt[k] = 0;
     for (int j = 0; j < cfg->n_samples; ++j) {
         uint32_t ctr[4] = {(uint32_t)j, (uint32_t)qpath, (uint32_t)(qpath >> 32), cfg->step};
         uint32_t key[2] = {cfg->seed, cfg->episode}, w[4];
         or_philox4x32_10(ctr, key, w);
         if (cfg->sampler == OR_SAMPLER_ANCESTRAL) {
-            int flag, zr, z = ancestral_draw(m, b, a, w, &flag);
-            /* a flagged state draw may land in the neighbouring state: replay the GPU's z */
-            if (flag && cfg->n_replay > 0 && replay_lookup(cfg, qpath, j, &zr)) z = zr;
+            int flag, xr;
+            int x = ancestral_state(m, b, w, &flag);
+            /* a flagged state draw may land in the neighbouring state: take the GPU's x if it
+               borders the near boundary, then x' and z follow from it with words 2-3 */
+            if (flag && cfg->n_replay > 0 && replay_lookup_x(cfg, qpath, j, &xr) && xr != x &&
+                xr >= 0 && xr < m->nx && borders_near_boundary(b, m->nx, or_uniform(w[1]), xr))
+                x = xr;
+            int z = ancestral_obs(m, x, a, w);
             zs[j] = (uint8_t)z;
             flags[j] = (uint8_t)flag;
             cnt[z]++;
@@ -680,17 +714,9 @@ static void qnode_draws(const or_model *m, const double *b, int a, const or_plan
         int flag;
         int z = or_inverse_cdf(P, nz, u, &flag);
         int zr;
-        if (flag && cfg->n_replay > 0 && replay_lookup(cfg, qpath, j, &zr) && zr != z) {
-            /* accept the replayed category only if it borders a near boundary (c.5 step 3) */
-            double t = u * C[nz - 1];
-            for (int k = 0; k < nz - 1; ++k) {
-                if (fabs(t - C[k]) >= OR_FLAG_GAP) continue;
-                int lo = nz - 1, hi = nz - 1;
-                for (int i = 0; i < nz; ++i) if (C[i] >= C[k]) { lo = i; break; }
-                for (int i = 0; i < nz; ++i) if (C[i] > C[k]) { hi = i; break; }
-                if (zr == lo || zr == hi) { z = zr; break; }
-            }
-        }
+        if (flag && cfg->n_replay > 0 && replay_lookup(cfg, qpath, j, &zr) && zr != z &&
+            borders_near_boundary(P, nz, u, zr))   /* accept only a category bordering a near boundary */
+            z = zr;
         zs[j] = (uint8_t)z;
         flags[j] = (uint8_t)flag;
         cnt[z]++;

@@ -89,11 +89,14 @@ typedef struct {
     uint32_t seed, step, episode;
     int sampler;   /* OR_SAMPLER_MARGINAL (reading R9, Philox word 0) or OR_SAMPLER_ANCESTRAL
                       (Alg. 4 literal: x ~ b, x' ~ T(x,a,.), z ~ O(x',.) with words 1..3) */
-    /* replay table for flagged, mismatched draws (SURVEY c.5 step 3) */
+    /* replay table for flagged, mismatched draws (SURVEY c.5 step 3): the GPU's observation
+       z (marginal sampler) or its state index x (ancestral sampler; x' and z are then recomputed
+       from that x) -- taken only when it borders the near CDF boundary */
     int n_replay;
     const uint64_t *replay_path;
     const int32_t *replay_j;
     const uint8_t *replay_z;
+    const int32_t *replay_x;
 } or_plan_cfg;
 
 or_trace *or_trace_new(int capture_beliefs /*0 none, 1 all non-leaf V-nodes*/);

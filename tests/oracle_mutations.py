@@ -37,6 +37,12 @@ MUTANTS = [
     ("PBVI: blind start at R_max", "if (!(m->is_grid && m->occ[i / na]) && m->R[i] < rmin) rmin = m->R[i];",
      "if (!(m->is_grid && m->occ[i / na]) && m->R[i] > rmin) rmin = m->R[i];"),
     ("advance: paths not re-based", "        v->path >>= 8;\n", "\n"),
+    ("PBVI expansion: nearest candidate", "if (pbvi_beats(dmin, best_d)) { best_d = dmin; best_a = a; }",
+     "if (dmin > 0.0 && (best_a < 0 || dmin < best_d)) { best_d = dmin; best_a = a; }"),
+    ("PBVI expansion: first candidate off the set", "if (pbvi_beats(dmin, best_d)) { best_d = dmin; best_a = a; }",
+     "if (best_a < 0 && dmin > 0.0) { best_d = dmin; best_a = a; }"),
+    ("replay: any category accepted", "borders_near_boundary(P, nz, u, zr))", "1)"),
+    ("ancestral replay: any state accepted", "&& borders_near_boundary(b, m->nx, or_uniform(w[1]), xr))", ")"),
 ]
 
 cc = "/usr/bin/gcc" if os.path.exists("/usr/bin/gcc") else "gcc"

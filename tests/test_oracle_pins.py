@@ -516,6 +516,87 @@ def test_pbvi_zero_sweeps_is_the_blind_bound():
         assert max(a @ b for a in al) == pytest.approx(rmin / (1 - 0.95), abs=1e-12)
 
 
+def _flagged_qnode(m, b, sampler, n=60000):
+    """First Q-node (over tree paths 1, 2, ...) with a flagged draw among n samples."""
+    for qpath in range(1, 400):
+        P, R, z, flag, cnt = m.qnode_sample(b, qpath % m.na, qpath, n, seed=2, sampler=sampler)
+        if flag.any():
+            return qpath, P, z, flag
+    raise AssertionError("no flagged draw found")
+
+
+def test_replay_takes_only_a_category_at_the_flagged_boundary():
+    """SURVEY c.5 step 3 / reading R11: where the oracle flags a draw (u C_15 within 1e-6 of a CDF
+    boundary) it follows the GPU's category only if that category borders the near boundary; a
+    far category, or any replay of a non-flagged draw, is ignored."""
+    gm = W.random_map(12, 12, 0.2, seed=3)
+    m = O.Model.grid(gm, action_mask=W.A8)
+    b = W.random_belief(gm, 4)
+    n = 60000
+    qpath, P, z, flag = _flagged_qnode(m, b, 0, n)
+    a = qpath % m.na
+    j = int(np.flatnonzero(flag)[0])
+    zo = int(z[j])
+    live = [k for k in range(16) if P[k] > 0]
+    lower = max([k for k in live if k < zo], default=None)
+    upper = min([k for k in live if k > zo], default=None)
+    far = [k for k in live if k not in (lower, zo, upper)]
+    for f in far[:3]:
+        _, _, z2, _, _ = m.qnode_sample(b, a, qpath, n, seed=2, replay=[(qpath, j, f)])
+        assert np.array_equal(z2, z)
+    took = 0
+    for cand in (lower, upper):
+        if cand is None:
+            continue
+        _, _, z3, _, _ = m.qnode_sample(b, a, qpath, n, seed=2, replay=[(qpath, j, cand)])
+        assert np.array_equal(np.delete(z3, j), np.delete(z, j))
+        took += int(z3[j] == cand)
+    assert took == 1                     # exactly the neighbour across the near boundary
+    j2 = int(np.flatnonzero(~flag)[0])
+    _, _, z4, _, _ = m.qnode_sample(b, a, qpath, n, seed=2, replay=[(qpath, j2, (int(z[j2]) + 1) % 16)])
+    assert np.array_equal(z4, z)
+
+
+def test_ancestral_replay_ignores_a_state_off_the_flagged_boundary():
+    """The same rule for Alg. 4's state draw (NEXT-3): a replayed state index x is taken only if
+    it borders the flagged boundary of the state CDF; cells far from it change nothing."""
+    gm = W.random_map(12, 12, 0.2, seed=3)
+    m = O.Model.grid(gm, action_mask=W.A8)
+    b = W.random_belief(gm, 4)
+    n = 2000
+    qpath, P, z, flag = _flagged_qnode(m, b, 1, n)
+    a = qpath % m.na
+    j = int(np.flatnonzero(flag)[0])
+    free = np.flatnonzero(gm.occupancy == 0)
+    for x in list(free[::17][:6]) + [int(np.flatnonzero(gm.occupancy)[0])]:
+        _, _, z2, _, _ = m.qnode_sample(b, a, qpath, n, seed=2, sampler=1, replay=[(qpath, j, 0, int(x))])
+        assert np.array_equal(z2, z), x
+
+
+def test_pbvi_expansion_takes_the_farthest_candidate():
+    """PAPER.md:126 (§IV-B): a new belief point is generated from a point already in the set by
+    forward sampling, keeping the candidate farthest (L1) from the set.  Hand-built case where the
+    farthest, the nearest and the first candidate differ: noise-free motion (p_int = 1), perfect
+    sensing, a 9x9 open room, b0 a 2x2 block (a, b / c, d) = (0.3, 0.1 / 0.45, 0.15) in the interior
+    where every cell has wall signature 0 -- so each of the 8 moves gives one posterior, b0
+    shifted.  L1 distances to b0 (derived by hand): a shift by a diagonal with the overlapping pair
+    (a, d) or (b, c) gives 2 - 2 min of the pair, an axis shift 1 + the two differences across it:
+    up-left/down-right 1.7, up/down 1.2, up-right/down-left 1.8, left/right 1.5.  Farthest =
+    up-right (ties to the lowest stencil id, reading B4); first = up-left; nearest = up."""
+    gm = W.from_ascii("\n".join(["." * 9] * 4 + ["....G...."] + ["." * 9] * 4))
+    m = O.Model.grid(gm, action_mask=W.A8, p_int=1.0, p_stay=0.0, p_lat=0.0, acc=1.0)
+    b0 = np.zeros(81)
+    for (r, c), w in {(3, 3): 0.3, (3, 4): 0.1, (4, 3): 0.45, (4, 4): 0.15}.items():
+        b0[r * 9 + c] = w
+    pts, _, _ = m.pbvi(b0, expansions=1, max_points=2, seed=5, sweeps=0)
+    assert pts.shape[0] == 2
+    want = np.zeros(81)                       # b0 moved up-right: (r, c) -> (r - 1, c + 1)
+    for (r, c), w in {(3, 3): 0.3, (3, 4): 0.1, (4, 3): 0.45, (4, 4): 0.15}.items():
+        want[(r - 1) * 9 + c + 1] = w
+    assert np.max(np.abs(pts[1] - want)) <= 1e-15
+    assert np.sum(np.abs(pts[1] - b0)) == pytest.approx(1.8, abs=1e-12)
+
+
 def test_pbvi_perfect_observation_chain_reaches_mdp_values():
     m = _chain()
     b0 = np.eye(5)[0]
