@@ -172,6 +172,11 @@ typedef struct {
     int64_t n_belief_updates;     /* sum of n_vnodes[1..depth] created by this call (SURVEY d.2) */
     double device_ms;             /* CUDA-event time of the whole step on `stream`             */
     int32_t shard_level;          /* multi-rank: first rank-local level is shard_level+1; -1 none */
+    int64_t n_flag_candidates;    /* draws of this step whose u * C_15 lies within 1e-6 of a boundary
+                                     of the GPU's own fp64 CDF (the c.5 "flagged" draws; marginal
+                                     sampler; on a rank: its own Q-nodes only)                  */
+    int64_t n_tiles_skipped;      /* (parent pair, row band) tiles whose beliefs held no mass and
+                                     were skipped (active-tile skipping)    */
 } qvts_plan_result;
 
 /* Multi-rank plan step: levels above `shard_level` are replicated, the V-nodes
@@ -222,6 +227,9 @@ QVTS_API qvts_status qvts_trace_leaf_values(const qvts_model *model, double *V /
  * the number of expanded V-nodes n_qwork[0..depth-1] per Q-level (n_q = n_qwork * |A|). */
 QVTS_API qvts_status qvts_trace_counts(const qvts_model *model, int32_t *depth, int64_t *n_v, int64_t *n_qwork);
 QVTS_API qvts_status qvts_trace_belief(const qvts_model *model, int32_t level, int64_t index, float *out_host);
+/* Alg. 4 sampler (QVTS_SAMPLER_ANCESTRAL) with want_trace: the state index x of every draw,
+ * [n_q][n_samples] int32 (row-major cell index), level 0..D-1.  QVTS_ERR_STATE otherwise. */
+QVTS_API qvts_status qvts_trace_state_draws(const qvts_model *model, int32_t level, int32_t *x);
 
 /* ---- (4b) anytime best-first QVTS (Alg. 1 inner loop + Algs. 2-7, Eq. 8; PAPER.md:130-298;
  * SURVEY §8(f) NEXT-2; reading B5) -------------------------------------------------

@@ -363,6 +363,9 @@ extern "C" qvts_status qvts_run_episodes(qvts_model *m, const qvts_episode_cfg *
         for (DevBuf *b : {&st_i32, &st_f64, &bel[0], &bel[1], &b0buf, &cdf, &act_ids, &act_list, &wave_tmp, &cnt,
                           &recbuf, &logs, &ukeys})
             b->release();
+        // level maps pointing into the released active lists must not outlive them:
+        // a later trace accessor would read freed memory
+        for (auto &q : m->ql) { q.mapped = false; q.vmap_ptr = nullptr; }
     };
     qvts_status s = QVTS_OK;
     const int nn = std::max(1, no);

@@ -192,15 +192,18 @@ qvts_status build_bands(Model &m, BandSet &bs, int rows) {
 }
 
 // Q in slot order, offset by qbar (SURVEY c.6 rule 5): qlist[slot][NAP].
+// T > 0: the leaf kernel's layout [step][NAP / 4][T slots][4] (slot s = step * T + t), so a warp's
+// 16-byte copies of one quarter-row are contiguous
 __global__ void k_qlist(const double *__restrict__ Q64, const int32_t *__restrict__ slot_cell,
-                        long long nslots, int NA, int NAP, int HW, double qbar, float *__restrict__ out) {
+                        long long nslots, int NA, int NAP, int HW, double qbar, float *__restrict__ out, int T = 0) {
     long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (s >= nslots) return;
     int x = slot_cell[s];
     for (int j = 0; j < NAP; ++j) {
         float v = 0.f;
         if (x >= 0 && j < NA) v = (float)(Q64[(size_t)j * HW + x] - qbar);
-        out[s * NAP + j] = v;
+        if (T > 0) out[(((s / T) * (NAP / 4) + j / 4) * T + s % T) * 4 + (j & 3)] = v;
+        else out[s * NAP + j] = v;
     }
 }
 
@@ -211,6 +214,15 @@ qvts_status build_qlists(Model &m, const double *src64, double qbar, bool fib, c
         long long n = bs->total_slots;
         k_qlist<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(src64, bs->slot_cell.as<int32_t>(), n, m.NA, m.NAP, m.HW,
                                                             qbar, dst.as<float>());
+        QVTS_CUDA(cudaGetLastError());
+    }
+    {
+        LeafBands &lb = m.leafb;
+        DevBuf &dst = fib ? lb.qlist_fib : lb.qlist;
+        QVTS_TRY(dst.ensure(sizeof(float) * lb.total_slots * m.NAP));
+        const long long n = lb.total_slots;
+        k_qlist<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(src64, lb.slot_cell.as<int32_t>(), n, m.NA, m.NAP, m.HW,
+                                                            qbar, dst.as<float>(), kLeafThreads);
         QVTS_CUDA(cudaGetLastError());
     }
     return build_leaf_qfrag(m, src64, qbar, fib, st);
@@ -480,16 +492,6 @@ extern "C" qvts_status qvts_model_create(const qvts_model_desc *d, qvts_model **
             }
     }
     m->ngc = (int)gc_cell.size();
-    // fused leaf level: the distinct cells whose belief R(b,a) reads (goal first), and for every
-    // goal term the index of its cell in that list
-    std::vector<int32_t> fcells{m->goal}, gc_fidx;
-    for (int32_t x : gc_cell) {
-        int f = -1;
-        for (size_t i = 0; i < fcells.size(); ++i) if (fcells[i] == x) f = (int)i;
-        if (f < 0) { f = (int)fcells.size(); fcells.push_back(x); }
-        gc_fidx.push_back(f);
-    }
-    m->nfcells = (int)fcells.size();
     m->n_free = 0;
     for (int x = 0; x < HW; ++x) m->n_free += m->occ[x] ? 0 : 1;
     std::vector<uint8_t> freev(HW), cell(HW);
@@ -509,8 +511,6 @@ extern "C" qvts_status qvts_model_create(const qvts_model_desc *d, qvts_model **
         if ((st = upload(m->d_O64, O64)) != QVTS_OK) break;
         if ((st = upload(m->d_O32, O32)) != QVTS_OK) break;
         if ((st = upload(m->d_gc_cell, gc_cell)) != QVTS_OK) break;
-        if ((st = upload(m->d_fcells, fcells)) != QVTS_OK) break;
-        if (!gc_fidx.empty() && (st = upload(m->d_gc_fidx, gc_fidx)) != QVTS_OK) break;
         if ((st = upload(m->d_gc_act, gc_act)) != QVTS_OK) break;
         if ((st = upload(m->d_gc_val, gc_val)) != QVTS_OK) break;
         // band sets: ~16K cells per band for many parents, ~2K for few (more CTAs per parent)
@@ -523,6 +523,7 @@ extern "C" qvts_status qvts_model_create(const qvts_model_desc *d, qvts_model **
         if (const char *ev = std::getenv("QVTS_BAND_ROWS")) big_rows = std::max(1, std::atoi(ev));
         if ((st = build_bands(*m, m->band_big, big_rows)) != QVTS_OK) break;
         if ((st = build_bands(*m, m->band_small, std::max(1, 1024 / W))) != QVTS_OK) break;
+        if ((st = build_leaf_bands(*m, m->leafb)) != QVTS_OK) break;
         if ((st = build_leaf_mma(*m)) != QVTS_OK) break;
         if (cudaEventCreate(&m->ev0) != cudaSuccess || cudaEventCreate(&m->ev1) != cudaSuccess) {
             set_error("cudaEventCreate failed"); st = QVTS_ERR_CUDA; break;
@@ -537,9 +538,9 @@ extern "C" void qvts_model_destroy(qvts_model *m) {
     if (!m) return;
     cudaSetDevice(m->device);
     DevBuf *bufs[] = {&m->d_m8, &m->d_sig, &m->d_cell, &m->bu_R, &m->bu_P, &m->bu_cnt, &m->bu_umask,
-                      &m->bu_U, &m->bu_off, &m->bu_path, &m->bu_root, &m->bu_key, &m->d_ctab, &m->d_R64, &m->d_O64, &m->d_O32, &m->d_gc_cell, &m->d_fcells, &m->d_gc_fidx, &m->fl_goalv,
+                      &m->bu_U, &m->bu_off, &m->bu_path, &m->bu_root, &m->bu_key, &m->d_ctab, &m->d_R64, &m->d_O64, &m->d_O32, &m->d_gc_cell,
                       &m->d_gc_act, &m->d_gc_val, &m->d_free, &m->d_V[0], &m->d_V[1], &m->d_A[0], &m->d_A[1], &m->d_alpha64, &m->d_resid,
-                      &m->d_Q64, &m->part, &m->tickets, &m->xs, &m->scan_tmp, &m->total, &m->counters, &m->vshard,
+                      &m->d_Q64, &m->part, &m->xs, &m->scan_tmp, &m->total, &m->counters, &m->vshard,
                       &m->ep_b[0], &m->ep_b[1], &m->ep_state, &m->ep_root_step, &m->ep_root_ep,
                       &m->pb_b0, &m->pb_B, &m->pb_G, &m->pb_Gn, &m->pb_GT, &m->pb_Bbar, &m->pb_Sc, &m->pb_Rb,
                       &m->pb_sel, &m->pb_astar, &m->pb_cand, &m->pb_misc, &m->pb_cls, &m->pb_chunks, &m->pb_part};
@@ -549,6 +550,8 @@ extern "C" void qvts_model_destroy(qvts_model *m) {
     for (BandSet *bs : {&m->band_big, &m->band_small}) {
         bs->bands.release(); bs->entries.release(); bs->slot_cell.release(); bs->qlist.release(); bs->qlist_fib.release();
     }
+    m->leafb.bands.release(); m->leafb.entries.release(); m->leafb.slot_cell.release();
+    m->leafb.qlist.release(); m->leafb.qlist_fib.release();
     for (cudaEvent_t e : m->evpool) cudaEventDestroy(e);
     for (auto &v : m->vl) { v.path.release(); v.parent_q.release(); v.z.release(); v.f.release(); v.root.release(); v.V.release(); v.belief.release(); }
     for (DevBuf *b : {&m->bf_bel, &m->bf_path, &m->bf_pq, &m->bf_z, &m->bf_f, &m->bf_root, &m->bf_depth, &m->bf_vU,
@@ -561,14 +564,10 @@ extern "C" void qvts_model_destroy(qvts_model *m) {
         q.vmap.release(); q.R.release(); q.P.release(); q.cnt.release(); q.umask.release(); q.U.release();
         q.off.release(); q.Q.release(); q.zdraw.release(); q.leafV.release();
     }
-    for (auto &q : m->ql) { q.vmap.release(); q.R.release(); q.P.release(); q.cnt.release(); q.umask.release(); q.U.release(); q.off.release(); q.Q.release(); q.zdraw.release(); q.leafV.release(); }
+    for (auto &q : m->ql) { q.vmap.release(); q.R.release(); q.P.release(); q.cnt.release(); q.umask.release(); q.U.release(); q.off.release(); q.Q.release(); q.zdraw.release(); q.leafV.release(); q.xdraw.release(); }
     if (m->bf_gexec) cudaGraphExecDestroy(m->bf_gexec);
     if (m->pg_exec) cudaGraphExecDestroy(m->pg_exec);
     if (m->pg_stream) cudaStreamDestroy(m->pg_stream);
-    if (m->ov_corr) cudaStreamDestroy(m->ov_corr);
-    if (m->ov_leaf) cudaStreamDestroy(m->ov_leaf);
-    for (cudaEvent_t e : m->ov_ev)
-        if (e) cudaEventDestroy(e);
     if (m->pg_join) cudaEventDestroy(m->pg_join);
     m->lvl_cnt.release();
     m->root_buf.release();

@@ -83,10 +83,6 @@ struct ReduceArgs {
     double acc;
     const int32_t *skip = nullptr;  // device flag: non-zero -> the launch does nothing (best-first)
     const long long *nwork_dev = nullptr;   // device-side parent count (graph-captured plan step)
-    // fused leaf level: the leaf parents' beliefs at the goal-term cells [v][nf] (k_child_meta)
-    const float *goalv = nullptr;
-    int nf = 0;
-    const int32_t *gc_fidx = nullptr;
 };
 
 // tree level of a V-node path: one non-zero byte per action level (low nibble a+1 >= 1)
@@ -220,14 +216,14 @@ __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int
     if (k != 4) {
         for (int g = lane; g < a.ngc; g += 32)
             if (a.gc_act[g] == j)
-                gsum += a.gc_val[g] * (double)(a.goalv ? a.goalv[v * a.nf + a.gc_fidx[g]] : bp[a.gc_cell[g]]);
+                gsum += a.gc_val[g] * (double)bp[a.gc_cell[g]];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) gsum += __shfl_xor_sync(0xffffffffu, gsum, o);
     }
     double R = 0.0;
     if (lane == 0) {
         if (k == 4) {
-            R = -2.0 * mass + 2.0 * (double)(a.goalv ? a.goalv[v * a.nf] : bp[a.goal]);
+            R = -2.0 * mass + 2.0 * (double)bp[a.goal];
         } else {
             const double Rp = a.p_stay * mass + a.p_int * sE[da] + a.p_lat * (sE[d1] + sE[d2]);
             R = (a.p_stay - 1.0) * mass - Rp + gsum;
@@ -382,11 +378,13 @@ __global__ void __launch_bounds__(256) k_ancestral_x(const float *__restrict__ b
                                                      const uint64_t *vpath, const int32_t *vroot,
                                                      const uint32_t *root_step, const uint32_t *root_ep,
                                                      uint32_t seed, int level, int n, int32_t *xs,
-                                                     const int32_t *skip = nullptr) {
+                                                     const int32_t *skip = nullptr,
+                                                     const long long *nwork_dev = nullptr) {
     constexpr int NA = mask_count(MASK);
     constexpr int CH = 256;
     extern __shared__ double sx[];   // [nch] chunk sums, then exclusive prefix in place
     if (skip && *skip) return;
+    if (nwork_dev && (long long)blockIdx.x >= *nwork_dev) return;   // graph path: worst-case grid
     const long long w = blockIdx.x;
     const long long v = vmap ? (long long)vmap[w] : w;
     const float *__restrict__ b = beliefs + v * bstride;
@@ -453,9 +451,10 @@ __global__ void __launch_bounds__(256) k_ancestral_x(const float *__restrict__ b
 //   H_s[k][a'] = sum h_k Q'(.,a')   (Q' = Q - qbar, SURVEY c.6 rule 5)
 // plus E[k] = sum occ(y + d_k) b(y) for R(b,a); k_reduce recombines them per action in fp64.
 // One CTA = 2 parents x one row band: 256 threads = 128 slot-threads x 2 parents, the parents in
-// the two half-warps so the static per-slot loads (entry, Q') are shared.  The CTAs of the bands
-// of one parent pair form a thread-block cluster and sum their class totals through DSMEM, so a
-// single fp64 partial per parent reaches HBM.
+// the two half-warps so the static per-slot loads (entry, Q') are shared; one fp64 partial per
+// (parent, band).  The plan's leaf level runs leaf.cu's k_leaf instead (same values, class-fixed
+// slots across bands, packed parent pairs) for the action sets it covers.
+
 // ---- S4: Bayes correction of every unique z of a Q-node ----------------------------------------
 // One CTA = one Q-node x 1024 cells (4 consecutive cells of one row per thread).  The thread
 // predicts bbar_a for its 4 cells once (linear form of k_hist) and writes every child
@@ -487,6 +486,8 @@ struct CorrectArgs {
     long long q0 = 0;                          // first Q-node of this launch (chunked launches)
     int stage_tp = 0;                          // > 0: the CTA's parent rows (+ halo) are staged in shared
                                                // memory with this row pitch (correct_stage)
+    int vec_in = 0, vec_out = 0;               // 16-byte row access to the parents / children: W, the
+                                               // strides AND the base pointers allow it (correct_stage)
 };
 
 // bbar_a for 4 consecutive cells (r, c0..c0+3): bbar = p_stay b + p_int h_a + p_lat (h_l1 + h_l2),
@@ -530,64 +531,6 @@ __device__ __forceinline__ void correct_predict(const CorrectArgs &a, int r, int
     }
 }
 
-// Fused leaf level (SURVEY d.3 "K5-vs-fused"): the leaf parents' beliefs are never written.  Each
-// is rebuilt inside the leaf k_hist's staging from its own parent (the grandparent of the
-// leaves) with k_correct's arithmetic, b_v(y) = O[sig(y)][z_v] bbar_a(y) / P(z_v), so the
-// staged tiles -- and every result -- are bit-identical to the materialised path.
-struct FusedLeaf {
-    const int32_t *parent_q, *z;       // per leaf-parent V-node: parent Q-node (work index), z
-    const double *P;                   // the parent level's P(z|b,a) [nq][16]
-    const float *gbel;                 // grandparent beliefs
-    long long gstride;
-    const int32_t *gvmap;              // the parent level's work -> V-node map (or NULL)
-    CorrectArgs c;                     // geometry + motion model for correct_predict
-};
-
-template <uint32_t MASK, int K>
-__device__ void fused_stage(const FusedLeaf &f, const float *__restrict__ gb, const float (&w16)[16], float *tile,
-                            int TP, int row0, int TH, int t) {
-    const int W = f.c.W, G = (W + 3) >> 2;
-    const bool vec = (W & 3) == 0;
-    for (int i = t; i < TH * G; i += kPairThreads) {
-        const int tr = i / G, c0 = 4 * (i - tr * G);
-        const int r = row0 - 1 + tr;
-        float o[4] = {0.f, 0.f, 0.f, 0.f};
-        if (r >= 0 && r < f.c.H) {
-            float nbh[3][6];
-#pragma unroll
-            for (int dr = 0; dr < 3; ++dr) {
-                const int rr = r + dr - 1;
-                const bool rok = rr >= 0 && rr < f.c.H;
-                const float *row = gb + (long long)rr * W;
-                if (vec) {
-                    const float4 m4 = rok ? __ldg(reinterpret_cast<const float4 *>(row + c0)) : make_float4(0.f, 0.f, 0.f, 0.f);
-                    nbh[dr][0] = (rok && c0 > 0) ? __ldg(row + c0 - 1) : 0.f;
-                    nbh[dr][1] = m4.x; nbh[dr][2] = m4.y; nbh[dr][3] = m4.z; nbh[dr][4] = m4.w;
-                    nbh[dr][5] = (rok && c0 + 4 < W) ? __ldg(row + c0 + 4) : 0.f;
-                } else {
-#pragma unroll
-                    for (int j = 0; j < 6; ++j) {
-                        const int cc = c0 - 1 + j;
-                        nbh[dr][j] = (rok && cc >= 0 && cc < W) ? __ldg(row + cc) : 0.f;
-                    }
-                }
-            }
-            float bb[4];
-            int sg[4];
-            correct_predict<K>(f.c, r, c0, nbh, bb, sg);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) o[j] = w16[sg[j]] * bb[j];
-        }
-        if (vec) {
-            *reinterpret_cast<float4 *>(tile + tr * TP + 4 + c0) = make_float4(o[0], o[1], o[2], o[3]);
-        } else {
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-                if (c0 + j < W) tile[tr * TP + 4 + c0 + j] = o[j];
-        }
-    }
-}
-
 struct HistArgs {
     const float *beliefs;
     long long bstride;
@@ -599,19 +542,14 @@ struct HistArgs {
     const float4 *qlist;
     int H, W, TW, tstride, red_off, sums_off;
     int vec16;            // 16-byte cp.async staging (W % 4 == 0, 16-byte aligned rows)
-    int cluster;          // 1: bands of a pair form one cluster and reduce through DSMEM
     double *part;
     int pstride;
-    int fused;            // 1: the last band CTA of a pair runs reduce_parent (tickets[pair])
-    int *tickets;
-    ReduceArgs red;
     const int32_t *skip = nullptr;  // device flag (best-first)
     const long long *nwork_dev = nullptr;   // device-side parent count (graph-captured plan step)
-    int fused_leaf = 0;             // 1: stage the leaf parents from their parents (FusedLeaf)
-    FusedLeaf fl;
+    unsigned long long *skipped = nullptr;  // (CTA, band) tiles skipped (active-tile skipping)
 };
 
-template <uint32_t MASK, bool LEAF, bool FUSED = false, bool DEV = false>
+template <uint32_t MASK, bool LEAF, bool DEV = false>
 __global__ void __launch_bounds__(kPairThreads, 2) k_hist(HistArgs a) {
     constexpr int NA = mask_count(MASK);
     constexpr int NAP = (NA + 3) & ~3;
@@ -647,34 +585,7 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_hist(HistArgs a) {
         const float *__restrict__ b = a.beliefs + vv * a.bstride;
         float *tile = smem + pp * a.tstride;
         const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tile);
-        if (FUSED) {
-            if (vp) {
-                const int q = a.fl.parent_q[vv], z = a.fl.z[vv];
-                const int ww = q / NA, j = q - ww * NA;
-                const long long gw = a.fl.gvmap ? (long long)a.fl.gvmap[ww] : ww;
-                const float *__restrict__ gb = a.fl.gbel + gw * a.fl.gstride;
-                __shared__ float s_w16[2][16];
-                if (t < 16) s_w16[pp][t] = (float)(a.fl.c.O64[t * 16 + z] / a.fl.P[(long long)q * 16 + z]);
-                __syncthreads();
-                const float (&w16)[16] = s_w16[pp];
-                switch (action_of<MASK>(j)) {   // CTA-half uniform: compile-time tap geometry
-                    case 0: fused_stage<MASK, 0>(a.fl, gb, w16, tile, TP, row0, TH, t); break;
-                    case 1: fused_stage<MASK, 1>(a.fl, gb, w16, tile, TP, row0, TH, t); break;
-                    case 2: fused_stage<MASK, 2>(a.fl, gb, w16, tile, TP, row0, TH, t); break;
-                    case 3: fused_stage<MASK, 3>(a.fl, gb, w16, tile, TP, row0, TH, t); break;
-                    case 4: fused_stage<MASK, 4>(a.fl, gb, w16, tile, TP, row0, TH, t); break;
-                    case 5: fused_stage<MASK, 5>(a.fl, gb, w16, tile, TP, row0, TH, t); break;
-                    case 6: fused_stage<MASK, 6>(a.fl, gb, w16, tile, TP, row0, TH, t); break;
-                    case 7: fused_stage<MASK, 7>(a.fl, gb, w16, tile, TP, row0, TH, t); break;
-                    default: fused_stage<MASK, 8>(a.fl, gb, w16, tile, TP, row0, TH, t); break;
-                }
-            } else {
-                for (int i = t; i < TH * a.W; i += kPairThreads) {
-                    const int tr = i / a.W, c = i - tr * a.W;
-                    tile[tr * TP + 4 + c] = 0.f;
-                }
-            }
-        } else if (a.vec16) {
+        if (a.vec16) {
             // warp per tile row, lanes over the row's 16-byte groups (no index division)
             const int W4 = a.W >> 2;
             for (int tr = warp; tr < TH; tr += kPairThreads / 32) {
@@ -723,7 +634,8 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_hist(HistArgs a) {
                 const long long wp = 2 * pair + pp;
                 if (wp < nwork) a.part[(wp * a.nb + band) * (long long)a.pstride + oo] = 0.0;
             }
-            if (!a.cluster) return;
+            if (t == 0 && a.skipped) atomicAdd(a.skipped, 1ULL);
+            return;
         }
     }
     const float *tile = smem + p * a.tstride;
@@ -858,43 +770,10 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_hist(HistArgs a) {
         }
         __syncthreads();
     }
-    if (a.cluster) {
-        // sum the class totals of the cluster's bands in fixed rank order through DSMEM
-        namespace cg = cooperative_groups;
-        cg::cluster_group cl = cg::this_cluster();
-        cl.sync();
-        const int nr = a.nb, rank = band;
-        const int per = (2 * NOUT + nr - 1) / nr;
-        for (int o = rank * per + t; o < min(2 * NOUT, (rank + 1) * per); o += kPairThreads) {
-            const int pp = o / NOUT, oo = o % NOUT;
-            const long long wp = 2 * pair + pp;
-            double sm = 0.0;
-            for (int rr = 0; rr < nr; ++rr) sm += cl.map_shared_rank(sums, rr)[o];
-            if (wp < nwork) a.part[wp * (long long)a.pstride + oo] = sm;
-        }
-        cl.sync();
-    } else {
-        for (int o = t; o < 2 * NOUT; o += kPairThreads) {
-            const int pp = o / NOUT, oo = o % NOUT;
-            const long long wp = 2 * pair + pp;
-            if (wp < nwork) a.part[(wp * a.nb + band) * (long long)a.pstride + oo] = sums[o];
-        }
-        if (a.fused) {
-            // the last band CTA of this parent pair runs the pair's reduce/sample (k_reduce's
-            // work) while the band partials are still in L2; the ticket only picks who, the sum
-            // order over bands is fixed
-            __shared__ int s_last;
-            __threadfence();
-            __syncthreads();
-            if (t == 0) s_last = (atomicAdd(a.tickets + pair, 1) == a.nb - 1);
-            __syncthreads();
-            if (s_last) {
-                __threadfence();
-                double *rsm = reinterpret_cast<double *>(smem);
-                for (int pp = 0; pp < 2; ++pp)
-                    if (2 * pair + pp < nwork) reduce_parent<MASK, LEAF>(a.red, 2 * pair + pp, rsm, kPairThreads);
-            }
-        }
+    for (int o = t; o < 2 * NOUT; o += kPairThreads) {
+        const int pp = o / NOUT, oo = o % NOUT;
+        const long long wp = 2 * pair + pp;
+        if (wp < nwork) a.part[(wp * a.nb + band) * (long long)a.pstride + oo] = sums[o];
     }
 }
 
@@ -964,7 +843,10 @@ __global__ void __launch_bounds__(256) k_correct(CorrectArgs a) {
             unsigned rem = um;
             for (int i = 0; i < u; ++i) rem &= rem - 1;
             const int z = __ffs(rem) - 1;
-            s_w[sg][u] = (float)(a.O64[sg * 16 + z] / a.P[q * 16 + z]);
+            // a zero-likelihood z (only reachable through the belief_update ABI, which then reports
+            // QVTS_ERR_ZERO_LIKELIHOOD) writes zeros instead of O/0 = inf/NaN
+            const double pz = a.P[q * 16 + z];
+            s_w[sg][u] = pz > 1e-30 ? (float)(a.O64[sg * 16 + z] / pz) : 0.f;
             if (tile == 0 && sg == 0 && a.cpath) {
                 const long long c = base + u;
                 const int level = a.level >= 0 ? a.level : path_level(a.vpath[v]);
@@ -980,7 +862,7 @@ __global__ void __launch_bounds__(256) k_correct(CorrectArgs a) {
     // rows per pass
     const int W = a.W;
     const float *__restrict__ b = a.beliefs + v * a.bstride;
-    const bool vec = ((W & 3) == 0) && ((a.cstride & 3) == 0) && ((a.bstride & 3) == 0);
+    const bool vec = a.vec_in != 0;
     const int r_end = min(a.H, (tile + 1) * a.rows_cta);
     // staged path: the parent's rows [r0 - 1, r_end + 1) land in shared memory in one cp.async
     // burst (row pitch stage_tp, column c at c + 4, zero halo columns and off-map rows), so the
@@ -1056,7 +938,7 @@ __global__ void __launch_bounds__(256) k_correct(CorrectArgs a) {
         const long long x0 = (long long)r * W + c0;
         auto put = [&](int u, const float (&o)[4]) {
             float *dst = a.child + (base + u) * a.cstride + x0;
-            if (vec) {
+            if (a.vec_out) {
                 __stcs(reinterpret_cast<float4 *>(dst), make_float4(o[0], o[1], o[2], o[3]));   // streaming
             } else {
 #pragma unroll
@@ -1078,63 +960,6 @@ __global__ void __launch_bounds__(256) k_correct(CorrectArgs a) {
     }
 }
 
-// Fused leaf level: the leaf parents' metadata (what k_correct writes from its tile-0 blocks) and
-// their beliefs at the goal-term cells, with k_correct's arithmetic; no belief is written.
-template <uint32_t MASK>
-__global__ void __launch_bounds__(256) k_child_meta(CorrectArgs a, long long nq, const int32_t *__restrict__ fcells,
-                                                   int nf, float *__restrict__ goalv) {
-    constexpr int NA = mask_count(MASK);
-    const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (idx >= nq * 16) return;
-    const long long q = idx >> 4;
-    const int u = (int)(idx & 15);
-    const unsigned um = a.umask[q];
-    if (u >= __popc(um)) return;
-    unsigned rem = um;
-    for (int i = 0; i < u; ++i) rem &= rem - 1;
-    const int z = __ffs(rem) - 1;
-    const long long w = q / NA;
-    const int j = (int)(q % NA);
-    const int k = action_of<MASK>(j);
-    const long long v = a.vmap ? (long long)a.vmap[w] : w;
-    const long long c = a.off[q] + u;
-    a.cpath[c] = a.vpath[v] | ((uint64_t)(k + 1) << (8 * a.level)) | ((uint64_t)z << (8 * a.level + 4));
-    a.cparent[c] = (int32_t)q;
-    a.cz[c] = z;
-    a.cf[c] = a.cnt[q * 16 + z];
-    a.croot[c] = a.vroot[v];
-    const float *__restrict__ b = a.beliefs + v * a.bstride;
-    for (int f = 0; f < nf; ++f) {
-        const int x = fcells[f], r = x / a.W, cx = x % a.W, c0 = cx & ~3;
-        float nbh[3][6];
-        for (int dr = 0; dr < 3; ++dr) {
-            const int rr = r + dr - 1;
-            const bool rok = rr >= 0 && rr < a.H;
-            for (int jj = 0; jj < 6; ++jj) {
-                const int cc = c0 - 1 + jj;
-                nbh[dr][jj] = (rok && cc >= 0 && cc < a.W) ? __ldg(b + (long long)rr * a.W + cc) : 0.f;
-            }
-        }
-        float bb[4];
-        int sg[4];
-        switch (k) {
-            case 0: correct_predict<0>(a, r, c0, nbh, bb, sg); break;
-            case 1: correct_predict<1>(a, r, c0, nbh, bb, sg); break;
-            case 2: correct_predict<2>(a, r, c0, nbh, bb, sg); break;
-            case 3: correct_predict<3>(a, r, c0, nbh, bb, sg); break;
-            case 4: correct_predict<4>(a, r, c0, nbh, bb, sg); break;
-            case 5: correct_predict<5>(a, r, c0, nbh, bb, sg); break;
-            case 6: correct_predict<6>(a, r, c0, nbh, bb, sg); break;
-            case 7: correct_predict<7>(a, r, c0, nbh, bb, sg); break;
-            default: correct_predict<8>(a, r, c0, nbh, bb, sg); break;
-        }
-        const int i = cx - c0;
-        const float ws = (float)(a.O64[sg[i] * 16 + z] / a.P[q * 16 + z]);
-        goalv[c * nf + f] = ws * bb[i];
-    }
-}
-
-// ---- S6 backup ---------------------------------------------------------------------------------
 template <int NA>
 __global__ void k_vmax(const double *__restrict__ Q, double *__restrict__ V, long long nwork, const int32_t *vmap,
                        const long long *nwork_dev = nullptr) {
@@ -1189,14 +1014,13 @@ static inline unsigned nblk(long long n, int b) { return (unsigned)((n + b - 1) 
 // k_correct's shared-memory staging of the parent rows: on when the rows are 16-byte copyable and
 // the CTA's rows + halo fit the default 48 KB; returns the dynamic shared memory to launch with
 static size_t correct_stage(CorrectArgs &c) {
-    const bool vec = (c.W & 3) == 0 && (c.cstride & 3) == 0 && (c.bstride & 3) == 0 &&
-                     (reinterpret_cast<uintptr_t>(c.beliefs) & 15) == 0;
+    c.vec_in = ((c.W & 3) == 0 && (c.bstride & 3) == 0 && (reinterpret_cast<uintptr_t>(c.beliefs) & 15) == 0) ? 1 : 0;
+    c.vec_out = ((c.W & 3) == 0 && (c.cstride & 3) == 0 && (reinterpret_cast<uintptr_t>(c.child) & 15) == 0) ? 1 : 0;
+    const bool vec = c.vec_in != 0;
     const int tp = c.W + 8;
     const size_t bytes = sizeof(float) * (size_t)(c.rows_cta + 2) * tp;
-    static const int env = [] {
-        const char *ev = std::getenv("QVTS_CORRECT_STAGE");
-        return ev ? std::atoi(ev) : 1;
-    }();
+    const char *ev = std::getenv("QVTS_CORRECT_STAGE");     // read per call (tests flip it)
+    const int env = ev ? std::atoi(ev) : 1;
     c.stage_tp = (env && vec && bytes <= 48 * 1024) ? tp : 0;
     return c.stage_tp ? bytes : 0;
 }
@@ -1217,15 +1041,11 @@ static inline int correct_rows_per_cta(int H, int G) {
 template <uint32_t MASK, bool LEAF>
 static qvts_status launch_hist(Model &m, const BandSet &bs, const float *beliefs, long long bstride,
                                const int32_t *vmap, long long nwork, int pstride, cudaStream_t st, int *nb_eff,
-                               const ReduceArgs *red = nullptr, bool *fused_out = nullptr,
-                               const int32_t *skip = nullptr, const FusedLeaf *fl = nullptr,
-                               const long long *nwork_dev = nullptr, long long part_off = 0) {
+                               const int32_t *skip = nullptr, const long long *nwork_dev = nullptr) {
     constexpr int NOUT = 16 * hist_cb<MASK, LEAF>() + 8;
     HistArgs a;
     a.skip = skip;
     a.nwork_dev = nwork_dev;
-    a.fused_leaf = fl ? 1 : 0;
-    if (fl) a.fl = *fl;
     a.beliefs = beliefs; a.bstride = bstride; a.vmap = vmap; a.nwork = nwork;
     a.bands = bs.bands.as<BandInfo>(); a.nb = bs.nb;
     a.entries = bs.entries.as<uint32_t>();
@@ -1237,53 +1057,17 @@ static qvts_status launch_hist(Model &m, const BandSet &bs, const float *beliefs
     a.red_off = 0;
     a.sums_off = ((2 * kRedChunk * (kHistThreads + 1)) + 3) & ~3;
     const int region = std::max(2 * a.tstride, a.sums_off + 2 * 2 * NOUT);
-    // DSMEM cluster reduction over the bands of a parent pair: off by default (measured slower
-    // than writing one fp64 partial per band); QVTS_HIST_CLUSTER=1 enables it
-    static const int use_cluster = [] {
-        const char *ev = std::getenv("QVTS_HIST_CLUSTER");
-        return ev ? std::atoi(ev) : 0;
-    }();
-    a.cluster = (use_cluster && bs.nb <= 8 && !nwork_dev) ? 1 : 0;
-    a.part = m.part.as<double>() + part_off; a.pstride = pstride;
-    // fused reduce (the last band CTA of each pair runs reduce_parent): measured slower than a
-    // separate k_reduce launch, so off unless QVTS_FUSED_REDUCE=1
-    static const int use_fused = [] {
-        const char *ev = std::getenv("QVTS_FUSED_REDUCE");
-        return ev ? std::atoi(ev) : 0;
-    }();
-    a.fused = (use_fused && red && !a.cluster) ? 1 : 0;
-    a.tickets = nullptr;
-    if (a.fused) {
-        const long long npairs = (nwork + 1) / 2;
-        QVTS_TRY(m.tickets.ensure(sizeof(int) * npairs));
-        QVTS_CUDA(cudaMemsetAsync(m.tickets.p, 0, sizeof(int) * npairs, st));
-        a.tickets = m.tickets.as<int>();
-        a.red = *red;
-        a.red.nb = bs.nb;
-    }
-    if (fused_out) *fused_out = a.fused != 0;
-    const size_t smem = (size_t)std::max<size_t>((size_t)region * sizeof(float),
-                                                 a.fused ? sizeof(double) * reduce_smem_doubles<MASK, LEAF>(pstride) : 0);
-    auto kfn = (LEAF && fl) ? k_hist<MASK, LEAF, LEAF, false>
-                            : (nwork_dev ? k_hist<MASK, LEAF, false, true> : k_hist<MASK, LEAF, false, false>);
+    a.part = m.part.as<double>(); a.pstride = pstride;
+    a.skipped = m.counters.p ? m.counters.as<unsigned long long>() + 3 : nullptr;
+    const size_t smem = (size_t)region * sizeof(float);
+    auto kfn = nwork_dev ? k_hist<MASK, LEAF, true> : k_hist<MASK, LEAF, false>;
     QVTS_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const long long nblocks = ((nwork + 1) / 2) * bs.nb;
     if (nblocks > 0x7FFFFFFFLL) { set_error("too many hist blocks"); return QVTS_ERR_INVALID_ARG; }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)nblocks);
-    cfg.blockDim = dim3(kPairThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = a.cluster ? bs.nb : 1;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    QVTS_PROF(LEAF ? 0 : 1, QVTS_CUDA(cudaLaunchKernelEx(&cfg, kfn, a)));
+    QVTS_PROF(LEAF ? 0 : 1, kfn<<<(unsigned)nblocks, kPairThreads, smem, st>>>(a));
+    QVTS_CUDA(cudaGetLastError());
     (LEAF ? m.pstat.leaf_cells : m.pstat.hist_cells) += nwork * m.n_free;
-    *nb_eff = a.cluster ? 1 : bs.nb;
+    *nb_eff = bs.nb;
     return QVTS_OK;
 }
 
@@ -1312,122 +1096,6 @@ static int pstride_of(bool leaf) {
     return 16 * (leaf ? hist_cb<MASK, true>() : hist_cb<MASK, false>()) + 8;
 }
 
-// The last transition of a plan step with the leaf level pipelined behind it: the Q-nodes of level
-// D-2 are cut into chunks of about equal child counts; chunk i's k_correct (HBM-write bound, on a
-// high-priority stream) overlaps the leaf k_hist + k_reduce of chunk i-1's children (FP32-ALU
-// bound, second stream).  Same kernels and arithmetic per parent, so every value is bit-identical
-// to the unchunked sequence.  Sets up m.ql[D-1] / m.vl[D-1] as the leaf iteration would.
-// Opt-in (QVTS_LEAF_OVERLAP=<chunks>): measured no gain at C4 (55.5 ms off; 55.7 / 56.0 / 56.4 ms with
-// 4 / 8 / 16 chunks) -- the leaf k_hist's two CTAs per SM hold the whole register file, so k_correct
-// CTAs cannot co-reside and the two only interleave.
-static int leaf_overlap_chunks(long long nleaf) {
-    static const int env = [] {
-        const char *ev = std::getenv("QVTS_LEAF_OVERLAP");
-        return ev ? std::atoi(ev) : 0;
-    }();
-    if (env <= 1 || nleaf < 64LL * env) return 0;
-    return env;
-}
-
-template <uint32_t MASK>
-static qvts_status leaf_overlap(Model &m, const CorrectArgs &c0, long long nq, long long total, int D, int n,
-                                const qvts_plan_cfg &cfg, const RootBatch &roots, bool trace, int nch,
-                                cudaStream_t st) {
-    constexpr int NA = mask_count(MASK);
-    const int dl = D - 1;
-    VLevel &vl = m.vl[dl];
-    QLevel &ql = m.ql[dl];
-    // child offsets on the host (the stream was synchronised for the child count)
-    std::vector<int32_t> off((size_t)nq);
-    QVTS_CUDA(cudaMemcpy(off.data(), m.ql[dl - 1].off.p, sizeof(int32_t) * nq, cudaMemcpyDeviceToHost));
-    std::vector<long long> qb{0}, wb{0};
-    for (int i = 1; i < nch; ++i) {
-        const long long target = total * i / nch;
-        long long q = qb.back();
-        while (q < nq && off[(size_t)q] < target) ++q;
-        if (q > qb.back() && q < nq) { qb.push_back(q); wb.push_back(off[(size_t)q]); }
-    }
-    qb.push_back(nq);
-    wb.push_back(total);
-    // the leaf level's arrays, as the leaf iteration of plan_levels_t allocates them
-    const long long nwork = total, nql = nwork * NA;
-    ql.nwork = nwork; ql.mapped = false; ql.vmap_ptr = nullptr;
-    QVTS_TRY(ql.R.ensure(sizeof(double) * std::max(1LL, nql)));
-    QVTS_TRY(ql.P.ensure(sizeof(double) * 16 * std::max(1LL, nql)));
-    QVTS_TRY(ql.cnt.ensure(sizeof(uint16_t) * 16 * std::max(1LL, nql)));
-    QVTS_TRY(ql.umask.ensure(sizeof(uint16_t) * std::max(1LL, nql)));
-    QVTS_TRY(ql.U.ensure(sizeof(int32_t) * std::max(1LL, nql)));
-    QVTS_TRY(ql.off.ensure(sizeof(int32_t) * std::max(1LL, nql)));
-    QVTS_TRY(ql.Q.ensure(sizeof(double) * std::max(1LL, nql)));
-    if (trace) {
-        QVTS_TRY(ql.zdraw.ensure((size_t)std::max(1LL, nql) * n));
-        QVTS_TRY(ql.leafV.ensure(sizeof(double) * 16 * std::max(1LL, nql)));
-    }
-    double expect = 1.0;
-    for (int i = 0; i < dl; ++i) expect *= 10.0;
-    const BandSet &bs = expect < 100.0 ? m.band_small : m.band_big;
-    const int pstride = pstride_of<MASK>(true);
-    QVTS_TRY(m.part.ensure(sizeof(double) * (size_t)(nwork + 1) * std::max(bs.nb, leaf_mma_records()) * pstride));
-    // streams: k_correct chunks at high priority, leaf chunks at normal priority, both after st
-    if (!m.ov_corr) {
-        int lo = 0, hi = 0;
-        QVTS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        QVTS_CUDA(cudaStreamCreateWithPriority(&m.ov_corr, cudaStreamNonBlocking, hi));
-        QVTS_CUDA(cudaStreamCreateWithFlags(&m.ov_leaf, cudaStreamNonBlocking));
-        for (auto &e : m.ov_ev) QVTS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    }
-    const int nc = (int)qb.size() - 1;
-    if (nc + 2 > (int)(sizeof(m.ov_ev) / sizeof(m.ov_ev[0]))) { set_error("too many overlap chunks"); return QVTS_ERR_INVALID_ARG; }
-    QVTS_CUDA(cudaEventRecord(m.ov_ev[0], st));
-    QVTS_CUDA(cudaStreamWaitEvent(m.ov_corr, m.ov_ev[0], 0));
-    QVTS_CUDA(cudaStreamWaitEvent(m.ov_leaf, m.ov_ev[0], 0));
-    CorrectArgs c = c0;
-    const size_t csm = correct_stage(c);
-    for (int i = 0; i < nc; ++i) {
-        c.q0 = qb[i];
-        const long long nblocks = (qb[i + 1] - qb[i]) * c.ntiles;
-        cudaEvent_t e;
-        prof_begin(m, 5, m.ov_corr, &e);
-        k_correct<MASK><<<(unsigned)nblocks, 256, csm, m.ov_corr>>>(c);
-        prof_end(m, 5, m.ov_corr, e);
-        QVTS_CUDA(cudaGetLastError());
-        QVTS_CUDA(cudaEventRecord(m.ov_ev[2 + i], m.ov_corr));
-    }
-    m.pstat.correct_cells_written += total * (long long)m.HW;
-    for (int i = 0; i < nc; ++i) {
-        QVTS_CUDA(cudaStreamWaitEvent(m.ov_leaf, m.ov_ev[2 + i], 0));
-        const long long w0 = wb[i], cnt = wb[i + 1] - wb[i];
-        if (cnt <= 0) continue;
-        const float *bel = vl.belief.as<float>() + w0 * m.HWp;
-        int nb_eff = bs.nb;
-        QVTS_TRY((launch_hist<MASK, true>(m, bs, bel, m.HWp, nullptr, cnt, pstride, m.ov_leaf, &nb_eff, nullptr, nullptr,
-                                          nullptr, nullptr, nullptr, w0 * bs.nb * (long long)pstride)));
-        ReduceArgs r;
-        r.part = m.part.as<double>() + w0 * bs.nb * (long long)pstride; r.pstride = pstride; r.nb = nb_eff;
-        r.nwork = cnt; r.vmap = nullptr;
-        r.beliefs = bel; r.bstride = m.HWp; r.vpath = vl.path.as<uint64_t>() + w0; r.vroot = vl.root.as<int32_t>() + w0;
-        r.root_step = roots.step_dev; r.root_ep = roots.episode_dev; r.seed = cfg.seed;
-        r.level = dl; r.n = n; r.O64 = m.d_O64.as<double>();
-        r.ngc = m.ngc; r.gc_cell = m.d_gc_cell.as<int32_t>(); r.gc_act = m.d_gc_act.as<int32_t>();
-        r.gc_val = m.d_gc_val.as<double>(); r.goal = m.goal;
-        r.p_stay = m.p_stay; r.p_int = m.p_int; r.p_lat = m.p_lat; r.gamma = m.gamma;
-        r.qbar = m.cur_leaf == QVTS_LEAF_FIB ? m.qbar_fib : m.qbar;
-        const long long q0 = w0 * NA;
-        r.R = ql.R.as<double>() + q0; r.P = ql.P.as<double>() + 16 * q0; r.cnt = ql.cnt.as<uint16_t>() + 16 * q0;
-        r.umask = ql.umask.as<uint16_t>() + q0; r.U = ql.U.as<int32_t>() + q0;
-        r.zdraw = trace ? ql.zdraw.as<uint8_t>() + q0 * n : nullptr;
-        r.Q = ql.Q.as<double>() + q0; r.leafV = trace ? ql.leafV.as<double>() + 16 * q0 : nullptr;
-        r.counters = m.counters.as<unsigned long long>();
-        r.xs = nullptr; r.m8 = m.d_m8.as<uint8_t>(); r.sig = m.d_sig.as<uint8_t>(); r.W = m.W; r.acc = m.acc;
-        QVTS_TRY((launch_reduce<MASK, true>(m, r, m.ov_leaf)));
-    }
-    QVTS_CUDA(cudaEventRecord(m.ov_ev[1], m.ov_leaf));
-    QVTS_CUDA(cudaStreamWaitEvent(st, m.ov_ev[1], 0));
-    QVTS_CUDA(cudaEventRecord(m.ov_ev[0], m.ov_corr));
-    QVTS_CUDA(cudaStreamWaitEvent(st, m.ov_ev[0], 0));
-    return QVTS_OK;
-}
-
 template <uint32_t MASK>
 static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_plan_cfg &cfg, const qvts_comm *comm,
                                  cudaStream_t st, long long *nv_out) {
@@ -1451,13 +1119,6 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
     QVTS_CUDA(cudaMemsetAsync(m.counters.p, 0, sizeof(unsigned long long) * 4, st));
     QVTS_TRY(m.total.ensure(sizeof(long long)));
     nv_out[0] = roots.n;
-    // fused leaf level (FusedLeaf): measured slower than materialising the leaf parents (DESIGN
-    // §7: the in-kernel rebuild costs more than k_correct's HBM writes), so off unless
-    // QVTS_FUSED_LEAF=1; never with a trace or the ancestral sampler (they need the beliefs)
-    const char *ev_fused = std::getenv("QVTS_FUSED_LEAF");
-    const int env_fused = ev_fused ? std::atoi(ev_fused) : 0;
-    const bool fuse = env_fused && D >= 2 && !trace && cfg.sampler == QVTS_SAMPLER_MARGINAL;
-    bool leaf_done = false;                     // the leaf level ran inside leaf_overlap
 
     static const char *const kLevelNames[kMaxLevels] = {"qvts level 0", "qvts level 1", "qvts level 2",
                                                          "qvts level 3", "qvts level 4", "qvts level 5",
@@ -1506,7 +1167,8 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
             for (int i = 0; i < d; ++i) expect *= 10.0;
             const BandSet &bs = expect < 100.0 ? m.band_small : m.band_big;
             const int pstride = pstride_of<MASK>(leaf);
-            QVTS_TRY(m.part.ensure(sizeof(double) * (size_t)(nwork + 1) * std::max(bs.nb, leaf_mma_records()) * pstride));
+            QVTS_TRY(m.part.ensure(sizeof(double) * (size_t)(nwork + 1) *
+                                   std::max({bs.nb, m.leafb.nb, leaf_mma_records()}) * pstride));
             int nb_eff = bs.nb;
             ReduceArgs r;
             r.part = m.part.as<double>(); r.pstride = pstride; r.nb = bs.nb; r.nwork = nwork; r.vmap = vmap;
@@ -1524,41 +1186,30 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
             r.counters = m.counters.as<unsigned long long>();
             r.xs = nullptr; r.m8 = m.d_m8.as<uint8_t>(); r.sig = m.d_sig.as<uint8_t>(); r.W = m.W; r.acc = m.acc;
             if (cfg.sampler == QVTS_SAMPLER_ANCESTRAL) {
-                QVTS_TRY(m.xs.ensure(sizeof(int32_t) * (size_t)nq * n));
+                // with a trace, every level keeps its state draws (qvts_trace_state_draws)
+                DevBuf &xb = trace ? ql.xdraw : m.xs;
+                QVTS_TRY(xb.ensure(sizeof(int32_t) * (size_t)nq * n));
                 const int nch = (m.HW + 255) / 256;
                 QVTS_PROF(7, k_ancestral_x<MASK><<<(unsigned)nwork, 256, sizeof(double) * (2 * nch + 1), st>>>(
                                  bel, bstride, vmap, nwork, m.HW, vl.path.as<uint64_t>(), vl.root.as<int32_t>(),
-                                 roots.step_dev, roots.episode_dev, cfg.seed, d, n, m.xs.as<int32_t>()));
+                                 roots.step_dev, roots.episode_dev, cfg.seed, d, n, xb.as<int32_t>()));
                 QVTS_CUDA(cudaGetLastError());
-                r.xs = m.xs.as<int32_t>();
+                r.xs = xb.as<int32_t>();
             }
-            bool fused = false;
-            FusedLeaf fl;
-            if (leaf && fuse) {
-                const int dg = D - 2;                       // the leaf parents' parents
-                fl.parent_q = vl.parent_q.as<int32_t>(); fl.z = vl.z.as<int32_t>();
-                fl.P = m.ql[dg].P.as<double>();
-                fl.gbel = dg == 0 ? roots.beliefs : m.vl[dg].belief.as<float>();
-                fl.gstride = dg == 0 ? roots.stride : m.HWp;
-                fl.gvmap = m.ql[dg].vmap_ptr;
-                std::memset(&fl.c, 0, sizeof(fl.c));
-                fl.c.m8 = m.d_m8.as<uint8_t>(); fl.c.cell = m.d_cell.as<uint8_t>(); fl.c.O64 = m.d_O64.as<double>();
-                fl.c.H = m.H; fl.c.W = m.W; fl.c.G = (m.W + 3) / 4;
-                fl.c.p_int = (float)m.p_int; fl.c.p_stay = (float)m.p_stay; fl.c.p_lat = (float)m.p_lat;
-                r.goalv = m.fl_goalv.as<float>(); r.nf = m.nfcells; r.gc_fidx = m.d_gc_fidx.as<int32_t>();
-            }
-            const ReduceArgs *rf = r.xs ? nullptr : &r;   // the fused reduce has no x draws
-            if (leaf && !fuse && leaf_mma_enabled(m, bstride, bel)) {
+            if (leaf && leaf_mma_enabled(m, bstride, bel)) {
                 QVTS_TRY(launch_leaf_mma_prof(m, bel, bstride, vmap, nwork, pstride, st, nullptr, nullptr));
                 nb_eff = leaf_mma_records();
-            } else if (leaf) QVTS_TRY((launch_hist<MASK, true>(m, bs, bel, bstride, vmap, nwork, pstride, st, &nb_eff, rf, &fused,
-                                                        nullptr, fuse ? &fl : nullptr)));
-            else QVTS_TRY((launch_hist<MASK, false>(m, bs, bel, bstride, vmap, nwork, pstride, st, &nb_eff, rf, &fused)));
+            } else if (leaf && leaf_kernel_supported(m)) {
+                nb_eff = leaf_nsplit(m, d);
+                QVTS_TRY(launch_leaf(m, bel, bstride, d == 0 ? roots.n : vl.n, vmap, nwork, nb_eff, pstride, 0, st));
+            } else if (leaf) {
+                QVTS_TRY((launch_hist<MASK, true>(m, bs, bel, bstride, vmap, nwork, pstride, st, &nb_eff)));
+            } else {
+                QVTS_TRY((launch_hist<MASK, false>(m, bs, bel, bstride, vmap, nwork, pstride, st, &nb_eff)));
+            }
             r.nb = nb_eff;
-            if (!fused) {
             if (leaf) QVTS_TRY((launch_reduce<MASK, true>(m, r, st)));
             else QVTS_TRY((launch_reduce<MASK, false>(m, r, st)));
-            }
             QVTS_CUDA(cudaGetLastError());
         }
         if (leaf) break;
@@ -1580,16 +1231,7 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
         QVTS_TRY(vc.f.ensure(sizeof(int32_t) * tn));
         QVTS_TRY(vc.root.ensure(sizeof(int32_t) * tn));
         QVTS_TRY(vc.V.ensure(sizeof(double) * tn));
-        const bool meta_only = fuse && d + 1 == D - 1;   // leaf parents: metadata + goal-term cells only
-        // pipeline the leaf level behind this k_correct (leaf_overlap): not when the leaf level
-        // would become the shard level (its parents then need a rank map), nor for the options
-        // that need the whole level at once (ancestral draws, tensor-core leaf, fused leaf)
-        const bool leaf_sharded = G > 1 && shard_level < 0 && total >= shard_min;
-        const int overlap_nch = (d + 1 == D - 1 && !meta_only && !leaf_sharded &&
-                                 cfg.sampler == QVTS_SAMPLER_MARGINAL && !leaf_mma_enabled(m, m.HWp, nullptr))
-                                    ? leaf_overlap_chunks(total) : 0;
-        if (meta_only) QVTS_TRY(m.fl_goalv.ensure(sizeof(float) * (size_t)tn * std::max(1, m.nfcells)));
-        else QVTS_TRY(vc.belief.ensure(sizeof(float) * (size_t)tn * m.HWp));
+        QVTS_TRY(vc.belief.ensure(sizeof(float) * (size_t)tn * m.HWp));
         if (nq > 0) {
             CorrectArgs c;
             c.beliefs = bel; c.bstride = bstride; c.vmap = vmap;
@@ -1607,20 +1249,12 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
             c.sel_q = c.sel_z = c.sel_out = nullptr;
             const long long nblocks = nq * c.ntiles;
             if (nblocks > 0x7FFFFFFFLL) { set_error("too many correct blocks"); return QVTS_ERR_INVALID_ARG; }
-            if (meta_only) {
-                QVTS_PROF(5, k_child_meta<MASK><<<nblk(nq * 16, 256), 256, 0, st>>>(c, nq, m.d_fcells.as<int32_t>(),
-                                                                                 m.nfcells, m.fl_goalv.as<float>()));
-            } else if (overlap_nch) {
-                QVTS_TRY(leaf_overlap<MASK>(m, c, nq, total, D, n, cfg, roots, trace, overlap_nch, st));
-                leaf_done = true;
-            } else {
-                { const size_t csm_ = correct_stage(c);
-                QVTS_PROF(5, k_correct<MASK><<<(unsigned)nblocks, 256, csm_, st>>>(c)); }
-                m.pstat.correct_cells_written += total * (long long)m.HW;
-            }
+            const size_t csm = correct_stage(c);
+            QVTS_PROF(5, k_correct<MASK><<<(unsigned)nblocks, 256, csm, st>>>(c));
+            m.pstat.correct_cells_written += total * (long long)m.HW;
             QVTS_CUDA(cudaGetLastError());
         }
-        if (leaf_done) break;
+
     }
     // S6 backup, bottom-up
     for (int d = D - 1; d >= 0; --d) {
@@ -1648,12 +1282,14 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
             }
         }
     }
-    // leaf V-node count (not materialised) and flagged-draw count, accumulated by k_reduce
-    unsigned long long cnts[2] = {0, 0};
+    // leaf V-node count (not materialised), flagged-draw count (k_reduce) and skipped tiles
+    unsigned long long cnts[4] = {0, 0, 0, 0};
     QVTS_CUDA(cudaMemcpyAsync(cnts, m.counters.p, sizeof(cnts), cudaMemcpyDeviceToHost, st));
     QVTS_CUDA(cudaStreamSynchronize(st));
     nv_out[D] = (long long)cnts[1];
     m.last_flagged = (long long)cnts[0];
+    m.last_skipped = (long long)(cnts[2] + cnts[3]);
+    m.last_xdraws = trace && cfg.sampler == QVTS_SAMPLER_ANCESTRAL;
     m.last_depth = D;
     m.last_shard_level = shard_level;
     m.last_n = n;
@@ -1725,17 +1361,21 @@ static qvts_status plan_levels_dev_t(Model &m, const float *root, const qvts_pla
             const int nch = (m.HW + 255) / 256;
             QVTS_PROF(7, k_ancestral_x<MASK><<<(unsigned)nwork, 256, sizeof(double) * (2 * nch + 1), st>>>(
                              bel, bstride, nullptr, nwork, m.HW, vl.path.as<uint64_t>(), vl.root.as<int32_t>(),
-                             r.root_step, r.root_ep, cfg.seed, d, n, m.xs.as<int32_t>()));
+                             r.root_step, r.root_ep, cfg.seed, d, n, m.xs.as<int32_t>(), nullptr, cnt + d));
             r.xs = m.xs.as<int32_t>();
         }
         int nb_eff = bs.nb;
         if (leaf && leaf_mma_enabled(m, bstride, bel)) {
             QVTS_TRY(launch_leaf_mma_prof(m, bel, bstride, nullptr, nwork, pstride, st, nullptr, cnt + d));
             nb_eff = leaf_mma_records();
-        } else if (leaf) QVTS_TRY((launch_hist<MASK, true>(m, bs, bel, bstride, nullptr, nwork, pstride, st, &nb_eff, nullptr,
-                                                    nullptr, nullptr, nullptr, cnt + d)));
-        else QVTS_TRY((launch_hist<MASK, false>(m, bs, bel, bstride, nullptr, nwork, pstride, st, &nb_eff, nullptr,
-                                                 nullptr, nullptr, nullptr, cnt + d)));
+        } else if (leaf && leaf_kernel_supported(m)) {
+            nb_eff = leaf_nsplit(m, d);
+            QVTS_TRY(launch_leaf(m, bel, bstride, std::max(1LL, vmax[d]), nullptr, nwork, nb_eff, pstride, 0, st, cnt + d));
+        } else if (leaf) {
+            QVTS_TRY((launch_hist<MASK, true>(m, bs, bel, bstride, nullptr, nwork, pstride, st, &nb_eff, nullptr, cnt + d)));
+        } else {
+            QVTS_TRY((launch_hist<MASK, false>(m, bs, bel, bstride, nullptr, nwork, pstride, st, &nb_eff, nullptr, cnt + d)));
+        }
         r.nb = nb_eff;
         if (leaf) QVTS_TRY((launch_reduce<MASK, true>(m, r, st)));
         else QVTS_TRY((launch_reduce<MASK, false>(m, r, st)));
@@ -1813,8 +1453,8 @@ static qvts_status plan_dev_prepare_t(Model &m, const qvts_plan_cfg &cfg, const 
             double expect = 1.0;
             for (int i = 0; i < d; ++i) expect *= 10.0;
             const BandSet &bs = expect < 100.0 ? m.band_small : m.band_big;
-            part = std::max(part, sizeof(double) * (size_t)(tn + 1) * std::max(bs.nb, leaf_mma_records()) *
-                                      pstride_of<MASK>(d == D - 1));
+            part = std::max(part, sizeof(double) * (size_t)(tn + 1) *
+                                      std::max({bs.nb, m.leafb.nb, leaf_mma_records()}) * pstride_of<MASK>(d == D - 1));
             if (cfg.sampler == QVTS_SAMPLER_ANCESTRAL)
                 QVTS_TRY(m.xs.ensure(sizeof(int32_t) * (size_t)nq * cfg.n_samples));
         }
@@ -1992,8 +1632,7 @@ static qvts_status bf_expand_launch_t(Model &m, const BfLaunch &L, QLevel &ql, c
         r.xs = m.xs.as<int32_t>();
     }
     int nb_eff = bs.nb;
-    QVTS_TRY((launch_hist<MASK, false>(m, bs, L.bel, L.stride, L.sel, 1, pstride, st, &nb_eff, nullptr, nullptr,
-                                       L.skip)));
+    QVTS_TRY((launch_hist<MASK, false>(m, bs, L.bel, L.stride, L.sel, 1, pstride, st, &nb_eff, L.skip)));
     r.nb = nb_eff;
     QVTS_TRY((launch_reduce<MASK, false>(m, r, st)));
     QVTS_PROF(4, k_scan<<<1, 1024, 0, st>>>(ql.U.as<int32_t>(), ql.off.as<int32_t>(), NA, L.total, L.skip));
@@ -2116,6 +1755,16 @@ static qvts_status plan_step_graph(Model &m, const float *root_dev, const qvts_p
                                   (uintptr_t)cfg.sampler, (uintptr_t)cfg.leaf_bound, (uintptr_t)m.part.p,
                                   (uintptr_t)m.lvl_cnt.p, (uintptr_t)m.counters.p, (uintptr_t)m.root_buf.p,
                                   (uintptr_t)m.xs.p, (uintptr_t)m.ep_root_step.p, (uintptr_t)m.ep_root_ep.p};
+    // the leaf offset qbar is a kernel argument captured by value: a later value / FIB iteration
+    // with another qbar (or rebuilt Q' lists) must re-capture
+    uint64_t qb_bits[2];
+    std::memcpy(&qb_bits[0], &m.qbar, sizeof(double));
+    std::memcpy(&qb_bits[1], &m.qbar_fib, sizeof(double));
+    key.push_back((uintptr_t)qb_bits[0]);
+    key.push_back((uintptr_t)qb_bits[1]);
+    for (const DevBuf *b : {&m.band_big.qlist, &m.band_big.qlist_fib, &m.band_small.qlist, &m.band_small.qlist_fib,
+                            &m.leafb.qlist, &m.leafb.qlist_fib})
+        key.push_back((uintptr_t)b->p);
     for (int d = 0; d <= cfg.depth; ++d) {
         const VLevel &vl = m.vl[d];
         for (const DevBuf *b : {&vl.path, &vl.parent_q, &vl.z, &vl.f, &vl.root, &vl.V, &vl.belief}) key.push_back((uintptr_t)b->p);
@@ -2141,16 +1790,21 @@ static qvts_status plan_step_graph(Model &m, const float *root_dev, const qvts_p
     QVTS_CUDA(cudaGraphLaunch(m.pg_exec, st));
     QVTS_CUDA(cudaEventRecord(m.ev1, st));
     long long cnt[kMaxLevels + 1];
-    unsigned long long ctr[2];
+    unsigned long long ctr[4];
     QVTS_CUDA(cudaMemcpyAsync(q, m.ql[0].Q.p, sizeof(double) * m.NA, cudaMemcpyDeviceToHost, st));
     QVTS_CUDA(cudaMemcpyAsync(cnt, m.lvl_cnt.p, sizeof(long long) * cfg.depth, cudaMemcpyDeviceToHost, st));
     QVTS_CUDA(cudaMemcpyAsync(ctr, m.counters.p, sizeof(ctr), cudaMemcpyDeviceToHost, st));
     QVTS_CUDA(cudaStreamSynchronize(st));
     QVTS_CUDA(cudaEventRecord(m.pg_join, st));
     QVTS_CUDA(cudaStreamWaitEvent(cst, m.pg_join, 0));
-    for (int d = 0; d < cfg.depth; ++d) { nv[d] = cnt[d]; m.vl[d].n = cnt[d]; m.ql[d].nwork = cnt[d]; }
+    for (int d = 0; d < cfg.depth; ++d) {
+        nv[d] = cnt[d]; m.vl[d].n = cnt[d]; m.ql[d].nwork = cnt[d];
+        m.ql[d].mapped = false; m.ql[d].vmap_ptr = nullptr;    // the graph's levels are unmapped
+    }
     nv[cfg.depth] = (long long)ctr[1];
     m.last_flagged = (long long)ctr[0];
+    m.last_skipped = (long long)(ctr[2] + ctr[3]);
+    m.last_xdraws = false;
     m.last_depth = cfg.depth;
     m.last_shard_level = -1;
     m.last_n = cfg.n_samples;
@@ -2229,6 +1883,8 @@ extern "C" qvts_status qvts_plan_step(qvts_model *m, const float *root_dev, cons
     }
     res->n_belief_updates = tot;
     res->device_ms = ms;
+    res->n_flag_candidates = m->last_flagged;
+    res->n_tiles_skipped = m->last_skipped;
     return QVTS_OK;
 }
 
@@ -2255,7 +1911,7 @@ __global__ void __launch_bounds__(256) k_bu_marg(CorrectArgs a, double *__restri
     const int j = (int)(q % NA), k = action_of<MASK>(j);
     const float *__restrict__ b = a.beliefs + (q / NA) * a.bstride;
     const int W = a.W;
-    const bool vec = ((W & 3) == 0) && ((a.bstride & 3) == 0);
+    const bool vec = a.vec_in != 0;                 // set on the host (alignment of b included)
     __shared__ float s_o[16];                       // O[s][z] of the selected z
     if (threadIdx.x < 16) s_o[threadIdx.x] = (float)a.O64[threadIdx.x * 16 + a.sel_z[grp]];
     __syncthreads();
@@ -2313,6 +1969,115 @@ __global__ void __launch_bounds__(256) k_bu_marg(CorrectArgs a, double *__restri
         part[grp * a.ntiles + tile] = sm;
     }
 }
+// Batched Eq. 3 in ONE pass over b (K9 at HBM rate): one thread-block cluster per belief, CTA
+// rank r owns rows [r R, (r+1) R).  Each CTA stages its rows (+1-row halo) in shared memory with
+// one cp.async burst, forms its part of P(z|b,a) = sum_y O[sig(y)][z] bbar_a(y) (fp64 per thread,
+// fixed-order block reduction), the cluster sums the NC parts in rank order through DSMEM (every
+// CTA gets the same bits), and each CTA then writes b' = (O[s][z] / P) bbar_a from the staged
+// rows with streaming float4 stores -- b is read once and b' written once (the two-pass path
+// reads b twice).  Same fp32 prediction and weights as k_correct (correct_predict).
+template <uint32_t MASK>
+__global__ void __launch_bounds__(256) k_bu_cluster(CorrectArgs a, double *__restrict__ pout) {
+    namespace cg = cooperative_groups;
+    constexpr int NA = mask_count(MASK);
+    cg::cluster_group cl = cg::this_cluster();
+    const int NC = (int)cl.num_blocks();
+    const int rank = (int)cl.block_rank();
+    const long long grp = blockIdx.x / NC;
+    const long long q = a.sel_q[grp];
+    const int zsel = a.sel_z[grp];
+    const int j = (int)(q % NA), k = action_of<MASK>(j);
+    const float *__restrict__ b = a.beliefs + (q / NA) * a.bstride;
+    const int W = a.W, TPc = a.stage_tp;
+    const int r0 = rank * a.rows_cta, r1 = min(a.H, r0 + a.rows_cta);
+    extern __shared__ float4 bu_smem4[];
+    float *stile = reinterpret_cast<float *>(bu_smem4);
+    __shared__ float s_o[16];
+    __shared__ double wsum[8], s_part;
+    __shared__ float s_w[16];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x < 16) s_o[threadIdx.x] = (float)a.O64[threadIdx.x * 16 + zsel];
+    // stage rows [r0 - 1, r1 + 1): off-map rows and the halo columns are zero
+    const int nr = r1 - r0 + 2, W4 = W >> 2;
+    for (int tr = warp; tr < nr; tr += 8) {
+        const int rr = r0 - 1 + tr;
+        const bool ok = rr >= 0 && rr < a.H;
+        const float *src = ok ? b + (long long)rr * W : b;
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(stile + tr * TPc + 4);
+        for (int c4 = lane; c4 < W4; c4 += 32)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst + 16u * c4),
+                         "l"(ok ? src + 4 * c4 : src), "r"(ok ? 16 : 0));
+        if (lane == 0) {
+            stile[tr * TPc + 3] = 0.f;
+            stile[tr * TPc + 4 + W] = 0.f;
+        }
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+    auto predict = [&](int r, int c0, float (&bb)[4], int (&sg)[4]) {
+        float nbh[3][6];
+#pragma unroll
+        for (int dr = 0; dr < 3; ++dr) {
+            const float *row = stile + (r - r0 + dr) * TPc + 4 + c0;
+            const float4 m4 = *reinterpret_cast<const float4 *>(row);
+            nbh[dr][0] = row[-1];
+            nbh[dr][1] = m4.x; nbh[dr][2] = m4.y; nbh[dr][3] = m4.z; nbh[dr][4] = m4.w;
+            nbh[dr][5] = row[4];
+        }
+        switch (k) {   // block-uniform: compile-time tap geometry per action
+            case 0: correct_predict<0>(a, r, c0, nbh, bb, sg); break;
+            case 1: correct_predict<1>(a, r, c0, nbh, bb, sg); break;
+            case 2: correct_predict<2>(a, r, c0, nbh, bb, sg); break;
+            case 3: correct_predict<3>(a, r, c0, nbh, bb, sg); break;
+            case 4: correct_predict<4>(a, r, c0, nbh, bb, sg); break;
+            case 5: correct_predict<5>(a, r, c0, nbh, bb, sg); break;
+            case 6: correct_predict<6>(a, r, c0, nbh, bb, sg); break;
+            case 7: correct_predict<7>(a, r, c0, nbh, bb, sg); break;
+            default: correct_predict<8>(a, r, c0, nbh, bb, sg); break;
+        }
+    };
+    const int ngrp = (r1 - r0) * a.G;
+    double acc = 0.0;
+    for (int idx = threadIdx.x; idx < ngrp; idx += 256) {
+        const int r = r0 + idx / a.G, c0 = 4 * (idx % a.G);
+        float bb[4];
+        int sg[4];
+        predict(r, c0, bb, sg);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc += (double)(s_o[sg[i]] * bb[i]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) wsum[warp] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double sm = 0.0;
+#pragma unroll
+        for (int w2 = 0; w2 < 8; ++w2) sm += wsum[w2];
+        s_part = sm;
+    }
+    cl.sync();                                   // every rank's part is in its shared memory
+    if (threadIdx.x < 16) {
+        double P = 0.0;
+        for (int rr = 0; rr < NC; ++rr) P += *cl.map_shared_rank(&s_part, rr);   // rank order
+        // a zero-likelihood z writes zeros (the host reports QVTS_ERR_ZERO_LIKELIHOOD)
+        s_w[threadIdx.x] = P > 1e-30 ? (float)(a.O64[threadIdx.x * 16 + zsel] / P) : 0.f;
+        if (threadIdx.x == 0 && rank == 0) pout[grp] = P;
+    }
+    cl.sync();                                   // no CTA leaves while another reads its part
+    float *outp = a.child + (long long)a.sel_out[grp] * a.cstride;
+    for (int idx = threadIdx.x; idx < ngrp; idx += 256) {
+        const int r = r0 + idx / a.G, c0 = 4 * (idx % a.G);
+        float bb[4];
+        int sg[4];
+        predict(r, c0, bb, sg);
+        float o[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) o[i] = s_w[sg[i]] * bb[i];
+        __stcs(reinterpret_cast<float4 *>(outp + (long long)r * W + c0), make_float4(o[0], o[1], o[2], o[3]));
+    }
+}
+
 // P(z | b, a) of each selected pair: the tile partials summed in order, into the Q-node layout
 // k_correct reads (P[q][z]) and the caller's per-belief array
 __global__ void k_bu_p(const double *__restrict__ part, int ntiles, const int32_t *__restrict__ sel_q,
@@ -2355,10 +2120,8 @@ extern "C" qvts_status qvts_belief_update_batch(qvts_model *m, const float *b_de
     c.beliefs = b_dev; c.bstride = b_stride; c.m8 = m->d_m8.as<uint8_t>(); c.cell = m->d_cell.as<uint8_t>();
     c.O64 = m->d_O64.as<double>(); c.H = m->H; c.W = m->W; c.G = (m->W + 3) / 4;
     // CTAs of ~BU_GROUPS groups of 4 cells (the plan's 1024 leave the one-child case latency-bound)
-    static const int bu_groups = [] {
-        const char *ev = std::getenv("QVTS_BU_GROUPS");
-        return ev ? std::max(256, std::atoi(ev)) : 2048;   // 32-row tiles at W = 256: k_correct stages them
-    }();
+    const char *ev_groups = std::getenv("QVTS_BU_GROUPS");     // read per call
+    const int bu_groups = ev_groups ? std::max(256, std::atoi(ev_groups)) : 2048;   // 32-row tiles at W = 256
     c.rows_cta = std::min(m->H, std::max(1, bu_groups / std::max(1, c.G)));
     c.ntiles = (m->H + c.rows_cta - 1) / c.rows_cta;
     c.p_int = (float)m->p_int; c.p_stay = (float)m->p_stay; c.p_lat = (float)m->p_lat; c.qsel = -1;
@@ -2369,8 +2132,55 @@ extern "C" qvts_status qvts_belief_update_batch(qvts_model *m, const float *b_de
     c.P = m->bu_R.as<double>();
     const long long nblocks = (long long)n * c.ntiles;
     if (nblocks > 0x7FFFFFFFLL) { set_error("batch too large"); return QVTS_ERR_INVALID_ARG; }
+    // one pass per belief on a thread-block cluster when the rows fit (16-byte rows, <= 8 CTAs of
+    // <= ~56 KB staged rows each); otherwise the two-pass path (normaliser, then k_correct)
+    {
+        const bool vec = (m->W & 3) == 0 && (b_stride & 3) == 0 && (out_stride & 3) == 0 &&
+                         (reinterpret_cast<uintptr_t>(b_dev) & 15) == 0 && (reinterpret_cast<uintptr_t>(out_dev) & 15) == 0;
+        const int tp = m->W + 8;
+        const int max_rows = std::max(1, (56 * 1024) / (4 * tp) - 2);
+        const int NC = (m->H + max_rows - 1) / max_rows;
+        const char *ev_bu = std::getenv("QVTS_BU_CLUSTER");          // read per call (0: two-pass path)
+        if (vec && NC <= 8 && (!ev_bu || std::atoi(ev_bu) != 0) && (long long)n * NC <= 0x7FFFFFFFLL) {
+            CorrectArgs cc = c;
+            cc.rows_cta = (m->H + NC - 1) / NC;
+            cc.stage_tp = tp;
+            const size_t smem = sizeof(float) * (size_t)(cc.rows_cta + 2) * tp;
+            cudaLaunchConfig_t lc = {};
+            lc.gridDim = dim3((unsigned)(n * NC));
+            lc.blockDim = dim3(256);
+            lc.dynamicSmemBytes = smem;
+            lc.stream = st;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = NC;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            lc.attrs = attr;
+            lc.numAttrs = 1;
+#define QVTS_BUC(MASK)                                                                                          \
+    {                                                                                                           \
+        QVTS_CUDA(cudaFuncSetAttribute(k_bu_cluster<MASK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+        QVTS_CUDA(cudaLaunchKernelEx(&lc, k_bu_cluster<MASK>, cc, m->bu_P.as<double>()));                       \
+    }
+            QVTS_DISPATCH_MASK(m->mask, QVTS_BUC);
+#undef QVTS_BUC
+            QVTS_CUDA(cudaGetLastError());
+            std::vector<double> p(n);
+            QVTS_CUDA(cudaMemcpyAsync(p.data(), m->bu_P.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+            QVTS_CUDA(cudaStreamSynchronize(st));
+            bool zero = false;
+            for (int g = 0; g < n; ++g) {
+                if (p_obs_out) p_obs_out[g] = p[g];
+                if (!(p[g] > 1e-30)) zero = true;
+            }
+            if (zero) { set_error("zero-likelihood observation in the batch"); return QVTS_ERR_ZERO_LIKELIHOOD; }
+            return QVTS_OK;
+        }
+    }
 #define QVTS_BUB(MASK)                                                                                          \
     {                                                                                                           \
+        correct_stage(c);                                                                                       \
         k_bu_marg<MASK><<<(unsigned)nblocks, 256, 0, st>>>(c, m->part.as<double>());                            \
         k_bu_p<<<nblk(n, 256), 256, 0, st>>>(m->part.as<double>(), c.ntiles, d_sel, d_sel + n, n,               \
                                              m->bu_R.as<double>(), m->bu_P.as<double>());                        \
@@ -2473,6 +2283,15 @@ extern "C" qvts_status qvts_trace_belief(const qvts_model *m, int32_t level, int
 }
 
 // Number of V-nodes per level of the last plan step (levels 0..depth) — convenience for bindings.
+extern "C" qvts_status qvts_trace_state_draws(const qvts_model *m, int32_t level, int32_t *x) {
+    QVTS_TRY(check_level(m, level, true));
+    if (!x) { set_error("NULL argument"); return QVTS_ERR_INVALID_ARG; }
+    if (!m->last_xdraws) { set_error("state draws need want_trace and the ancestral sampler"); return QVTS_ERR_STATE; }
+    QVTS_CUDA(cudaSetDevice(m->device));
+    const QLevel &ql = m->ql[level];
+    return d2h(x, ql.xdraw, (size_t)ql.nwork * m->NA * m->last_n);
+}
+
 extern "C" qvts_status qvts_trace_counts(const qvts_model *m, int32_t *depth, int64_t *n_v, int64_t *n_qwork) {
     if (!m) { set_error("model is NULL"); return QVTS_ERR_INVALID_ARG; }
     if (m->last_depth < 0) { set_error("no plan step has run"); return QVTS_ERR_STATE; }

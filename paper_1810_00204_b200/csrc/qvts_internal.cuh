@@ -69,6 +69,26 @@ struct BandSet {
     DevBuf bands, entries, slot_cell, qlist, qlist_fib;
 };
 
+// Leaf level (leaf.cu): one CTA of kLeafThreads slot-threads per PAIR of leaf parents walks every
+// row band of the grid; slot-thread t owns wall-signature class cls(t) in every band (class slot
+// ranges fixed for the whole grid), so its fp32 accumulators run across all bands and the class
+// reduction happens once per parent pair: one fp64 partial record per parent (per band group).
+constexpr int kLeafThreads = 128;
+struct LeafBand {
+    int row0, nrows, L, pad;      // L = steps of this band (multiple of 4); entries padded by 8 more steps
+    long long slot_off;           // slot (i, t) of this band = slot_off + i * kLeafThreads + t
+};
+struct LeafBands {
+    int nb = 0, rows = 0, TP = 0, TS = 0;   // segment row pitch; one parent's tile (all segments), floats
+    int nseg = 1, SW = 0, HB = 0;            // column segments of SW cells (grid column c of segment s at
+                                             // c - s SW + 4 of its rows), segment stride HB
+    int cs[17] = {0};                        // slot-threads [cs[c], cs[c+1]) own class c in every band
+    long long total_slots = 0, steps = 0;    // steps = sum of the bands' L (padding included)
+    std::vector<LeafBand> h_bands;
+    std::vector<int32_t> h_slot_cell;
+    DevBuf bands, entries, slot_cell, qlist, qlist_fib;
+};
+
 // Tensor-core leaf level (leafmma.cu): per row band, the free cells sorted by wall-signature class
 // and cut into chunks of 16 (the MMA's K); per (chunk, lane) the Q' B fragments.
 struct LeafMma {
@@ -93,7 +113,7 @@ struct QLevel {
     DevBuf vmap;                      // work index -> V-node index (only when sharded)
     bool mapped = false;
     const int32_t *vmap_ptr = nullptr;   // the map in use (vmap, or the caller's active-root list)
-    DevBuf R, P, cnt, umask, U, off, Q, zdraw, leafV;
+    DevBuf R, P, cnt, umask, U, off, Q, zdraw, leafV, xdraw;
 };
 
 struct Model {
@@ -107,9 +127,8 @@ struct Model {
     // device tables
     DevBuf d_m8, d_sig, d_cell /* sig | occ<<4 */, d_ctab, d_R64, d_O64, d_O32, d_gc_cell, d_gc_act, d_gc_val, d_free;
     int ngc = 0;
-    DevBuf d_fcells, d_gc_fidx, fl_goalv;   // fused leaf level: goal-term cells, their values
-    int nfcells = 0;
     BandSet band_big, band_small;
+    LeafBands leafb;
     LeafMma lm;
     // value iteration
     bool have_q = false;
@@ -123,9 +142,10 @@ struct Model {
     // plan workspace
     VLevel vl[kMaxLevels + 1];
     QLevel ql[kMaxLevels];
-    DevBuf part, scan_tmp, total, counters, vshard, tickets, xs;
+    DevBuf part, scan_tmp, total, counters, vshard, xs;
     int last_depth = -1, last_n = 0, last_shard_level = -1;
-    long long last_flagged = 0;
+    long long last_flagged = 0, last_skipped = 0;
+    bool last_xdraws = false;
     bool last_trace = false;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // graph-captured plan step (small trees): device level counts, private stream, cached graph
@@ -133,9 +153,6 @@ struct Model {
     cudaStream_t pg_stream = nullptr;
     cudaEvent_t pg_join = nullptr;
     cudaGraphExec_t pg_exec = nullptr;
-    // leaf level pipelined behind the last k_correct (plan.cu leaf_overlap)
-    cudaStream_t ov_corr = nullptr, ov_leaf = nullptr;
-    cudaEvent_t ov_ev[40] = {};
     std::vector<uintptr_t> pg_key;
     // instrumentation
     bool prof = false;
@@ -188,6 +205,15 @@ bool leaf_mma_enabled(const Model &m, long long bstride, const float *beliefs);
 int leaf_mma_records();              // fp64 records per parent written by the leaf kernel (one per warp)
 qvts_status launch_leaf_mma(Model &m, const float *beliefs, long long bstride, const int32_t *vmap, long long nwork,
                             int pstride, cudaStream_t st, const int32_t *skip, const long long *nwork_dev);
+
+// leaf.cu: the class-fixed band lists, and the leaf-level launch (S1+S2+S5 for every leaf parent);
+// nsplit CTAs share a parent pair's bands (one fp64 record each, summed in split order by k_reduce)
+qvts_status build_leaf_bands(Model &m, LeafBands &lb);
+bool leaf_kernel_supported(const Model &m);
+int leaf_nsplit(const Model &m, int level);
+qvts_status launch_leaf(Model &m, const float *beliefs, long long bstride, long long nbel, const int32_t *vmap,
+                        long long nwork, int nsplit, int pstride, long long part_off, cudaStream_t st,
+                        const long long *nwork_dev = nullptr);
 
 // model.cu
 qvts_status build_bands(Model &m, BandSet &bs, int rows);

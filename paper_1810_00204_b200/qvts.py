@@ -25,6 +25,7 @@ EXPORTS = [
     "qvts_trace_vnodes", "qvts_trace_leaf_values", "qvts_trace_belief", "qvts_run_episodes",
     "qvts_trace_counts", "qvts_set_profiling", "qvts_get_profile", "qvts_fib_iteration", "qvts_get_alpha",
     "qvts_pbvi", "qvts_get_pbvi", "qvts_plan_best_first", "qvts_trace_best_first", "qvts_bf_advance", "qvts_belief_update_batch",
+    "qvts_trace_state_draws",
 ]
 QVTS_BF_BUDGET, QVTS_BF_GAP, QVTS_BF_TERMINAL, QVTS_BF_POOL, QVTS_BF_TIME = 0, 1, 2, 3, 4
 QVTS_LEAF_QMDP, QVTS_LEAF_FIB = 0, 1
@@ -53,7 +54,7 @@ class qvts_plan_cfg(C.Structure):
 class qvts_plan_result(C.Structure):
     _fields_ = [("action", C.c_int32), ("n_actions", C.c_int32), ("q_root", C.c_double * 9),
                 ("n_vnodes", C.c_int64 * 9), ("n_belief_updates", C.c_int64), ("device_ms", C.c_double),
-                ("shard_level", C.c_int32)]
+                ("shard_level", C.c_int32), ("n_flag_candidates", C.c_int64), ("n_tiles_skipped", C.c_int64)]
 
 
 class qvts_bf_cfg(C.Structure):
@@ -132,6 +133,7 @@ def lib() -> C.CDLL:
         L.qvts_trace_vnodes.argtypes = [vp, C.c_int32, vp, vp, vp, vp, vp]
         L.qvts_trace_leaf_values.argtypes = [vp, vp]
         L.qvts_trace_belief.argtypes = [vp, C.c_int32, C.c_int64, vp]
+        L.qvts_trace_state_draws.argtypes = [vp, C.c_int32, vp]
         L.qvts_trace_counts.argtypes = [vp, C.POINTER(C.c_int32), vp, vp]
         L.qvts_set_profiling.argtypes = [vp, C.c_int32]
         L.qvts_get_profile.argtypes = [vp, C.POINTER(qvts_profile)]
@@ -335,6 +337,12 @@ def qvts_trace_leaf_values(h, n_q):
     return V
 
 
+def qvts_trace_state_draws(h, level, n_q, n_samples):
+    x = np.zeros((n_q, max(1, n_samples)), np.int32)
+    _check(lib().qvts_trace_state_draws(h, level, x.ctypes.data), "qvts_trace_state_draws")
+    return x
+
+
 def qvts_trace_belief(h, level, index, n_cells):
     out = np.zeros(n_cells, np.float32)
     _check(lib().qvts_trace_belief(h, level, index, out.ctypes.data), "qvts_trace_belief")
@@ -482,13 +490,16 @@ class Model:
     def run_episodes(self, n_episodes, **kw):
         return qvts_run_episodes(self.h, n_episodes, **kw)
 
-    def trace(self, with_draws=False, n_samples=0, beliefs=False):
+    def trace(self, with_draws=False, n_samples=0, beliefs=False, with_states=False):
         """Pull the whole tree of the last plan step to the host (small configs).  with_draws and
-        the leaf values need a plan step run with want_trace=True."""
+        the leaf values need a plan step run with want_trace=True; with_states (the ancestral
+        sampler's state index per draw) also needs sampler=QVTS_SAMPLER_ANCESTRAL."""
         D, nv, nq = qvts_trace_counts(self.h)
         levels = []
         for d in range(D):
             q = qvts_trace_qnodes(self.h, d, nq[d] * self.n_actions, n_samples, with_draws)
+            if with_states:
+                q["x"] = qvts_trace_state_draws(self.h, d, nq[d] * self.n_actions, n_samples)
             v = qvts_trace_vnodes(self.h, d, nv[d])
             if beliefs and d > 0:
                 v["belief"] = np.stack([qvts_trace_belief(self.h, d, i, self.n_cells) for i in range(nv[d])]) \

@@ -9,9 +9,10 @@ TOL = 1e-5          # beliefs, P, R, Q, V: absolute (north star)
 TIE = 1e-6          # chosen actions may differ only across a tie within this (north star)
 
 
-def gpu_tree(model, n, with_beliefs=False):
-    """Flatten the GPU trace into dicts keyed by tree path."""
-    t = model.trace(with_draws=True, n_samples=n, beliefs=with_beliefs)
+def gpu_tree(model, n, with_beliefs=False, with_states=False):
+    """Flatten the GPU trace into dicts keyed by tree path (with_states: the ancestral sampler's
+    state index x of every draw, for the c.5 replay of flagged state draws)."""
+    t = model.trace(with_draws=True, n_samples=n, beliefs=with_beliefs, with_states=with_states)
     D = t["depth"]
     na = model.n_actions
     q, v, bel = {}, {}, {}
@@ -19,7 +20,8 @@ def gpu_tree(model, n, with_beliefs=False):
         lq, lv = t["levels"][d]["q"], t["levels"][d]["v"]
         for i in range(len(lq["path"])):
             q[int(lq["path"][i])] = dict(level=d, idx=i, R=lq["R"][i], P=lq["P"][i], cnt=lq["cnt"][i],
-                                         Q=lq["Q"][i], z=lq["z"][i])
+                                         Q=lq["Q"][i], z=lq["z"][i],
+                                         x=lq["x"][i] if with_states else None)
         if d > 0:
             for i in range(len(lv["path"])):
                 v[int(lv["path"][i])] = dict(level=d, V=lv["V"][i], z=int(lv["z"][i]), f=int(lv["f"][i]))
@@ -47,7 +49,9 @@ def oracle_tree(res):
 
 
 def draw_mismatches(gq, oq):
-    """Mismatched draws per Q-node path; raises on a mismatch of a non-flagged draw."""
+    """Mismatched draws per Q-node path; raises on a mismatch of a non-flagged draw.  Replay
+    entries carry the GPU's z and, for the ancestral sampler, its state index x (the oracle then
+    takes x only if it borders the flagged boundary and recomputes x' and z from it)."""
     replay, n_flag_mismatch = [], 0
     for p, o in oq.items():
         g = gq.get(p)
@@ -58,7 +62,10 @@ def draw_mismatches(gq, oq):
             if not o["flag"][j]:
                 raise AssertionError(f"non-flagged draw mismatch at path {p:#x} sample {j}: "
                                      f"gpu {g['z'][j]} oracle {o['z'][j]}")
-            replay.append((p, int(j), int(g["z"][j])))
+            if g.get("x") is not None:
+                replay.append((p, int(j), int(g["z"][j]), int(g["x"][j])))
+            else:
+                replay.append((p, int(j), int(g["z"][j])))
             n_flag_mismatch += 1
     return replay, n_flag_mismatch
 
