@@ -63,6 +63,39 @@ __host__ __device__ constexpr bool is_diag(int k) { return k == 0 || k == 2 || k
 // diagonal directions di in {0, 2, 5, 7} -> accumulator 0..3
 __host__ __device__ constexpr int diag_slot(int di) { return di == 0 ? 0 : di == 2 ? 1 : di == 5 ? 2 : 3; }
 
+// tensor memory (TMEM) as per-thread fp64 storage: 32x32b shape, thread i of warp w <-> lane
+// 32 (w % 4) + i, consecutive 32-bit columns
+__device__ __forceinline__ void tm_ld16(uint32_t ta, uint32_t *v) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                   "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                 : "r"(ta));
+}
+__device__ __forceinline__ void tm_ld4(uint32_t ta, uint32_t *v) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]) : "r"(ta));
+}
+__device__ __forceinline__ void tm_st16(uint32_t ta, const uint32_t *v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+                 :: "r"(ta), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+                    "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+                 : "memory");
+}
+__device__ __forceinline__ void tm_st4(uint32_t ta, const uint32_t *v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};"
+                 :: "r"(ta), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]) : "memory");
+}
+// the 9 class-mass sums of both parents (18 doubles = 36 columns): read, += fp32 band sums, write
+__device__ __forceinline__ void tm_sums(uint32_t ta, uint32_t (&w)[36], bool load) {
+    if (load) {
+        tm_ld16(ta, w); tm_ld16(ta + 16, w + 16); tm_ld4(ta + 32, w + 32);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    } else {
+        tm_st16(ta, w); tm_st16(ta + 16, w + 16); tm_st4(ta + 32, w + 32);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+}
+
 // shared load at a compile-time byte offset from a 32-bit shared address
 template <int OFF>
 __device__ __forceinline__ float lds_at(uint32_t addr) {
@@ -128,7 +161,33 @@ __global__ void __launch_bounds__(kLeafThreads, 2) k_leaf(LeafArgs a, const __gr
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     uint32_t phase = 0;
+    // Per-thread accumulators are band-local (fp32 within one band: ~1/8 of a thread's cells) and
+    // folded into running totals in tensor memory at every band end, in band order: the 9
+    // class-mass sums (b and the 8 h_k) as fp64 (36 columns), the 72 products and 4 diagonal
+    // masses as fp32 pairs (152 columns at A8) -- 256 columns per CTA, two CTAs per SM fill the 512.
+    constexpr int NACC = 2 * (9 * NA + 4);               // fp32 columns of F and E
+    constexpr int NCH = (NACC + 15) / 16;
+    constexpr uint32_t TMC = 48 + 16 * NCH <= 128 ? 128u : 256u;   // allocation: a power of 2
+    __shared__ uint32_t s_tmem;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(&s_tmem)), "n"(TMC));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();                                     // the barrier is initialised for every thread
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tm_sum = s_tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+    const uint32_t tm_acc = tm_sum + 48;                 // F then E, 2 columns per pair, 16-column chunks
+    {
+        uint32_t z[36];
+#pragma unroll
+        for (int i = 0; i < 36; ++i) z[i] = 0u;
+        tm_sums(tm_sum, z, false);
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) tm_st16(tm_acc + 16 * c, z);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
 
     float2 F[9][NA], S[9], E[4];
 #pragma unroll
@@ -139,6 +198,8 @@ __global__ void __launch_bounds__(kLeafThreads, 2) k_leaf(LeafArgs a, const __gr
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i) E[i] = make_float2(0.f, 0.f);
+    // pair i of the F/E accumulators (F row-major, then E)
+    auto acc_pair = [&](int i) -> float2 & { return i < 9 * NA ? F[i / NA][i % NA] : E[i - 9 * NA]; };
 
     const uint32_t tbase = (uint32_t)__cvta_generic_to_shared(smem);
     // the slot-stream ring after the two tiles: Q' rows [ring][NQ4][T] float4, entries [ring][T]
@@ -338,6 +399,41 @@ __global__ void __launch_bounds__(kLeafThreads, 2) k_leaf(LeafArgs a, const __gr
 #undef QVTS_READY
 #undef QVTS_FETCH
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        {   // this band's fp32 class-mass sums into the fp64 totals
+            uint32_t w[36];
+            tm_sums(tm_sum, w, true);
+#pragma unroll
+            for (int i = 0; i < 18; ++i) {
+                const int f = i >> 1;
+                double d = __hiloint2double((int)w[2 * i + 1], (int)w[2 * i]);
+                d += (double)((i & 1) ? S[f].y : S[f].x);
+                w[2 * i] = (uint32_t)__double2loint(d);
+                w[2 * i + 1] = (uint32_t)__double2hiint(d);
+            }
+            tm_sums(tm_sum, w, false);
+#pragma unroll
+            for (int f = 0; f < 9; ++f) S[f] = make_float2(0.f, 0.f);
+            // F and E: 8 pairs per 16-column chunk, fp32 adds of the band partials
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) {
+                uint32_t v[16];
+                tm_ld16(tm_acc + 16 * c, v);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const int i = 8 * c + k;
+                    if (i < 9 * NA + 4) {
+                        float2 &x = acc_pair(i);
+                        const float2 tot = fadd2(make_float2(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1])), x);
+                        v[2 * k] = __float_as_uint(tot.x);
+                        v[2 * k + 1] = __float_as_uint(tot.y);
+                        x = make_float2(0.f, 0.f);
+                    }
+                }
+                tm_st16(tm_acc + 16 * c, v);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
         __syncthreads();   // the tiles are overwritten by the next band
     }
 
@@ -345,16 +441,32 @@ __global__ void __launch_bounds__(kLeafThreads, 2) k_leaf(LeafArgs a, const __gr
     // class, value) sums its class's slot-threads in fixed order in fp64 (4 interleaved sums)
     constexpr int RS = T + 1;
     float *red = smem;
+    double *red64 = reinterpret_cast<double *>(smem + ((2 * NV * RS + 3) & ~3));   // [2][9][T] class masses
 #pragma unroll
-    for (int v = 0; v < NV; ++v) {
-        float2 x;
-        if (v < 9) x = S[v];
-        else if (v < CB) { const int u = v - 9; x = F[u / NA][u % NA]; }
-        else x = E[v - CB];
-        red[(0 * NV + v) * RS + t] = x.x;
-        red[(1 * NV + v) * RS + t] = x.y;
+    for (int c = 0; c < NCH; ++c) {                       // the F / E totals from tensor memory
+        uint32_t v[16];
+        tm_ld16(tm_acc + 16 * c, v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int i = 8 * c + k;
+            if (i < 9 * NA + 4) {
+                red[(0 * NV + 9 + i) * RS + t] = __uint_as_float(v[2 * k]);
+                red[(1 * NV + 9 + i) * RS + t] = __uint_as_float(v[2 * k + 1]);
+            }
+        }
     }
+    {
+        uint32_t w[36];
+        tm_sums(tm_sum, w, true);
+#pragma unroll
+        for (int i = 0; i < 18; ++i)
+            red64[((i & 1) * 9 + (i >> 1)) * T + t] = __hiloint2double((int)w[2 * i + 1], (int)w[2 * i]);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tmem), "n"(TMC));
     // record layout of k_hist<leaf>: [class][CB] then 8 blocked-mass values (orthogonal ones 0:
     // k_reduce derives them from the class masses); one record per (parent, split)
     const int NOUT = 16 * CB + 8;
@@ -372,16 +484,27 @@ __global__ void __launch_bounds__(kLeafThreads, 2) k_leaf(LeafArgs a, const __gr
             const int d = oo - 16 * CB;
             if (d == 0 || d == 2 || d == 5 || d == 7) { v = CB + diag_slot(d); t0 = 0; t1 = T; }
         }
-        const float *rp = red + (p * NV + v) * RS;
         double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
         int th = t0;
-        for (; th + 3 < t1; th += 4) {
-            s0 += (double)rp[th];
-            s1 += (double)rp[th + 1];
-            s2 += (double)rp[th + 2];
-            s3 += (double)rp[th + 3];
+        if (v < 9) {                                    // class masses: fp64 per thread
+            const double *rp = red64 + (p * 9 + v) * T;
+            for (; th + 3 < t1; th += 4) {
+                s0 += rp[th];
+                s1 += rp[th + 1];
+                s2 += rp[th + 2];
+                s3 += rp[th + 3];
+            }
+            for (; th < t1; ++th) s0 += rp[th];
+        } else {
+            const float *rp = red + (p * NV + v) * RS;
+            for (; th + 3 < t1; th += 4) {
+                s0 += (double)rp[th];
+                s1 += (double)rp[th + 1];
+                s2 += (double)rp[th + 2];
+                s3 += (double)rp[th + 3];
+            }
+            for (; th < t1; ++th) s0 += (double)rp[th];
         }
-        for (; th < t1; ++th) s0 += (double)rp[th];
         a.part[(wp * a.nsplit + split) * (long long)a.pstride + oo] = (s0 + s1) + (s2 + s3);
     }
 }
@@ -645,7 +768,8 @@ static qvts_status launch_leaf_t(Model &m, const float *beliefs, long long bstri
     const char *ev = std::getenv("QVTS_LEAF_TMA");              // read per call (0: cp.async staging)
     a.use_tma = ((!ev || std::atoi(ev) != 0) && leaf_tensor_map(m, beliefs, bstride, nbel, &tm)) ? 1 : 0;
     const size_t smem = std::max(sizeof(float) * 2 * (size_t)lb.TS + leaf_ring_bytes(m.NAP),
-                                 sizeof(float) * 2 * (size_t)NV * (kLeafThreads + 1));
+                                 sizeof(float) * (((2 * (size_t)NV * (kLeafThreads + 1)) + 3) & ~(size_t)3) +
+                                     sizeof(double) * 2 * 9 * kLeafThreads);
     auto kfn = lb.TP == 136 ? k_leaf<MASK, 136> : k_leaf<MASK, 0>;
     QVTS_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const long long nblocks = ((nwork + 1) / 2) * nsplit;

@@ -139,17 +139,20 @@ __device__ __forceinline__ int ancestral_tail(const ReduceArgs &a, int x, int k,
 // backup Q = R + gamma sum_z (f_z/n) V(z) in ascending z (Alg. 6 with gamma, R13).
 template <uint32_t MASK, bool LEAF>
 __host__ __device__ constexpr int reduce_smem_doubles(int pstride) {
-    // band sums, blocked-mass totals, per-warp S / numerators (leaf), per-warp CDF (16 warps max)
-    return pstride + 8 + (LEAF ? mask_count(MASK) * 32 * mask_count(MASK) : 0) + 16 * 16;
+    // band sums, blocked-mass totals, per-warp S / numerators (leaf), per-warp CDF, O[16][16]
+    return pstride + 8 + (LEAF ? mask_count(MASK) * 32 * mask_count(MASK) : 0) + 16 * mask_count(MASK) + 256;
 }
 
-// Executed by a whole CTA of nthreads (a multiple of 32) for parent w; warp j handles actions
-// j, j + nwarps, ...  rsm: reduce_smem_doubles(pstride) doubles of shared memory.
+// Executed by a CTA of |A| warps for parent w; warp j handles action j.
+// rsm: reduce_smem_doubles(pstride) doubles of shared memory.
 template <uint32_t MASK, bool LEAF>
 __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int nthreads) {
     constexpr int NA = mask_count(MASK);
     constexpr int CB = hist_cb<MASK, LEAF>();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = nthreads >> 5;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // O[s][z] in shared memory (every warp reads it in the P and leaf-numerator sums)
+    double *sO = rsm + a.pstride + 8 + (LEAF ? NA * 32 * NA : 0) + 16 * NA;
+    for (int i = threadIdx.x; i < 256; i += nthreads) sO[i] = a.O64[i];
     double *sp = rsm;                          // [pstride] band-summed partials
     double *sE = rsm + a.pstride;              // [8] blocked-mass totals
     const double *pp = a.part + w * a.nb * (long long)a.pstride;
@@ -193,7 +196,8 @@ __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int
     const int root = a.vroot[v];
     const uint32_t step = a.root_step[root], ep = a.root_ep[root];
     int nflag = 0, leaves = 0;
-    for (int j = warp; j < NA; j += nwarps) {
+    {
+    const int j = warp;                        // this warp's action (the CTA has |A| warps)
     double *sS = sE + 8 + warp * 32 * NA;      // [16][NA] S of this warp's action
     double *sR = sS + 16 * NA;                 // [16][NA] its (z, a') numerators
     const long long q = w * NA + j;
@@ -234,13 +238,12 @@ __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int
 #pragma unroll
     for (int s = 0; s < 16; ++s) {
         const double m = __shfl_sync(0xffffffffu, Ms, s);
-        if (lane < 16) Pz += a.O64[s * 16 + lane] * m;
+        if (lane < 16) Pz += sO[s * 16 + lane] * m;
     }
     // ascending-z CDF in fp64, summed sequentially (A.5); kept in shared memory (16 doubles per
     // warp) rather than 32 registers per lane, which spilled under the kernel's register bound
-    double *C = rsm + a.pstride + 8 + (LEAF ? NA * 32 * NA : 0) + 16 * warp;
+    double *C = rsm + a.pstride + 8 + (LEAF ? NA * 32 * NA : 0) + 16 * warp;   // [16] per warp
     double acc = 0.0;
-    __syncwarp();                              // the previous action's draws are done with C
 #pragma unroll
     for (int z = 0; z < 16; ++z) {
         acc += __shfl_sync(0xffffffffu, Pz, z);
@@ -262,13 +265,16 @@ __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int
             } else {
                 const double u = philox_uniform(r.x);
                 const double tt = u * C[15];
-                z = 0;
-                double gap = INFINITY;
+                // z = #{k : C_k <= tt} (A.5) by binary search over the non-decreasing CDF; the gap
+                // min_{k<15} |tt - C_k| is attained at the boundaries around tt, C_{z-1} and C_z
+                int lo = 0;
 #pragma unroll
-                for (int kk = 0; kk < 16; ++kk) {
-                    z += (C[kk] <= tt) ? 1 : 0;
-                    if (kk < 15) gap = fmin(gap, fabs(tt - C[kk]));
-                }
+                for (int st = 8; st > 0; st >>= 1)
+                    if (C[lo + st - 1] <= tt) lo += st;
+                z = lo + (C[lo] <= tt ? 1 : 0);          // in 0..16
+                double gap = INFINITY;
+                if (z >= 1 && z - 1 < 15) gap = tt - C[z - 1];
+                if (z < 15) gap = fmin(gap, C[z] - tt);
                 z = min(z, 15);
                 nflag += gap < 1e-6 ? 1 : 0;
             }
@@ -310,12 +316,10 @@ __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int
         // lane -> (u, a'): numerator sum_s O[s][z_u] S[s][a']
         for (int idx = lane; idx < U * NA; idx += 32) {
             const int u = idx / NA, j2 = idx % NA;
-            unsigned rem = um;
-            for (int i = 0; i < u; ++i) rem &= rem - 1;
-            const int z = __ffs(rem) - 1;
+            const int z = (int)__fns(um, 0, u + 1);       // the (u+1)-th sampled z, ascending
             double num = 0.0;
 #pragma unroll
-            for (int s = 0; s < 16; ++s) num += a.O64[s * 16 + z] * sS[s * NA + j2];
+            for (int s = 0; s < 16; ++s) num += sO[s * 16 + z] * sS[s * NA + j2];
             sR[u * NA + j2] = num;
         }
         __syncwarp();
@@ -323,9 +327,7 @@ __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int
         double Vz = 0.0, wz = 0.0;
         int zu = 0;
         if (lane < U) {
-            unsigned rem = um;
-            for (int i = 0; i < lane; ++i) rem &= rem - 1;
-            zu = __ffs(rem) - 1;
+            zu = (int)__fns(um, 0, lane + 1);
             double best = -INFINITY;
             for (int j2 = 0; j2 < NA; ++j2) best = fmax(best, sR[lane * NA + j2]);
             Vz = best;   // divided below by P(z), held by lane z
@@ -341,9 +343,8 @@ __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int
         double accq = 0.0;
         for (int u = 0; u < U; ++u) accq += __shfl_sync(0xffffffffu, wz, u) * __shfl_sync(0xffffffffu, Vz, u);
         if (lane == 0) a.Q[q] = R + a.gamma * accq;
-        __syncwarp();
     }
-    }   // actions of this warp
+    }   // this warp's action
     // flagged-draw and leaf counts: per warp, one global atomic each (counts are integers)
     for (int o = 16; o > 0; o >>= 1) nflag += __shfl_xor_sync(0xffffffffu, nflag, o);
     if (lane == 0 && a.counters) {

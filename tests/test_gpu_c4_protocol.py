@@ -32,6 +32,14 @@ torch = pytest.importorskip("torch")
 _G = {}   # read by the forked workers
 
 
+@pytest.fixture(scope="module")
+def Q():
+    assert torch.cuda.is_available(), "GPU tests need CUDA"
+    from paper_1810_00204_b200 import qvts
+    qvts.lib()
+    return qvts
+
+
 def _qnode_check(o, b, ai, qpath, n, gq_R, gq_P, gq_z, seed=1):
     """R, P and draws of one Q-node against the oracle on belief b."""
     P, R, z, flag, cnt = o.qnode_sample(b, ai, qpath, n, seed=seed)

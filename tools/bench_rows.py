@@ -40,7 +40,7 @@ m.belief_update(b, 1, 0, o)
 dt, p = timed(lambda: m.belief_update(b, 1, 0, o), reps=50)
 out["K9_belief_update_C4"] = {"us_per_call": dt * 1e6, "algorithmic_bytes": 8 * m.n_cells,
                               "effective_GBps": 8 * m.n_cells / dt / 1e9,
-                              "note": "synchronous ABI call (hist + reduce + P readback + correct)"}
+                              "note": "synchronous ABI call (the batched path with n = 1: one cluster pass + P readback)"}
 # batched Eq. 3 (K9 at HBM scale): n beliefs read, n posteriors written
 NB = 2048
 bb = torch.tensor(np.stack([W.random_belief(gm, 500 + i % 64, dtype=np.float32) for i in range(NB)]), device="cuda")
@@ -59,7 +59,18 @@ out["K9_belief_update_batch_C4"] = {"n": NB, "ms_per_batch": dt * 1e3, "device_m
                                     "algorithmic_bytes": NB * 8 * m.n_cells,
                                     "effective_GBps": NB * 8 * m.n_cells / dt / 1e9,
                                     "effective_GBps_device": NB * 8 * m.n_cells / (dev_ms / 1e3) / 1e9,
-                                    "note": "read b + write b' per pair (algorithmic); two passes over b (selected-action class sums, then k_correct) and one sync"}
+                                    "note": "read b + write b' per pair (algorithmic); one pass per belief on a thread-block cluster (k_bu_cluster: staged rows, normaliser parts summed through DSMEM, posterior written), one sync"}
+# the two-pass path (QVTS_BU_CLUSTER=0), for comparison
+os.environ["QVTS_BU_CLUSTER"] = "0"
+m.belief_update_batch(bb, acts, zs, ob)
+e0.record()
+m.belief_update_batch(bb, acts, zs, ob)
+e1.record()
+torch.cuda.synchronize()
+dev2 = e0.elapsed_time(e1)
+os.environ.pop("QVTS_BU_CLUSTER")
+out["K9_belief_update_batch_C4"]["two_pass_device_ms"] = dev2
+out["K9_belief_update_batch_C4"]["two_pass_effective_GBps_device"] = NB * 8 * m.n_cells / (dev2 / 1e3) / 1e9
 for leaf in (Q.QVTS_LEAF_QMDP, Q.QVTS_LEAF_FIB):
     m.plan_step(b, 4, 16, seed=1, step=0, leaf_bound=leaf)
     dt, r = timed(lambda: m.plan_step(b, 4, 16, seed=1, step=1, leaf_bound=leaf), reps=3)
