@@ -1972,30 +1972,39 @@ __global__ void __launch_bounds__(256) k_bu_marg(CorrectArgs a, double *__restri
 }
 // Batched Eq. 3 in ONE pass over b (K9 at HBM rate): one thread-block cluster per belief, CTA
 // rank r owns rows [r R, (r+1) R).  Each CTA stages its rows (+1-row halo) in shared memory with
-// one cp.async burst, forms its part of P(z|b,a) = sum_y O[sig(y)][z] bbar_a(y) (fp64 per thread,
-// fixed-order block reduction), the cluster sums the NC parts in rank order through DSMEM (every
-// CTA gets the same bits), and each CTA then writes b' = (O[s][z] / P) bbar_a from the staged
-// rows with streaming float4 stores -- b is read once and b' written once (the two-pass path
-// reads b twice).  Same fp32 prediction and weights as k_correct (correct_predict).
-template <uint32_t MASK>
-__global__ void __launch_bounds__(256) k_bu_cluster(CorrectArgs a, double *__restrict__ pout) {
+// one cp.async burst; every thread predicts its <= kBuGroups groups of 4 cells ONCE (action
+// geometry compile-time) and keeps bbar and the signatures in registers, adds its part of
+// P(z|b,a) = sum_y O[sig(y)][z] bbar_a(y) (fp32 per thread, fp64 across threads in fixed order),
+// the cluster sums the NC parts in rank order through DSMEM (every CTA gets the same bits), and
+// the thread writes b' = (O[s][z] / P) bbar from its registers with streaming float4 stores --
+// b is read once and b' written once.  Same fp32 prediction and weights as k_correct.
+
+// One kernel for every action: the three source taps of the selected action (the intended move
+// and its two ring laterals, reading R3) are runtime offsets into the staged rows and runtime bits
+// of the occupancy byte, so every CTA runs the same small code path (one launch per batch).
+struct BuActs { int act[9]; };
+constexpr int kBuGroups = 11;        // 4-cell groups per thread (rows_cta * W / 4 <= 11 * 256)
+__global__ void __launch_bounds__(256, 3) k_bu_cluster(CorrectArgs a, double *__restrict__ pout, int NA, BuActs acts) {
     namespace cg = cooperative_groups;
-    constexpr int NA = mask_count(MASK);
     cg::cluster_group cl = cg::this_cluster();
     const int NC = (int)cl.num_blocks();
     const int rank = (int)cl.block_rank();
     const long long grp = blockIdx.x / NC;
     const long long q = a.sel_q[grp];
     const int zsel = a.sel_z[grp];
-    const int j = (int)(q % NA), k = action_of<MASK>(j);
+    const int k = acts.act[q % NA];
     const float *__restrict__ b = a.beliefs + (q / NA) * a.bstride;
     const int W = a.W, TPc = a.stage_tp;
     const int r0 = rank * a.rows_cta, r1 = min(a.H, r0 + a.rows_cta);
+    // tap geometry: source y - d of each tap as a row-major offset, its blocked bit in m8
+    const bool stay = k == 4;
+    const int k1 = stay ? 4 : lat1(k), k2 = stay ? 4 : lat2(k);
+    const int offa = -st_dr(k) * TPc - st_dc(k), off1 = -st_dr(k1) * TPc - st_dc(k1), off2 = -st_dr(k2) * TPc - st_dc(k2);
+    const uint32_t bita = stay ? 0u : (uint32_t)nbit(k), bit1 = stay ? 0u : (uint32_t)nbit(k1), bit2 = stay ? 0u : (uint32_t)nbit(k2);
     extern __shared__ float4 bu_smem4[];
     float *stile = reinterpret_cast<float *>(bu_smem4);
-    __shared__ float s_o[16];
+    __shared__ float s_o[16], s_w[16];
     __shared__ double wsum[8], s_part;
-    __shared__ float s_w[16];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x < 16) s_o[threadIdx.x] = (float)a.O64[threadIdx.x * 16 + zsel];
     // stage rows [r0 - 1, r1 + 1): off-map rows and the halo columns are zero
@@ -2015,38 +2024,52 @@ __global__ void __launch_bounds__(256) k_bu_cluster(CorrectArgs a, double *__res
     }
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();
-    auto predict = [&](int r, int c0, float (&bb)[4], int (&sg)[4]) {
-        float nbh[3][6];
+    // a thread owns one 4-cell column group and every RPP-th row of the CTA (W / 4 divides 256,
+    // checked on the host), so all addresses advance by constants; bbar and the signatures of its
+    // <= kBuGroups groups stay in registers from the normaliser pass to the write pass
+    const int RPP = 256 / W4, c0 = 4 * (threadIdx.x % W4), rl0 = threadIdx.x / W4;
+    const int nrows = r1 - r0;
+    const uint32_t mka = 1u << bita, mk1 = 1u << bit1, mk2 = 1u << bit2;   // the taps' blocked bits
+    const unsigned int *cellp = reinterpret_cast<const unsigned int *>(a.cell + (r0 + rl0) * W + c0);
+    const unsigned int *m8p = reinterpret_cast<const unsigned int *>(a.m8 + (r0 + rl0) * W + c0);
+    const float *rowp = stile + (rl0 + 1) * TPc + 4 + c0;
+    const int cstep = RPP * W / 4, rstep = RPP * TPc;
+    float bb[kBuGroups][4];
+    uint32_t sg4[kBuGroups];
+    float accf = 0.f;
 #pragma unroll
-        for (int dr = 0; dr < 3; ++dr) {
-            const float *row = stile + (r - r0 + dr) * TPc + 4 + c0;
-            const float4 m4 = *reinterpret_cast<const float4 *>(row);
-            nbh[dr][0] = row[-1];
-            nbh[dr][1] = m4.x; nbh[dr][2] = m4.y; nbh[dr][3] = m4.z; nbh[dr][4] = m4.w;
-            nbh[dr][5] = row[4];
-        }
-        switch (k) {   // block-uniform: compile-time tap geometry per action
-            case 0: correct_predict<0>(a, r, c0, nbh, bb, sg); break;
-            case 1: correct_predict<1>(a, r, c0, nbh, bb, sg); break;
-            case 2: correct_predict<2>(a, r, c0, nbh, bb, sg); break;
-            case 3: correct_predict<3>(a, r, c0, nbh, bb, sg); break;
-            case 4: correct_predict<4>(a, r, c0, nbh, bb, sg); break;
-            case 5: correct_predict<5>(a, r, c0, nbh, bb, sg); break;
-            case 6: correct_predict<6>(a, r, c0, nbh, bb, sg); break;
-            case 7: correct_predict<7>(a, r, c0, nbh, bb, sg); break;
-            default: correct_predict<8>(a, r, c0, nbh, bb, sg); break;
-        }
-    };
-    const int ngrp = (r1 - r0) * a.G;
-    double acc = 0.0;
-    for (int idx = threadIdx.x; idx < ngrp; idx += 256) {
-        const int r = r0 + idx / a.G, c0 = 4 * (idx % a.G);
-        float bb[4];
-        int sg[4];
-        predict(r, c0, bb, sg);
+    for (int g = 0; g < kBuGroups; ++g) {
+        sg4[g] = 0u;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) acc += (double)(s_o[sg[i]] * bb[i]);
+        for (int i = 0; i < 4; ++i) bb[g][i] = 0.f;
+        if (rl0 + RPP * g < nrows) {
+            const uint32_t info4 = __ldg(cellp), m84 = __ldg(m8p);
+            const float4 b4 = *reinterpret_cast<const float4 *>(rowp);
+            const float b0v[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float b0 = b0v[i];
+                float v = b0;
+                if (!stay) {   // k_correct's arithmetic (correct_predict): same fp32 operations
+                    const uint32_t m8 = m84 >> (8 * i);
+                    const float sa = rowp[offa + i], s1 = rowp[off1 + i], s2 = rowp[off2 + i];
+                    const float ha = (m8 & mka) ? sa + b0 : sa;
+                    const float h1 = (m8 & mk1) ? s1 + b0 : s1;
+                    const float h2 = (m8 & mk2) ? s2 + b0 : s2;
+                    v = fmaf(a.p_lat, h1 + h2, fmaf(a.p_int, ha, a.p_stay * b0));
+                }
+                bb[g][i] = ((info4 >> (8 * i)) & 16u) ? 0.f : v;          // occupied: no mass
+            }
+            sg4[g] = info4 & 0x0F0F0F0Fu;                                  // the 4 signatures
+#pragma unroll
+            for (int i = 0; i < 4; ++i) accf = fmaf(s_o[(sg4[g] >> (8 * i)) & 15u], bb[g][i], accf);
+        }
+        cellp += cstep;
+        m8p += cstep;
+        rowp += rstep;
     }
+    // fixed-order reduction: fp64 butterfly within each warp, then the 8 warp sums in order
+    double acc = (double)accf;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) wsum[warp] = acc;
@@ -2066,16 +2089,16 @@ __global__ void __launch_bounds__(256) k_bu_cluster(CorrectArgs a, double *__res
         if (threadIdx.x == 0 && rank == 0) pout[grp] = P;
     }
     cl.sync();                                   // no CTA leaves while another reads its part
-    float *outp = a.child + (long long)a.sel_out[grp] * a.cstride;
-    for (int idx = threadIdx.x; idx < ngrp; idx += 256) {
-        const int r = r0 + idx / a.G, c0 = 4 * (idx % a.G);
-        float bb[4];
-        int sg[4];
-        predict(r, c0, bb, sg);
-        float o[4];
+    float *outp = a.child + (long long)a.sel_out[grp] * a.cstride + (r0 + rl0) * W + c0;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) o[i] = s_w[sg[i]] * bb[i];
-        __stcs(reinterpret_cast<float4 *>(outp + (long long)r * W + c0), make_float4(o[0], o[1], o[2], o[3]));
+    for (int g = 0; g < kBuGroups; ++g) {
+        if (rl0 + RPP * g < nrows) {
+            float o[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) o[i] = s_w[(sg4[g] >> (8 * i)) & 15u] * bb[g][i];
+            __stcs(reinterpret_cast<float4 *>(outp), make_float4(o[0], o[1], o[2], o[3]));
+        }
+        outp += RPP * W;
     }
 }
 
@@ -2139,10 +2162,12 @@ extern "C" qvts_status qvts_belief_update_batch(qvts_model *m, const float *b_de
         const bool vec = (m->W & 3) == 0 && (b_stride & 3) == 0 && (out_stride & 3) == 0 &&
                          (reinterpret_cast<uintptr_t>(b_dev) & 15) == 0 && (reinterpret_cast<uintptr_t>(out_dev) & 15) == 0;
         const int tp = m->W + 8;
-        const int max_rows = std::max(1, (56 * 1024) / (4 * tp) - 2);
+        // rows per CTA: the staged rows fit ~56 KB and each thread holds <= kBuGroups 4-cell groups
+        const int max_rows = std::max(1, std::min((56 * 1024) / (4 * tp) - 2, kBuGroups * 256 / std::max(1, m->W / 4)));
         const int NC = (m->H + max_rows - 1) / max_rows;
         const char *ev_bu = std::getenv("QVTS_BU_CLUSTER");          // read per call (0: two-pass path)
-        if (vec && NC <= 8 && (!ev_bu || std::atoi(ev_bu) != 0) && (long long)n * NC <= 0x7FFFFFFFLL) {
+        const bool groups_ok = m->W / 4 >= 1 && 256 % (m->W / 4) == 0;   // the kernel's column-group mapping
+        if (vec && groups_ok && NC <= 8 && (!ev_bu || std::atoi(ev_bu) != 0) && (long long)n * NC <= 0x7FFFFFFFLL) {
             CorrectArgs cc = c;
             cc.rows_cta = (m->H + NC - 1) / NC;
             cc.stage_tp = tp;
@@ -2159,13 +2184,10 @@ extern "C" qvts_status qvts_belief_update_batch(qvts_model *m, const float *b_de
             attr[0].val.clusterDim.z = 1;
             lc.attrs = attr;
             lc.numAttrs = 1;
-#define QVTS_BUC(MASK)                                                                                          \
-    {                                                                                                           \
-        QVTS_CUDA(cudaFuncSetAttribute(k_bu_cluster<MASK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-        QVTS_CUDA(cudaLaunchKernelEx(&lc, k_bu_cluster<MASK>, cc, m->bu_P.as<double>()));                       \
-    }
-            QVTS_DISPATCH_MASK(m->mask, QVTS_BUC);
-#undef QVTS_BUC
+            BuActs acts_id;
+            for (int j = 0; j < 9; ++j) acts_id.act[j] = j < NA ? m->action_id[j] : 4;
+            QVTS_CUDA(cudaFuncSetAttribute(k_bu_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            QVTS_CUDA(cudaLaunchKernelEx(&lc, k_bu_cluster, cc, m->bu_P.as<double>(), NA, acts_id));
             QVTS_CUDA(cudaGetLastError());
             std::vector<double> p(n);
             QVTS_CUDA(cudaMemcpyAsync(p.data(), m->bu_P.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));

@@ -565,11 +565,14 @@ def test_belief_update_batch_C3_paths_and_alignment(Q, cluster, monkeypatch):
     Bm[:, 1:] = dev(B)
     outm = torch.zeros((nb, HW + 1), dtype=torch.float32, device="cuda")
     pm = g.belief_update_batch(Bm[:, 1:], acts, zs, outm[:, 1:])
-    assert np.max(np.abs(np.asarray(pm) - np.asarray(p))) <= 1e-12
+    # the misaligned views take the two-pass path (fp64 per-cell sums); the cluster path sums
+    # fp32 per-thread partials of <= 48 cells: the normalisers agree to ~1e-9, both within 1e-7 of
+    # the oracle above
+    assert np.max(np.abs(np.asarray(pm) - np.asarray(p))) <= 1e-8
     assert np.max(np.abs(outm[:, 1:].cpu().numpy() - res)) <= 1e-7
     single = torch.empty(HW + 1, dtype=torch.float32, device="cuda")
     ps = g.belief_update(Bm[0, 1:], int(acts[0]), int(zs[0]), single[1:])
-    assert abs(ps - p[0]) <= 1e-12 and np.max(np.abs(single[1:].cpu().numpy() - res[0])) <= 1e-7
+    assert abs(ps - p[0]) <= 1e-8 and np.max(np.abs(single[1:].cpu().numpy() - res[0])) <= 1e-7
     g.close()
 
 
