@@ -24,6 +24,7 @@
 //   ring with its own cp.async groups.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 
@@ -380,6 +381,22 @@ __global__ void __launch_bounds__(kLeafThreads, 2) k_leaf(LeafArgs a, const __gr
         uint32_t eA, eB;
         float4 qA[NQ4], qB[NQ4];
         float2 nbA[9], nbB[9];
+        if constexpr (NA > 8) {
+            // A9: the 81 product pairs leave no registers for a second neighbourhood / Q' row in
+            // flight, so each cell fetches, loads and accumulates in turn (the co-resident warps
+            // cover the shared-memory latency)
+            for (int i = 0; i < bi.L; i += 8) {
+                QVTS_ISSUE(7) QVTS_READY(); QVTS_FETCH(0, eA, qA) load_nb(eA, nbA); cell(eA, nbA, qA);
+                QVTS_ISSUE(0) QVTS_READY(); QVTS_FETCH(1, eA, qA) load_nb(eA, nbA); cell(eA, nbA, qA);
+                QVTS_ISSUE(1) QVTS_READY(); QVTS_FETCH(2, eA, qA) load_nb(eA, nbA); cell(eA, nbA, qA);
+                QVTS_ISSUE(2) QVTS_READY(); QVTS_FETCH(3, eA, qA) load_nb(eA, nbA); cell(eA, nbA, qA);
+                if (i + 4 >= bi.L) break;
+                QVTS_ISSUE(3) QVTS_READY(); QVTS_FETCH(4, eA, qA) load_nb(eA, nbA); cell(eA, nbA, qA);
+                QVTS_ISSUE(4) QVTS_READY(); QVTS_FETCH(5, eA, qA) load_nb(eA, nbA); cell(eA, nbA, qA);
+                QVTS_ISSUE(5) QVTS_READY(); QVTS_FETCH(6, eA, qA) load_nb(eA, nbA); cell(eA, nbA, qA);
+                QVTS_ISSUE(6) QVTS_READY(); QVTS_FETCH(7, eA, qA) load_nb(eA, nbA); cell(eA, nbA, qA);
+            }
+        } else {
         QVTS_FETCH(0, eA, qA)
         load_nb(eA, nbA);
         // cell i: issue step i + 7 into slot (i + 7) & 7, wait for step i + 1, fetch it, load its
@@ -394,6 +411,7 @@ __global__ void __launch_bounds__(kLeafThreads, 2) k_leaf(LeafArgs a, const __gr
             QVTS_ISSUE(4) QVTS_READY(); QVTS_FETCH(6, eA, qA) load_nb(eA, nbA); cell(eB, nbB, qB);
             QVTS_ISSUE(5) QVTS_READY(); QVTS_FETCH(7, eB, qB) load_nb(eB, nbB); cell(eA, nbA, qA);
             QVTS_ISSUE(6) QVTS_READY(); QVTS_FETCH(0, eA, qA) load_nb(eA, nbA); cell(eB, nbB, qB);
+        }
         }
 #undef QVTS_ISSUE
 #undef QVTS_READY
@@ -437,83 +455,88 @@ __global__ void __launch_bounds__(kLeafThreads, 2) k_leaf(LeafArgs a, const __gr
         __syncthreads();   // the tiles are overwritten by the next band
     }
 
-    // class reduction, once per parent pair: red[p][v][slot] (fp32), then every output (parent,
-    // class, value) sums its class's slot-threads in fixed order in fp64 (4 interleaved sums)
+    // class reduction, once per parent pair and one parent at a time: red[v][slot] (fp32) and
+    // red64[9][slot] (fp64 class masses), then every output (class, value) sums its class's
+    // slot-threads in fixed order in fp64 (4 interleaved sums)
     constexpr int RS = T + 1;
     float *red = smem;
-    double *red64 = reinterpret_cast<double *>(smem + ((2 * NV * RS + 3) & ~3));   // [2][9][T] class masses
+    double *red64 = reinterpret_cast<double *>(smem + ((NV * RS + 3) & ~3));
+    const int NOUT = 16 * CB + 8;
 #pragma unroll
-    for (int c = 0; c < NCH; ++c) {                       // the F / E totals from tensor memory
-        uint32_t v[16];
-        tm_ld16(tm_acc + 16 * c, v);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    for (int p = 0; p < 2; ++p) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int i = 8 * c + k;
-            if (i < 9 * NA + 4) {
-                red[(0 * NV + 9 + i) * RS + t] = __uint_as_float(v[2 * k]);
-                red[(1 * NV + 9 + i) * RS + t] = __uint_as_float(v[2 * k + 1]);
+        for (int c = 0; c < NCH; ++c) {                   // the F / E totals from tensor memory
+            uint32_t v[16];
+            tm_ld16(tm_acc + 16 * c, v);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int i = 8 * c + k;
+                if (i < 9 * NA + 4) red[(9 + i) * RS + t] = __uint_as_float(v[2 * k + p]);
             }
         }
-    }
-    {
-        uint32_t w[36];
-        tm_sums(tm_sum, w, true);
+        {
+            uint32_t w[36];
+            tm_sums(tm_sum, w, true);
 #pragma unroll
-        for (int i = 0; i < 18; ++i)
-            red64[((i & 1) * 9 + (i >> 1)) * T + t] = __hiloint2double((int)w[2 * i + 1], (int)w[2 * i]);
+            for (int f = 0; f < 9; ++f)
+                red64[f * T + t] = __hiloint2double((int)w[2 * (2 * f + p) + 1], (int)w[2 * (2 * f + p)]);
+        }
+        __syncthreads();
+        // record layout of k_hist<leaf>: [class][CB] then 8 blocked-mass values (orthogonal ones 0:
+        // k_reduce derives them from the class masses); one record per (parent, split)
+        const long long wp = 2 * pair + p;
+        for (int oo = t; oo < NOUT && wp < nwork; oo += T) {
+            int t0 = 0, t1 = 0, v = 0;
+            if (oo < 16 * CB) {
+                const int c = oo / CB;
+                v = oo - c * CB;
+                t0 = a.cs[c];
+                t1 = a.cs[c + 1];
+            } else {
+                const int d = oo - 16 * CB;
+                if (d == 0 || d == 2 || d == 5 || d == 7) { v = CB + diag_slot(d); t0 = 0; t1 = T; }
+            }
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            int th = t0;
+            if (v < 9) {                                    // class masses: fp64 per thread
+                const double *rp = red64 + v * T;
+                for (; th + 3 < t1; th += 4) {
+                    s0 += rp[th];
+                    s1 += rp[th + 1];
+                    s2 += rp[th + 2];
+                    s3 += rp[th + 3];
+                }
+                for (; th < t1; ++th) s0 += rp[th];
+            } else {
+                const float *rp = red + v * RS;
+                for (; th + 3 < t1; th += 4) {
+                    s0 += (double)rp[th];
+                    s1 += (double)rp[th + 1];
+                    s2 += (double)rp[th + 2];
+                    s3 += (double)rp[th + 3];
+                }
+                for (; th < t1; ++th) s0 += (double)rp[th];
+            }
+            a.part[(wp * a.nsplit + split) * (long long)a.pstride + oo] = (s0 + s1) + (s2 + s3);
+        }
+        __syncthreads();                                    // red is rewritten for the next parent
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tmem), "n"(TMC));
-    // record layout of k_hist<leaf>: [class][CB] then 8 blocked-mass values (orthogonal ones 0:
-    // k_reduce derives them from the class masses); one record per (parent, split)
-    const int NOUT = 16 * CB + 8;
-    for (int o = t; o < 2 * NOUT; o += T) {
-        const int p = o / NOUT, oo = o - p * NOUT;
-        const long long wp = 2 * pair + p;
-        if (wp >= nwork) continue;
-        int t0 = 0, t1 = 0, v = 0;
-        if (oo < 16 * CB) {
-            const int c = oo / CB;
-            v = oo - c * CB;
-            t0 = a.cs[c];
-            t1 = a.cs[c + 1];
-        } else {
-            const int d = oo - 16 * CB;
-            if (d == 0 || d == 2 || d == 5 || d == 7) { v = CB + diag_slot(d); t0 = 0; t1 = T; }
-        }
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-        int th = t0;
-        if (v < 9) {                                    // class masses: fp64 per thread
-            const double *rp = red64 + (p * 9 + v) * T;
-            for (; th + 3 < t1; th += 4) {
-                s0 += rp[th];
-                s1 += rp[th + 1];
-                s2 += rp[th + 2];
-                s3 += rp[th + 3];
-            }
-            for (; th < t1; ++th) s0 += rp[th];
-        } else {
-            const float *rp = red + (p * NV + v) * RS;
-            for (; th + 3 < t1; th += 4) {
-                s0 += (double)rp[th];
-                s1 += (double)rp[th + 1];
-                s2 += (double)rp[th + 2];
-                s3 += (double)rp[th + 3];
-            }
-            for (; th < t1; ++th) s0 += (double)rp[th];
-        }
-        a.part[(wp * a.nsplit + split) * (long long)a.pstride + oo] = (s0 + s1) + (s2 + s3);
-    }
 }
 
 // ---- host side ------------------------------------------------------------------------------------
 static constexpr int kLeafSmemBudget = 112 * 1024;   // two CTAs per SM (2 x (112 + 1) KB <= 228 KB): tiles + ring
 static size_t leaf_ring_bytes(int NAP) { return (size_t)kLeafRing * kLeafThreads * (NAP * 4 + 4); }
 
-bool leaf_kernel_supported(const Model &m) { return m.mask == 0x1EF || m.mask == 0x0AA; }
+bool leaf_kernel_supported(const Model &m) {
+    const char *ev = std::getenv("QVTS_LEAF_KERNEL");           // read per call (0: the k_hist<leaf> path)
+    if (ev && std::atoi(ev) == 0) return false;
+    return m.mask == 0x1EF || m.mask == 0x0AA || m.mask == 0x1FF;
+}
 
 // bands per CTA: parent-count-independent (a function of the level only), so the summation order
 // -- and every value -- is the same for any batch, wave or rank count
@@ -768,8 +791,8 @@ static qvts_status launch_leaf_t(Model &m, const float *beliefs, long long bstri
     const char *ev = std::getenv("QVTS_LEAF_TMA");              // read per call (0: cp.async staging)
     a.use_tma = ((!ev || std::atoi(ev) != 0) && leaf_tensor_map(m, beliefs, bstride, nbel, &tm)) ? 1 : 0;
     const size_t smem = std::max(sizeof(float) * 2 * (size_t)lb.TS + leaf_ring_bytes(m.NAP),
-                                 sizeof(float) * (((2 * (size_t)NV * (kLeafThreads + 1)) + 3) & ~(size_t)3) +
-                                     sizeof(double) * 2 * 9 * kLeafThreads);
+                                 sizeof(float) * ((((size_t)NV * (kLeafThreads + 1)) + 3) & ~(size_t)3) +
+                                     sizeof(double) * 9 * kLeafThreads);
     auto kfn = lb.TP == 136 ? k_leaf<MASK, 136> : k_leaf<MASK, 0>;
     QVTS_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const long long nblocks = ((nwork + 1) / 2) * nsplit;
@@ -792,6 +815,8 @@ qvts_status launch_leaf(Model &m, const float *beliefs, long long bstride, long 
             return launch_leaf_t<0x1EF>(m, beliefs, bstride, nbel, vmap, nwork, nsplit, pstride, part_off, st, nwork_dev);
         case 0x0AA:
             return launch_leaf_t<0x0AA>(m, beliefs, bstride, nbel, vmap, nwork, nsplit, pstride, part_off, st, nwork_dev);
+        case 0x1FF:
+            return launch_leaf_t<0x1FF>(m, beliefs, bstride, nbel, vmap, nwork, nsplit, pstride, part_off, st, nwork_dev);
         default: set_error("leaf kernel: unsupported action set"); return QVTS_ERR_INVALID_ARG;
     }
 }
