@@ -538,10 +538,17 @@ bool leaf_kernel_supported(const Model &m) {
     return m.mask == 0x1EF || m.mask == 0x0AA || m.mask == 0x1FF;
 }
 
-// bands per CTA: parent-count-independent (a function of the level only), so the summation order
-// -- and every value -- is the same for any batch, wave or rank count
+// CTAs per parent pair: one (all bands), at every level.  Parent-count-independent, so the
+// summation order -- and every value -- is the same for any batch, wave or rank count.  Splitting
+// the bands over CTAs (a band record per CTA, summed by k_reduce) was measured slower even where
+// the level is small: C3 latency 0.367 -> 0.330 ms and a C5 episode batch 11.2 -> 7.3 s with one
+// CTA per pair (profiles/r02_leaf_nsplit_ab.json).  QVTS_LEAF_NSPLIT (read per call) overrides it
+// for measurement.
 int leaf_nsplit(const Model &m, int level) {
-    return level >= 3 ? 1 : std::max(1, m.leafb.nb);
+    (void)level;
+    const char *ev = std::getenv("QVTS_LEAF_NSPLIT");
+    if (ev && std::atoi(ev) > 0) return std::min(std::atoi(ev), std::max(1, m.leafb.nb));
+    return 1;
 }
 
 // Class-fixed band lists.  Bands: as tall as two parents' tiles allow (two CTAs per SM), balanced.

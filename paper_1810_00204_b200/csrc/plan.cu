@@ -23,15 +23,25 @@
 
 namespace qvts {
 
+// stencil id of the j-th action of MASK for a run-time j: one shift of a packed nibble table
+template <uint32_t MASK>
+__host__ __device__ constexpr uint64_t action_table() {
+    uint64_t t = 0;
+    for (int i = 0; i < mask_count(MASK); ++i) t |= (uint64_t)mask_action(MASK, i) << (4 * i);
+    return t;
+}
 template <uint32_t MASK>
 __device__ __forceinline__ int action_of(int j) {
-    constexpr int NA = mask_count(MASK);
-    int k = 0;
-#pragma unroll
-    for (int i = 0; i < NA; ++i)
-        if (i == j) k = mask_action(MASK, i);
-    return k;
+    return (int)((action_table<MASK>() >> (4 * j)) & 15u);
 }
+// laterals of a run-time stencil id (stencil.cuh lat1 / lat2) from packed nibble tables
+__host__ __device__ constexpr uint64_t lateral_table(bool second) {
+    uint64_t t = 0;
+    for (int k = 0; k < 9; ++k) t |= (uint64_t)(second ? lat2(k) : lat1(k)) << (4 * k);
+    return t;
+}
+__device__ __forceinline__ int lat1_rt(int k) { return (int)((lateral_table(false) >> (4 * k)) & 15u); }
+__device__ __forceinline__ int lat2_rt(int k) { return (int)((lateral_table(true) >> (4 * k)) & 15u); }
 
 template <uint32_t MASK, bool LEAF>
 __host__ __device__ constexpr int hist_cb() {      // class-binned values per thread
@@ -47,8 +57,15 @@ __host__ __device__ constexpr int dir_k(int di) { return di < 4 ? di : di + 1; }
 __host__ __device__ constexpr bool is_orth(int k) { return k == 1 || k == 3 || k == 5 || k == 7; }
 __host__ __device__ constexpr int orth_bit(int k) { return k == 1 ? 0 : k == 3 ? 1 : k == 5 ? 2 : 3; }
 // occupancy of y + d_k for every cell of signature class s, or 0 when it is not class-constant
+// (the orthogonal ids are exactly the odd ones and orth_bit(k) = k >> 1: no table for a run-time k)
+__host__ __device__ constexpr bool orth_is_odd() {
+    for (int k = 0; k < 9; ++k)
+        if (is_orth(k) != ((k & 1) != 0) || (is_orth(k) && orth_bit(k) != (k >> 1))) return false;
+    return true;
+}
+static_assert(orth_is_odd(), "class_blocked's closed form");
 __device__ __forceinline__ double class_blocked(int k, int s) {
-    return (k != 4 && is_orth(k) && ((s >> orth_bit(k)) & 1)) ? 1.0 : 0.0;
+    return ((k & 1) && ((s >> (k >> 1)) & 1)) ? 1.0 : 0.0;
 }
 
 // ---- S2 tail + S3 (+ S5 tail + S6 leaf backup) ------------------------------------------------
@@ -134,84 +151,107 @@ __device__ __forceinline__ int ancestral_tail(const ReduceArgs &a, int x, int k,
 // One CTA per parent V-node, one warp per action (Q-node).  The CTA first sums the parent's band
 // partials into shared memory (coalesced, fixed band order, fp64); then each warp: per-action
 // recombination of the linear fields -> M[s], P(z|b,a) (Eq. 3 normaliser), R(b,a),
-// n Philox draws (lane j = sample j), counts by ballot; for the leaf level also the Q_MDP value of
-// every sampled child, V(z) = qbar + max_a' [sum_s O[s][z] S[s][a']] / P(z), and the Q-node's
-// backup Q = R + gamma sum_z (f_z/n) V(z) in ascending z (Alg. 6 with gamma, R13).
+// n Philox draws (lane j = sample j), counts; for the leaf level also the Q_MDP value of every
+// sampled child, V(z) = qbar + max_a' [sum_s O[s][z] S[s][a']] / P(z), and the Q-node's backup
+// Q = R + gamma sum_z (f_z/n) V(z) in ascending z (Alg. 6 with gamma, R13).
+//
+// Shared memory (doubles): band sums [pstride] | E[8], sum b, pad [16] | per warp: scratch
+// [kRedWarpScratch + (LEAF ? 32 NA : 0)] | O[16][16].  A warp's scratch: M[s] (then the leaf values
+// V(z_u)), P(z|b,a), the ascending CDF, 16 counts and the compacted sampled-z list (ints), and at
+// the leaf S[s][a'] and the (z_u, a') numerators.
+constexpr int kRedWarpScratch = 16 + 16 + 16 + 16;
+template <uint32_t MASK, bool LEAF>
+__host__ __device__ constexpr int reduce_warp_doubles() {
+    return kRedWarpScratch + (LEAF ? 32 * mask_count(MASK) : 0);
+}
 template <uint32_t MASK, bool LEAF>
 __host__ __device__ constexpr int reduce_smem_doubles(int pstride) {
-    // band sums, blocked-mass totals, per-warp S / numerators (leaf), per-warp CDF, O[16][16]
-    return pstride + 8 + (LEAF ? mask_count(MASK) * 32 * mask_count(MASK) : 0) + 16 * mask_count(MASK) + 256;
+    return pstride + 16 + mask_count(MASK) * reduce_warp_doubles<MASK, LEAF>() + 256;
 }
 
 // Executed by a CTA of |A| warps for parent w; warp j handles action j.
 // rsm: reduce_smem_doubles(pstride) doubles of shared memory.
-template <uint32_t MASK, bool LEAF>
+template <uint32_t MASK, bool LEAF, bool ANC>
 __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int nthreads) {
     constexpr int NA = mask_count(MASK);
     constexpr int CB = hist_cb<MASK, LEAF>();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // O[s][z] in shared memory (every warp reads it in the P and leaf-numerator sums)
-    double *sO = rsm + a.pstride + 8 + (LEAF ? NA * 32 * NA : 0) + 16 * NA;
-    for (int i = threadIdx.x; i < 256; i += nthreads) sO[i] = a.O64[i];
     double *sp = rsm;                          // [pstride] band-summed partials
-    double *sE = rsm + a.pstride;              // [8] blocked-mass totals
+    double *sE = rsm + a.pstride;              // [8] blocked-mass totals, [8] = sum b
+    double *sO = sE + 16 + NA * reduce_warp_doubles<MASK, LEAF>();   // O[s][z]
+    for (int i = threadIdx.x; i < 256; i += nthreads) sO[i] = a.O64[i];
     const double *pp = a.part + w * a.nb * (long long)a.pstride;
-    // band sum, fixed band order (sequential over bands, as before); a thread takes two adjacent
-    // elements per pass as one 16-byte load per band (pstride is even), 4 bands in flight
+    // band sum, fixed band order (sequential over bands); a thread takes two adjacent elements per
+    // pass as one 16-byte load per band (pstride is even), 4 bands in flight; one band: a copy
     const double2 *pp2 = reinterpret_cast<const double2 *>(pp);
+    double2 *sp2 = reinterpret_cast<double2 *>(sp);
     const int half = a.pstride >> 1;
-    for (int i = threadIdx.x; i < half; i += nthreads) {
-        double acc0 = 0.0, acc1 = 0.0;
-        for (int bd = 0; bd < a.nb; bd += 4) {
-            double2 x[4];
+    if (a.nb == 1) {
+        for (int i = threadIdx.x; i < half; i += nthreads) sp2[i] = pp2[i];
+    } else {
+        for (int i = threadIdx.x; i < half; i += nthreads) {
+            double acc0 = 0.0, acc1 = 0.0;
+            for (int bd = 0; bd < a.nb; bd += 4) {
+                double2 x[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (bd + u < a.nb) x[u] = pp2[(long long)(bd + u) * half + i];
+                for (int u = 0; u < 4; ++u)
+                    if (bd + u < a.nb) x[u] = pp2[(long long)(bd + u) * half + i];
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (bd + u < a.nb) { acc0 += x[u].x; acc1 += x[u].y; }
+                for (int u = 0; u < 4; ++u)
+                    if (bd + u < a.nb) { acc0 += x[u].x; acc1 += x[u].y; }
+            }
+            sp2[i] = make_double2(acc0, acc1);
         }
-        sp[2 * i] = acc0;
-        sp[2 * i + 1] = acc1;
     }
     __syncthreads();
-    // E[d] = sum_y occ(y + d) b(y); orthogonal directions come from the class masses (signature bit)
-    if (threadIdx.x < 8) {
-        const int d = threadIdx.x, kd = d < 4 ? d : d + 1;
-        double e = sp[16 * CB + d];
-        if (is_orth(kd)) {
+    // E[d] = sum_y occ(y + d) b(y); orthogonal directions come from the class masses (signature
+    // bit); thread 8: the belief mass sum_s (class mass), ascending s
+    if (threadIdx.x < 9) {
+        const int d = threadIdx.x;
+        double e;
+        if (d == 8) {
             e = 0.0;
-            for (int s2 = 0; s2 < 16; ++s2) e += class_blocked(kd, s2) * sp[s2 * CB];
+            for (int s2 = 0; s2 < 16; ++s2) e += sp[s2 * CB];
+        } else {
+            const int kd = d < 4 ? d : d + 1;
+            e = sp[16 * CB + d];
+            if (is_orth(kd)) {
+                e = 0.0;
+                for (int s2 = 0; s2 < 16; ++s2) e += class_blocked(kd, s2) * sp[s2 * CB];
+            }
         }
         sE[d] = e;
     }
     __syncthreads();
     const long long v = a.vmap ? (long long)a.vmap[w] : w;
     const float *bp = a.beliefs + v * a.bstride;
-    const double mass_s = lane < 16 ? sp[lane * CB] : 0.0;
-    double mass = 0.0;
-#pragma unroll
-    for (int s = 0; s < 16; ++s) mass += __shfl_sync(0xffffffffu, mass_s, s);
+    const double mass = sE[8];
     const uint64_t vpath = a.vpath[v];
     const int root = a.vroot[v];
     const uint32_t step = a.root_step[root], ep = a.root_ep[root];
     int nflag = 0, leaves = 0;
     {
     const int j = warp;                        // this warp's action (the CTA has |A| warps)
-    double *sS = sE + 8 + warp * 32 * NA;      // [16][NA] S of this warp's action
-    double *sR = sS + 16 * NA;                 // [16][NA] its (z, a') numerators
+    double *sW = sE + 16 + warp * reduce_warp_doubles<MASK, LEAF>();
+    double *sM = sW;                           // [16] M[s]; at the leaf later V(z_u)
+    double *sP = sW + 16;                      // [16] P(z|b,a)
+    double *C = sW + 32;                       // [16] ascending CDF
+    int *sCnt = reinterpret_cast<int *>(sW + 48);   // [16] draw counts per z
+    int *sZ = sCnt + 16;                       // [16] the sampled z's, ascending
+    double *sS = sW + kRedWarpScratch;         // [16][NA] S of this warp's action (leaf)
+    double *sR = sS + 16 * NA;                 // [16][NA] its (z_u, a') numerators (leaf, NA not 2^k)
     const long long q = w * NA + j;
     const int k = action_of<MASK>(j);
-    const int da = k == 4 ? 0 : nbit(k), d1 = k == 4 ? 0 : nbit(lat1(k)), d2 = k == 4 ? 0 : nbit(lat2(k));
-    const int k1 = k == 4 ? 4 : lat1(k), k2 = k == 4 ? 4 : lat2(k);
-    // M[s]: bbar_a summed over signature class s
-    double Ms = 0.0;
+    const int k1 = k == 4 ? 4 : lat1_rt(k), k2 = k == 4 ? 4 : lat2_rt(k);
+    const int da = k == 4 ? 0 : nbit(k), d1 = k == 4 ? 0 : nbit(k1), d2 = k == 4 ? 0 : nbit(k2);
+    // M[s]: bbar_a summed over signature class s; the counts are cleared alongside
     if (lane < 16) {
         const double *c = sp + lane * CB;
         const double hma = c[1 + da] + class_blocked(k, lane) * c[0];
         const double hm1 = c[1 + d1] + class_blocked(k1, lane) * c[0];
         const double hm2 = c[1 + d2] + class_blocked(k2, lane) * c[0];
-        Ms = (k == 4) ? c[0] : a.p_stay * c[0] + a.p_int * hma + a.p_lat * (hm1 + hm2);
+        sM[lane] = (k == 4) ? c[0] : a.p_stay * c[0] + a.p_int * hma + a.p_lat * (hm1 + hm2);
+        sCnt[lane] = 0;
     }
     // R(b,a) = (p_stay - 1) sum b - sum c_a b + goal terms, sum c_a b = p_stay mass + p_int E_a + p_lat (E_l1 + E_l2)
     // goal terms G(x, a) b(x): the warp's lanes take the entries (all loads of a round in
@@ -233,34 +273,35 @@ __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int
             R = (a.p_stay - 1.0) * mass - Rp + gsum;
         }
     }
-    // P(z|b,a) = sum_s O[s][z] M[s]  (fixed s order)
+    __syncwarp();
+    // P(z|b,a) = sum_s O[s][z] M[s]  (fixed s order); lane z < 16
     double Pz = 0.0;
+    if (lane < 16) {
 #pragma unroll
-    for (int s = 0; s < 16; ++s) {
-        const double m = __shfl_sync(0xffffffffu, Ms, s);
-        if (lane < 16) Pz += sO[s * 16 + lane] * m;
+        for (int s = 0; s < 16; ++s) Pz += sO[s * 16 + lane] * sM[s];
+        sP[lane] = Pz;
     }
-    // ascending-z CDF in fp64, summed sequentially (A.5); kept in shared memory (16 doubles per
-    // warp) rather than 32 registers per lane, which spilled under the kernel's register bound
-    double *C = rsm + a.pstride + 8 + (LEAF ? NA * 32 * NA : 0) + 16 * warp;   // [16] per warp
-    double acc = 0.0;
+    __syncwarp();
+    // ascending-z CDF in fp64, summed sequentially (A.5)
+    if (lane == 0) {
+        double acc = 0.0;
 #pragma unroll
-    for (int z = 0; z < 16; ++z) {
-        acc += __shfl_sync(0xffffffffu, Pz, z);
-        if (lane == 0) C[z] = acc;
+        for (int z = 0; z < 16; ++z) {
+            acc += sP[z];
+            C[z] = acc;
+        }
     }
     __syncwarp();
     // S3: n draws keyed by the tree path (Appendix A.2-A.5)
     const int level = a.level >= 0 ? a.level : path_level(vpath);   // level < 0: from the path
     const uint64_t qpath = vpath | ((uint64_t)(k + 1) << (8 * level));
-    int cntk = 0;
     for (int j0 = 0; j0 < a.n; j0 += 32) {
         const int jj = j0 + lane;
-        int z = -1;
         if (jj < a.n) {
+            int z;
             const uint4 r = philox4x32_10(make_uint4((uint32_t)jj, (uint32_t)qpath, (uint32_t)(qpath >> 32), step),
                                           make_uint2(a.seed, ep));
-            if (a.xs) {            // Alg. 4 literal: x drawn by k_ancestral_x, then x' and z
+            if constexpr (ANC) {   // Alg. 4 literal: x drawn by k_ancestral_x, then x' and z
                 z = ancestral_tail(a, a.xs[q * a.n + jj], k, philox_uniform(r.z), philox_uniform(r.w));
             } else {
                 const double u = philox_uniform(r.x);
@@ -279,19 +320,18 @@ __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int
                 nflag += gap < 1e-6 ? 1 : 0;
             }
             if (a.zdraw) a.zdraw[q * a.n + jj] = (uint8_t)z;
-        }
-#pragma unroll
-        for (int kk = 0; kk < 16; ++kk) {
-            const unsigned bal = __ballot_sync(0xffffffffu, z == kk);
-            if (lane == kk) cntk += __popc(bal);
+            atomicAdd(&sCnt[z], 1);            // integer counts: exact in any order
         }
     }
-    const unsigned um = __ballot_sync(0xffffffffu, lane < 16 && cntk > 0) & 0xFFFFu;
+    __syncwarp();
+    const int cntk = lane < 16 ? sCnt[lane] : 0;
+    const unsigned um = __ballot_sync(0xffffffffu, cntk > 0) & 0xFFFFu;
     const int U = __popc(um);
     leaves += U;
     if (lane < 16) {
         a.P[q * 16 + lane] = Pz;
         a.cnt[q * 16 + lane] = (uint16_t)cntk;
+        if (cntk > 0) sZ[__popc(um & ((1u << lane) - 1u))] = lane;   // rank among the sampled z
     }
     if (lane == 0) {
         a.R[q] = R;
@@ -299,45 +339,66 @@ __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int
         a.U[q] = U;
     }
     if (LEAF) {
-        // S[s][a'] of this action from the linear fields, staged for the (z, a') dot products
-        if (lane < 16) {
-            const double *c = sp + lane * CB;
-            const double oa = class_blocked(k, lane), o1 = class_blocked(k1, lane), o2 = class_blocked(k2, lane);
+        // S[s][a'] of this action from the linear fields: lane -> (s = lane % 16, half of the a')
+        constexpr int NH = (NA + 1) / 2;
+        {
+            const int s = lane & 15, j0 = (lane >> 4) * NH;
+            const double *c = sp + s * CB;
+            const double oa = class_blocked(k, s), o1 = class_blocked(k1, s), o2 = class_blocked(k2, s);
 #pragma unroll
-            for (int j2 = 0; j2 < NA; ++j2) {
-                const double zb = c[9 + j2];
-                const double ha = c[9 + NA + da * NA + j2] + oa * zb;
-                const double h1 = c[9 + NA + d1 * NA + j2] + o1 * zb;
-                const double h2 = c[9 + NA + d2 * NA + j2] + o2 * zb;
-                sS[lane * NA + j2] = (k == 4) ? zb : a.p_stay * zb + a.p_int * ha + a.p_lat * (h1 + h2);
+            for (int t2 = 0; t2 < NH; ++t2) {
+                const int j2 = j0 + t2;
+                if (NA % 2 == 0 || j2 < NA) {
+                    const double zb = c[9 + j2];
+                    const double ha = c[9 + NA + da * NA + j2] + oa * zb;
+                    const double h1 = c[9 + NA + d1 * NA + j2] + o1 * zb;
+                    const double h2 = c[9 + NA + d2 * NA + j2] + o2 * zb;
+                    sS[s * NA + j2] = (k == 4) ? zb : a.p_stay * zb + a.p_int * ha + a.p_lat * (h1 + h2);
+                }
             }
         }
         __syncwarp();
-        // lane -> (u, a'): numerator sum_s O[s][z_u] S[s][a']
-        for (int idx = lane; idx < U * NA; idx += 32) {
-            const int u = idx / NA, j2 = idx % NA;
-            const int z = (int)__fns(um, 0, u + 1);       // the (u+1)-th sampled z, ascending
-            double num = 0.0;
+        // lane -> (u, a'): numerator sum_s O[s][z_u] S[s][a']; the max over a' and
+        // V(z_u) = qbar + max / P(z_u) land in sM[u]
+        double *sV = sM;
+        if constexpr ((NA & (NA - 1)) == 0) {
+            // NA a power of two: a lane group of NA holds one z_u, max by butterfly
+            for (int idx0 = 0; idx0 < U * NA; idx0 += 32) {
+                const int idx = idx0 + lane, u = idx / NA, j2 = idx % NA;
+                double num = -INFINITY;
+                if (idx < U * NA) {
+                    const int z = sZ[u];
+                    num = 0.0;
 #pragma unroll
-            for (int s = 0; s < 16; ++s) num += sO[s * 16 + z] * sS[s * NA + j2];
-            sR[u * NA + j2] = num;
+                    for (int s = 0; s < 16; ++s) num += sO[s * 16 + z] * sS[s * NA + j2];
+                }
+#pragma unroll
+                for (int o = 1; o < NA; o <<= 1) num = fmax(num, __shfl_xor_sync(0xffffffffu, num, o));
+                if (j2 == 0 && idx < U * NA) sV[u] = a.qbar + num / sP[sZ[u]];
+            }
+        } else {
+            for (int idx = lane; idx < U * NA; idx += 32) {
+                const int u = idx / NA, j2 = idx % NA;
+                const int z = sZ[u];
+                double num = 0.0;
+#pragma unroll
+                for (int s = 0; s < 16; ++s) num += sO[s * 16 + z] * sS[s * NA + j2];
+                sR[u * NA + j2] = num;
+            }
+            __syncwarp();
+            if (lane < U) {
+                double best = -INFINITY;
+                for (int j2 = 0; j2 < NA; ++j2) best = fmax(best, sR[lane * NA + j2]);
+                sV[lane] = a.qbar + best / sP[sZ[lane]];
+            }
         }
         __syncwarp();
-        // lane u < U: V(z_u) = qbar + max_a' num / P(z_u); then the backup in ascending z on lane 0
+        // lane u < U: weight f_u / n and V(z_u); the backup in ascending z
         double Vz = 0.0, wz = 0.0;
-        int zu = 0;
         if (lane < U) {
-            zu = (int)__fns(um, 0, lane + 1);
-            double best = -INFINITY;
-            for (int j2 = 0; j2 < NA; ++j2) best = fmax(best, sR[lane * NA + j2]);
-            Vz = best;   // divided below by P(z), held by lane z
-        }
-        const int zsrc = lane < U ? zu : 0;
-        const double Pexact = __shfl_sync(0xffffffffu, Pz, zsrc);
-        const int f = __shfl_sync(0xffffffffu, cntk, zsrc);
-        if (lane < U) {
-            Vz = a.qbar + Vz / Pexact;
-            wz = (double)f / (double)a.n;
+            const int zu = sZ[lane];
+            Vz = sV[lane];
+            wz = (double)sCnt[zu] / (double)a.n;
             if (a.leafV) a.leafV[q * 16 + zu] = Vz;
         }
         double accq = 0.0;
@@ -361,12 +422,14 @@ __host__ __device__ constexpr int reduce_min_blocks() {
     return 1536 / (mask_count(MASK) * 32) > 8 ? 8 : 1536 / (mask_count(MASK) * 32);
 }
 
-template <uint32_t MASK, bool LEAF>
+// ANC: the ancestral sampler's x' and z tail (a.xs set), compiled apart so the marginal sampler's
+// kernel carries none of its registers
+template <uint32_t MASK, bool LEAF, bool ANC>
 __global__ void __launch_bounds__(mask_count(MASK) * 32, reduce_min_blocks<MASK>()) k_reduce(ReduceArgs a) {
     extern __shared__ double rsm[];
     if (a.skip && *a.skip) return;
     if (a.nwork_dev && (long long)blockIdx.x >= *a.nwork_dev) return;
-    reduce_parent<MASK, LEAF>(a, blockIdx.x, rsm, mask_count(MASK) * 32);
+    reduce_parent<MASK, LEAF, ANC>(a, blockIdx.x, rsm, mask_count(MASK) * 32);
 }
 
 // ---- NEXT-3: the state draw x ~ b of Alg. 4 for every sample of every Q-node of a parent ------
@@ -1085,9 +1148,10 @@ template <uint32_t MASK, bool LEAF>
 static qvts_status launch_reduce(Model &m, const ReduceArgs &r, cudaStream_t st) {
     constexpr int NA = mask_count(MASK);
     const size_t smem = sizeof(double) * reduce_smem_doubles<MASK, LEAF>(r.pstride);
-    QVTS_CUDA(cudaFuncSetAttribute(k_reduce<MASK, LEAF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    auto kfn = r.xs ? k_reduce<MASK, LEAF, true> : k_reduce<MASK, LEAF, false>;
+    QVTS_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (r.nwork > 0x7FFFFFFFLL) { set_error("too many parents"); return QVTS_ERR_INVALID_ARG; }
-    QVTS_PROF(LEAF ? 2 : 3, k_reduce<MASK, LEAF><<<(unsigned)r.nwork, NA * 32, smem, st>>>(r));
+    QVTS_PROF(LEAF ? 2 : 3, kfn<<<(unsigned)r.nwork, NA * 32, smem, st>>>(r));
     QVTS_CUDA(cudaGetLastError());
     return QVTS_OK;
 }
