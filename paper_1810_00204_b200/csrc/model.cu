@@ -41,6 +41,26 @@ void DevBuf::release() {
     cap = 0;
 }
 
+qvts_status HostBuf::ensure(size_t bytes) {
+    if (bytes <= cap && p) return QVTS_OK;
+    release();
+    const size_t want = std::max<size_t>(bytes + bytes / 4, 4096);
+    if (cudaHostAlloc(&p, want, cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        p = nullptr;
+        set_error("cudaHostAlloc failed");
+        return QVTS_ERR_CUDA;
+    }
+    cap = want;
+    return QVTS_OK;
+}
+
+void HostBuf::release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+}
+
 
 // ---- instrumentation -----------------------------------------------------------------------------
 static cudaEvent_t next_event(Model &m) {
@@ -469,27 +489,31 @@ extern "C" qvts_status qvts_model_create(const qvts_model_desc *d, qvts_model **
         }
     // Goal terms of R(b,a) = (p_stay - 1) sum b - sum c_a b + sum_x G(x,a) b(x), where
     // G(x,a) = sum_k T'(x,a,k) [N_k(x) = goal] is non-zero only around the goal.
-    std::vector<int32_t> gc_cell, gc_act;
+    // Entries grouped by action (action-major, cells in raster order within an action): k_reduce's
+    // warp for action j reads [gc_off[j], gc_off[j+1]), at most 9 entries (the goal's 3x3 block).
+    std::vector<int32_t> gc_cell, gc_off;
     std::vector<double> gc_val;
     {
         int gr = m->goal / W, gcc = m->goal % W;
-        for (int dr = -1; dr <= 1; ++dr)
-            for (int dc = -1; dc <= 1; ++dc) {
-                int r = gr + dr, c = gcc + dc;
-                if (r < 0 || r >= H || c < 0 || c >= W || m->occ[r * W + c]) continue;
-                int x = r * W + c;
-                for (int j = 0; j < NA; ++j) {
-                    int k = m->action_id[j];
-                    if (k == 4) continue;
+        for (int j = 0; j < NA; ++j) {
+            gc_off.push_back((int32_t)gc_cell.size());
+            const int k = m->action_id[j];
+            if (k == 4) continue;
+            for (int dr = -1; dr <= 1; ++dr)
+                for (int dc = -1; dc <= 1; ++dc) {
+                    int r = gr + dr, c = gcc + dc;
+                    if (r < 0 || r >= H || c < 0 || c >= W || m->occ[r * W + c]) continue;
+                    int x = r * W + c;
                     double g = 0.0;
                     auto hit = [&](int kk) { return (kk == 4) ? (x == m->goal) : (r + st_dr(kk) == gr && c + st_dc(kk) == gcc); };
                     if (hit(k)) g += m->p_int;
                     if (hit(4)) g += m->p_stay;
                     if (hit(lat1(k))) g += m->p_lat;
                     if (hit(lat2(k))) g += m->p_lat;
-                    if (g != 0.0) { gc_cell.push_back(x); gc_act.push_back(j); gc_val.push_back(g); }
+                    if (g != 0.0) { gc_cell.push_back(x); gc_val.push_back(g); }
                 }
-            }
+        }
+        gc_off.push_back((int32_t)gc_cell.size());
     }
     m->ngc = (int)gc_cell.size();
     m->n_free = 0;
@@ -511,7 +535,7 @@ extern "C" qvts_status qvts_model_create(const qvts_model_desc *d, qvts_model **
         if ((st = upload(m->d_O64, O64)) != QVTS_OK) break;
         if ((st = upload(m->d_O32, O32)) != QVTS_OK) break;
         if ((st = upload(m->d_gc_cell, gc_cell)) != QVTS_OK) break;
-        if ((st = upload(m->d_gc_act, gc_act)) != QVTS_OK) break;
+        if ((st = upload(m->d_gc_off, gc_off)) != QVTS_OK) break;
         if ((st = upload(m->d_gc_val, gc_val)) != QVTS_OK) break;
         // band sets: ~16K cells per band for many parents, ~2K for few (more CTAs per parent)
         // big bands: as tall as two CTAs' tiles per SM allow, balanced over the grid
@@ -538,13 +562,14 @@ extern "C" void qvts_model_destroy(qvts_model *m) {
     if (!m) return;
     cudaSetDevice(m->device);
     DevBuf *bufs[] = {&m->d_m8, &m->d_sig, &m->d_cell, &m->bu_R, &m->bu_P, &m->bu_cnt, &m->bu_umask,
-                      &m->bu_U, &m->bu_off, &m->bu_path, &m->bu_root, &m->bu_key, &m->d_ctab, &m->d_R64, &m->d_O64, &m->d_O32, &m->d_gc_cell,
-                      &m->d_gc_act, &m->d_gc_val, &m->d_free, &m->d_V[0], &m->d_V[1], &m->d_A[0], &m->d_A[1], &m->d_alpha64, &m->d_resid,
+                      &m->bu_U, &m->bu_off, &m->bu_path, &m->bu_root, &m->d_ctab, &m->d_R64, &m->d_O64, &m->d_O32, &m->d_gc_cell,
+                      &m->d_gc_off, &m->d_gc_val, &m->d_free, &m->d_V[0], &m->d_V[1], &m->d_A[0], &m->d_A[1], &m->d_alpha64, &m->d_resid,
                       &m->d_Q64, &m->part, &m->xs, &m->scan_tmp, &m->total, &m->counters, &m->vshard,
                       &m->ep_b[0], &m->ep_b[1], &m->ep_state, &m->ep_root_step, &m->ep_root_ep,
                       &m->pb_b0, &m->pb_B, &m->pb_G, &m->pb_Gn, &m->pb_GT, &m->pb_Bbar, &m->pb_Sc, &m->pb_Rb,
                       &m->pb_sel, &m->pb_astar, &m->pb_cand, &m->pb_misc, &m->pb_cls, &m->pb_chunks, &m->pb_part};
     for (DevBuf *b : bufs) b->release();
+    m->bu_host.release();
     for (DevBuf *b : {&m->lm.wr, &m->lm.offs, &m->lm.dmask, &m->lm.cells, &m->lm.qfr, &m->lm.qfr_fib})
         b->release();
     for (BandSet *bs : {&m->band_big, &m->band_small}) {

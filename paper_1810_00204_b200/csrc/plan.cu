@@ -83,7 +83,7 @@ struct ReduceArgs {
     int level, n;
     const double *O64;
     int ngc;
-    const int32_t *gc_cell, *gc_act;
+    const int32_t *gc_cell, *gc_off;   // goal entries grouped by action: [gc_off[j], gc_off[j+1])
     const double *gc_val;
     int goal;
     double p_stay, p_int, p_lat, gamma, qbar;
@@ -148,47 +148,64 @@ __device__ __forceinline__ int ancestral_tail(const ReduceArgs &a, int x, int k,
     return 15;
 }
 
-// One CTA per parent V-node, one warp per action (Q-node).  The CTA first sums the parent's band
-// partials into shared memory (coalesced, fixed band order, fp64); then each warp: per-action
-// recombination of the linear fields -> M[s], P(z|b,a) (Eq. 3 normaliser), R(b,a),
-// n Philox draws (lane j = sample j), counts; for the leaf level also the Q_MDP value of every
-// sampled child, V(z) = qbar + max_a' [sum_s O[s][z] S[s][a']] / P(z), and the Q-node's backup
-// Q = R + gamma sum_z (f_z/n) V(z) in ascending z (Alg. 6 with gamma, R13).
+// One CTA per parent V-node, one warp per action (Q-node).  The CTA first brings the parent's
+// record into shared memory (one bulk copy when there is one band, as at every leaf level; else
+// the band records summed in fixed band order, fp64); then each warp: per-action recombination of
+// the linear fields -> M[s], P(z|b,a) (Eq. 3 normaliser), R(b,a), n Philox draws
+// (lane j = sample j), counts; for the leaf level also the Q_MDP value of every sampled child,
+// V(z) = qbar + max_a' [sum_s O[s][z] S[s][a']] / P(z), and the Q-node's backup
+// Q = R + gamma sum_z (f_z/n) V(z) (Alg. 6 with gamma, R13).
 //
-// Shared memory (doubles): band sums [pstride] | E[8], sum b, pad [16] | per warp: scratch
-// [kRedWarpScratch + (LEAF ? 32 NA : 0)] | O[16][16].  A warp's scratch: M[s] (then the leaf values
-// V(z_u)), P(z|b,a), the ascending CDF, 16 counts and the compacted sampled-z list (ints), and at
-// the leaf S[s][a'] and the (z_u, a') numerators.
-constexpr int kRedWarpScratch = 16 + 16 + 16 + 16;
-template <uint32_t MASK, bool LEAF>
-__host__ __device__ constexpr int reduce_warp_doubles() {
-    return kRedWarpScratch + (LEAF ? 32 * mask_count(MASK) : 0);
-}
+// Both sums over signatures, P(z) = sum_s O[s][z] M[s] and the numerators, use that O is the
+// Kronecker product of the four sensors' 2x2 matrices K = [[acc, 1-acc], [1-acc, acc]] (PAPER.md:336,
+// reading R7): lane s holds the vector, four butterfly stages x <- acc x + (1-acc) x(lane ^ 2^b)
+// leave sum_s O[s][z] x[s] on lane z (both half-warps hold it), 4 x 2 shuffles + 2 FP operations
+// per vector instead of a 16 x 16 product.
+//
+// Shared memory (doubles): the parent's record [pstride] | E[8], sum b, pad [16] | per warp
+// [kRedWarpScratch]: P(z|b,a) [16], the ascending CDF [16], 16 draw counts (ints).
+constexpr int kRedWarpScratch = 16 + 16 + 16;
 template <uint32_t MASK, bool LEAF>
 __host__ __device__ constexpr int reduce_smem_doubles(int pstride) {
-    return pstride + 16 + mask_count(MASK) * reduce_warp_doubles<MASK, LEAF>() + 256;
+    return pstride + 16 + mask_count(MASK) * kRedWarpScratch;
 }
 
 // Executed by a CTA of |A| warps for parent w; warp j handles action j.
-// rsm: reduce_smem_doubles(pstride) doubles of shared memory.
+// rsm: reduce_smem_doubles(pstride) doubles of shared memory (16-byte aligned; pstride even).
 template <uint32_t MASK, bool LEAF, bool ANC>
 __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int nthreads) {
     constexpr int NA = mask_count(MASK);
     constexpr int CB = hist_cb<MASK, LEAF>();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double *sp = rsm;                          // [pstride] band-summed partials
-    double *sE = rsm + a.pstride;              // [8] blocked-mass totals, [8] = sum b
-    double *sO = sE + 16 + NA * reduce_warp_doubles<MASK, LEAF>();   // O[s][z]
-    for (int i = threadIdx.x; i < 256; i += nthreads) sO[i] = a.O64[i];
+    const int sl = lane & 15, hf = lane >> 4;  // signature / z of the lane, half-warp
+    double *sp = rsm;                          // [pstride] band-summed record
+    double *sE = rsm + a.pstride;              // [8] blocked-mass totals, [8] = sum b, [9] = 1/n
     const double *pp = a.part + w * a.nb * (long long)a.pstride;
-    // band sum, fixed band order (sequential over bands); a thread takes two adjacent elements per
-    // pass as one 16-byte load per band (pstride is even), 4 bands in flight; one band: a copy
-    const double2 *pp2 = reinterpret_cast<const double2 *>(pp);
-    double2 *sp2 = reinterpret_cast<double2 *>(sp);
-    const int half = a.pstride >> 1;
     if (a.nb == 1) {
-        for (int i = threadIdx.x; i < half; i += nthreads) sp2[i] = pp2[i];
+        // one band: the record is a plain copy -- one bulk (TMA) copy, an mbarrier for completion
+        __shared__ alignas(8) unsigned long long s_bar;
+        const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_bar);
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar));
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+            const uint32_t bytes = (uint32_t)(8 * a.pstride);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                             (uint32_t)__cvta_generic_to_shared(sp)),
+                         "l"(pp), "r"(bytes), "r"(bar)
+                         : "memory");
+        }
+        __syncthreads();                       // the barrier is initialised before anyone waits
+        asm volatile(
+            "{\n .reg .pred P1;\n WAIT_%=:\n"
+            " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
+            " @!P1 bra WAIT_%=;\n}\n" ::"r"(bar) : "memory");
     } else {
+        // band records summed in fixed band order; a thread takes two adjacent elements per pass
+        // as one 16-byte load per band (pstride is even), 4 bands in flight
+        const double2 *pp2 = reinterpret_cast<const double2 *>(pp);
+        double2 *sp2 = reinterpret_cast<double2 *>(sp);
+        const int half = a.pstride >> 1;
         for (int i = threadIdx.x; i < half; i += nthreads) {
             double acc0 = 0.0, acc1 = 0.0;
             for (int bd = 0; bd < a.nb; bd += 4) {
@@ -202,25 +219,40 @@ __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int
             }
             sp2[i] = make_double2(acc0, acc1);
         }
+        __syncthreads();
     }
-    __syncthreads();
     // E[d] = sum_y occ(y + d) b(y); orthogonal directions come from the class masses (signature
-    // bit); thread 8: the belief mass sum_s (class mass), ascending s
+    // bit: the 8 classes with bit kd/2 set, ascending); thread 8: the belief mass sum_s (class
+    // mass), ascending s; threads 32 + j: action j's stencil ids and field indices, packed
+    __shared__ uint32_t s_pack[9];
     if (threadIdx.x < 9) {
         const int d = threadIdx.x;
         double e;
         if (d == 8) {
             e = 0.0;
+#pragma unroll
             for (int s2 = 0; s2 < 16; ++s2) e += sp[s2 * CB];
         } else {
             const int kd = d < 4 ? d : d + 1;
             e = sp[16 * CB + d];
             if (is_orth(kd)) {
+                const int bt = kd >> 1;              // orth_bit(kd)
                 e = 0.0;
-                for (int s2 = 0; s2 < 16; ++s2) e += class_blocked(kd, s2) * sp[s2 * CB];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int s2 = ((i >> bt) << (bt + 1)) | (1 << bt) | (i & ((1 << bt) - 1));
+                    e += sp[s2 * CB];
+                }
             }
         }
         sE[d] = e;
+    } else if (threadIdx.x >= 32 && threadIdx.x < 32 + NA) {
+        const int k = action_of<MASK>(threadIdx.x - 32);
+        const int k1 = k == 4 ? 4 : lat1_rt(k), k2 = k == 4 ? 4 : lat2_rt(k);
+        const int da = k == 4 ? 0 : nbit(k), d1 = k == 4 ? 0 : nbit(k1), d2 = k == 4 ? 0 : nbit(k2);
+        s_pack[threadIdx.x - 32] = (uint32_t)(k | k1 << 4 | k2 << 8 | da << 12 | d1 << 16 | d2 << 20);
+    } else if (threadIdx.x == 64) {
+        sE[9] = 1.0 / (double)a.n;
     }
     __syncthreads();
     const long long v = a.vmap ? (long long)a.vmap[w] : w;
@@ -229,40 +261,44 @@ __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int
     const uint64_t vpath = a.vpath[v];
     const int root = a.vroot[v];
     const uint32_t step = a.root_step[root], ep = a.root_ep[root];
+    const double ka = a.acc, kb = 1.0 - a.acc;  // the sensor matrix K
     int nflag = 0, leaves = 0;
     {
     const int j = warp;                        // this warp's action (the CTA has |A| warps)
-    double *sW = sE + 16 + warp * reduce_warp_doubles<MASK, LEAF>();
-    double *sM = sW;                           // [16] M[s]; at the leaf later V(z_u)
-    double *sP = sW + 16;                      // [16] P(z|b,a)
-    double *C = sW + 32;                       // [16] ascending CDF
-    int *sCnt = reinterpret_cast<int *>(sW + 48);   // [16] draw counts per z
-    int *sZ = sCnt + 16;                       // [16] the sampled z's, ascending
-    double *sS = sW + kRedWarpScratch;         // [16][NA] S of this warp's action (leaf)
-    double *sR = sS + 16 * NA;                 // [16][NA] its (z_u, a') numerators (leaf, NA not 2^k)
+    double *sW = sE + 16 + warp * kRedWarpScratch;
+    double *sP = sW;                           // [16] P(z|b,a)
+    double *C = sW + 16;                       // [16] ascending CDF
+    int *sCnt = reinterpret_cast<int *>(sW + 32);   // [16] draw counts per z
     const long long q = w * NA + j;
-    const int k = action_of<MASK>(j);
-    const int k1 = k == 4 ? 4 : lat1_rt(k), k2 = k == 4 ? 4 : lat2_rt(k);
-    const int da = k == 4 ? 0 : nbit(k), d1 = k == 4 ? 0 : nbit(k1), d2 = k == 4 ? 0 : nbit(k2);
-    // M[s]: bbar_a summed over signature class s; the counts are cleared alongside
-    if (lane < 16) {
-        const double *c = sp + lane * CB;
-        const double hma = c[1 + da] + class_blocked(k, lane) * c[0];
-        const double hm1 = c[1 + d1] + class_blocked(k1, lane) * c[0];
-        const double hm2 = c[1 + d2] + class_blocked(k2, lane) * c[0];
-        sM[lane] = (k == 4) ? c[0] : a.p_stay * c[0] + a.p_int * hma + a.p_lat * (hm1 + hm2);
-        sCnt[lane] = 0;
+    const uint32_t pk = s_pack[j];
+    const int k = pk & 15, k1 = (pk >> 4) & 15, k2 = (pk >> 8) & 15;
+    const int da = (pk >> 12) & 15, d1 = (pk >> 16) & 15, d2 = (pk >> 20) & 15;
+    // the taps' blocked bits for class sl (class_blocked as predicates: h + [blocked] x is the add or h)
+    const bool ba = class_blocked(k, sl) != 0.0, b1 = class_blocked(k1, sl) != 0.0, b2 = class_blocked(k2, sl) != 0.0;
+    const double *c = sp + sl * CB;            // class sl's record
+    // M[s]: bbar_a summed over signature class s (lane s and s + 16); the counts are cleared
+    double Pz;
+    {
+        const double c0 = c[0];
+        double hma = c[1 + da], hm1 = c[1 + d1], hm2 = c[1 + d2];
+        if (ba) hma += c0;
+        if (b1) hm1 += c0;
+        if (b2) hm2 += c0;
+        Pz = (k == 4) ? c0 : a.p_stay * c0 + a.p_int * hma + a.p_lat * (hm1 + hm2);
     }
-    // R(b,a) = (p_stay - 1) sum b - sum c_a b + goal terms, sum c_a b = p_stay mass + p_int E_a + p_lat (E_l1 + E_l2)
-    // goal terms G(x, a) b(x): the warp's lanes take the entries (all loads of a round in
-    // flight at once instead of one dependent chain per entry on lane 0), fixed-order tree sum
+    if (lane < 16) sCnt[lane] = 0;
+    // P(z|b,a) = sum_s O[s][z] M[s]: the four sensor butterflies, lane z
+#pragma unroll
+    for (int bt = 1; bt < 16; bt <<= 1) Pz = fma(ka, Pz, kb * __shfl_xor_sync(0xffffffffu, Pz, bt));
+    // R(b,a) = (p_stay - 1) sum b - sum c_a b + goal terms, sum c_a b = p_stay mass + p_int E_a + p_lat (E_l1 + E_l2);
+    // goal terms G(x, a) b(x): this action's <= 9 entries (model.cu groups them by action), one
+    // per lane, tree sum
     double gsum = 0.0;
     if (k != 4) {
-        for (int g = lane; g < a.ngc; g += 32)
-            if (a.gc_act[g] == j)
-                gsum += a.gc_val[g] * (double)bp[a.gc_cell[g]];
+        const int g0 = a.gc_off[j], ng = a.gc_off[j + 1] - g0;
+        if (lane < ng) gsum = a.gc_val[g0 + lane] * (double)bp[a.gc_cell[g0 + lane]];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) gsum += __shfl_xor_sync(0xffffffffu, gsum, o);
+        for (int o = 8; o > 0; o >>= 1) gsum += __shfl_xor_sync(0xffffffffu, gsum, o);
     }
     double R = 0.0;
     if (lane == 0) {
@@ -273,22 +309,22 @@ __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int
             R = (a.p_stay - 1.0) * mass - Rp + gsum;
         }
     }
-    __syncwarp();
-    // P(z|b,a) = sum_s O[s][z] M[s]  (fixed s order); lane z < 16
-    double Pz = 0.0;
-    if (lane < 16) {
-#pragma unroll
-        for (int s = 0; s < 16; ++s) Pz += sO[s * 16 + lane] * sM[s];
-        sP[lane] = Pz;
-    }
+    if (lane < 16) sP[lane] = Pz;
     __syncwarp();
     // ascending-z CDF in fp64, summed sequentially (A.5)
     if (lane == 0) {
+        const double2 *p2 = reinterpret_cast<const double2 *>(sP);
+        double2 *c2 = reinterpret_cast<double2 *>(C);
         double acc = 0.0;
 #pragma unroll
-        for (int z = 0; z < 16; ++z) {
-            acc += sP[z];
-            C[z] = acc;
+        for (int i = 0; i < 8; ++i) {
+            const double2 pv = p2[i];
+            double2 cv;
+            acc += pv.x;
+            cv.x = acc;
+            acc += pv.y;
+            cv.y = acc;
+            c2[i] = cv;
         }
     }
     __syncwarp();
@@ -324,14 +360,13 @@ __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int
         }
     }
     __syncwarp();
-    const int cntk = lane < 16 ? sCnt[lane] : 0;
+    const int cntk = sCnt[sl];                 // lane z and z + 16
     const unsigned um = __ballot_sync(0xffffffffu, cntk > 0) & 0xFFFFu;
     const int U = __popc(um);
     leaves += U;
     if (lane < 16) {
         a.P[q * 16 + lane] = Pz;
         a.cnt[q * 16 + lane] = (uint16_t)cntk;
-        if (cntk > 0) sZ[__popc(um & ((1u << lane) - 1u))] = lane;   // rank among the sampled z
     }
     if (lane == 0) {
         a.R[q] = R;
@@ -339,71 +374,44 @@ __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int
         a.U[q] = U;
     }
     if (LEAF) {
-        // S[s][a'] of this action from the linear fields: lane -> (s = lane % 16, half of the a')
+        // S[s][a'] of this action from the linear fields, lane -> (s, this half's a'), then the same
+        // butterflies: lane z holds the numerators sum_s O[s][z] S[s][a'] of its half's a'
         constexpr int NH = (NA + 1) / 2;
-        {
-            const int s = lane & 15, j0 = (lane >> 4) * NH;
-            const double *c = sp + s * CB;
-            const double oa = class_blocked(k, s), o1 = class_blocked(k1, s), o2 = class_blocked(k2, s);
+        const double c0 = c[0];
+        double Sv[NH];
 #pragma unroll
-            for (int t2 = 0; t2 < NH; ++t2) {
-                const int j2 = j0 + t2;
-                if (NA % 2 == 0 || j2 < NA) {
-                    const double zb = c[9 + j2];
-                    const double ha = c[9 + NA + da * NA + j2] + oa * zb;
-                    const double h1 = c[9 + NA + d1 * NA + j2] + o1 * zb;
-                    const double h2 = c[9 + NA + d2 * NA + j2] + o2 * zb;
-                    sS[s * NA + j2] = (k == 4) ? zb : a.p_stay * zb + a.p_int * ha + a.p_lat * (h1 + h2);
-                }
+        for (int t2 = 0; t2 < NH; ++t2) {
+            const int j2 = hf * NH + t2;
+            Sv[t2] = 0.0;
+            if (NA % 2 == 0 || j2 < NA) {
+                const double zb = c[9 + j2];
+                double ha = c[9 + NA + da * NA + j2], h1 = c[9 + NA + d1 * NA + j2], h2 = c[9 + NA + d2 * NA + j2];
+                if (ba) ha += zb;
+                if (b1) h1 += zb;
+                if (b2) h2 += zb;
+                Sv[t2] = (k == 4) ? zb : a.p_stay * zb + a.p_int * ha + a.p_lat * (h1 + h2);
             }
         }
-        __syncwarp();
-        // lane -> (u, a'): numerator sum_s O[s][z_u] S[s][a']; the max over a' and
-        // V(z_u) = qbar + max / P(z_u) land in sM[u]
-        double *sV = sM;
-        if constexpr ((NA & (NA - 1)) == 0) {
-            // NA a power of two: a lane group of NA holds one z_u, max by butterfly
-            for (int idx0 = 0; idx0 < U * NA; idx0 += 32) {
-                const int idx = idx0 + lane, u = idx / NA, j2 = idx % NA;
-                double num = -INFINITY;
-                if (idx < U * NA) {
-                    const int z = sZ[u];
-                    num = 0.0;
+        (void)c0;
 #pragma unroll
-                    for (int s = 0; s < 16; ++s) num += sO[s * 16 + z] * sS[s * NA + j2];
-                }
+        for (int bt = 1; bt < 16; bt <<= 1)
 #pragma unroll
-                for (int o = 1; o < NA; o <<= 1) num = fmax(num, __shfl_xor_sync(0xffffffffu, num, o));
-                if (j2 == 0 && idx < U * NA) sV[u] = a.qbar + num / sP[sZ[u]];
-            }
-        } else {
-            for (int idx = lane; idx < U * NA; idx += 32) {
-                const int u = idx / NA, j2 = idx % NA;
-                const int z = sZ[u];
-                double num = 0.0;
+            for (int t2 = 0; t2 < NH; ++t2) Sv[t2] = fma(ka, Sv[t2], kb * __shfl_xor_sync(0xffffffffu, Sv[t2], bt));
+        double best = -INFINITY;
 #pragma unroll
-                for (int s = 0; s < 16; ++s) num += sO[s * 16 + z] * sS[s * NA + j2];
-                sR[u * NA + j2] = num;
-            }
-            __syncwarp();
-            if (lane < U) {
-                double best = -INFINITY;
-                for (int j2 = 0; j2 < NA; ++j2) best = fmax(best, sR[lane * NA + j2]);
-                sV[lane] = a.qbar + best / sP[sZ[lane]];
-            }
+        for (int t2 = 0; t2 < NH; ++t2)
+            if (NA % 2 == 0 || hf * NH + t2 < NA) best = fmax(best, Sv[t2]);
+        best = fmax(best, __shfl_xor_sync(0xffffffffu, best, 16));
+        // lane z < 16, z sampled: V(z) = qbar + max_a' num / P(z); the backup sums f_z V(z)
+        double fv = 0.0;
+        if (lane < 16 && cntk > 0) {
+            const double Vz = a.qbar + best / Pz;
+            if (a.leafV) a.leafV[q * 16 + lane] = Vz;
+            fv = (double)cntk * Vz;
         }
-        __syncwarp();
-        // lane u < U: weight f_u / n and V(z_u); the backup in ascending z
-        double Vz = 0.0, wz = 0.0;
-        if (lane < U) {
-            const int zu = sZ[lane];
-            Vz = sV[lane];
-            wz = (double)sCnt[zu] / (double)a.n;
-            if (a.leafV) a.leafV[q * 16 + zu] = Vz;
-        }
-        double accq = 0.0;
-        for (int u = 0; u < U; ++u) accq += __shfl_sync(0xffffffffu, wz, u) * __shfl_sync(0xffffffffu, Vz, u);
-        if (lane == 0) a.Q[q] = R + a.gamma * accq;
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) fv += __shfl_xor_sync(0xffffffffu, fv, o);
+        if (lane == 0) a.Q[q] = R + a.gamma * (fv * sE[9]);     // sE[9] = 1/n
     }
     }   // this warp's action
     // flagged-draw and leaf counts: per warp, one global atomic each (counts are integers)
@@ -1151,6 +1159,7 @@ static qvts_status launch_reduce(Model &m, const ReduceArgs &r, cudaStream_t st)
     auto kfn = r.xs ? k_reduce<MASK, LEAF, true> : k_reduce<MASK, LEAF, false>;
     QVTS_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (r.nwork > 0x7FFFFFFFLL) { set_error("too many parents"); return QVTS_ERR_INVALID_ARG; }
+    if (r.pstride & 1) { set_error("record stride must be even (16-byte bulk copies)"); return QVTS_ERR_INVALID_ARG; }
     QVTS_PROF(LEAF ? 2 : 3, kfn<<<(unsigned)r.nwork, NA * 32, smem, st>>>(r));
     QVTS_CUDA(cudaGetLastError());
     return QVTS_OK;
@@ -1240,7 +1249,7 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
             r.beliefs = bel; r.bstride = bstride; r.vpath = vl.path.as<uint64_t>(); r.vroot = vl.root.as<int32_t>();
             r.root_step = roots.step_dev; r.root_ep = roots.episode_dev; r.seed = cfg.seed;
             r.level = d; r.n = n; r.O64 = m.d_O64.as<double>();
-            r.ngc = m.ngc; r.gc_cell = m.d_gc_cell.as<int32_t>(); r.gc_act = m.d_gc_act.as<int32_t>();
+            r.ngc = m.ngc; r.gc_cell = m.d_gc_cell.as<int32_t>(); r.gc_off = m.d_gc_off.as<int32_t>();
             r.gc_val = m.d_gc_val.as<double>(); r.goal = m.goal;
             r.p_stay = m.p_stay; r.p_int = m.p_int; r.p_lat = m.p_lat; r.gamma = m.gamma;
             r.qbar = m.cur_leaf == QVTS_LEAF_FIB ? m.qbar_fib : m.qbar;
@@ -1412,7 +1421,7 @@ static qvts_status plan_levels_dev_t(Model &m, const float *root, const qvts_pla
         r.beliefs = bel; r.bstride = bstride; r.vpath = vl.path.as<uint64_t>(); r.vroot = vl.root.as<int32_t>();
         r.root_step = m.ep_root_step.as<uint32_t>(); r.root_ep = m.ep_root_ep.as<uint32_t>(); r.seed = cfg.seed;
         r.level = d; r.n = n; r.O64 = m.d_O64.as<double>();
-        r.ngc = m.ngc; r.gc_cell = m.d_gc_cell.as<int32_t>(); r.gc_act = m.d_gc_act.as<int32_t>();
+        r.ngc = m.ngc; r.gc_cell = m.d_gc_cell.as<int32_t>(); r.gc_off = m.d_gc_off.as<int32_t>();
         r.gc_val = m.d_gc_val.as<double>(); r.goal = m.goal;
         r.p_stay = m.p_stay; r.p_int = m.p_int; r.p_lat = m.p_lat; r.gamma = m.gamma;
         r.qbar = m.cur_leaf == QVTS_LEAF_FIB ? m.qbar_fib : m.qbar;
@@ -1558,9 +1567,9 @@ static qvts_status root_marginals_t(Model &m, const RootBatch &roots, cudaStream
     r.part = m.part.as<double>(); r.pstride = pstride; r.nb = nb_eff; r.nwork = nwork; r.vmap = roots.active;
     r.beliefs = roots.beliefs; r.bstride = roots.stride; r.vpath = v0.path.as<uint64_t>(); r.vroot = v0.root.as<int32_t>();
     r.root_step = roots.step_dev; r.root_ep = roots.episode_dev; r.n = 1; r.O64 = m.d_O64.as<double>();
-    r.ngc = m.ngc; r.gc_cell = m.d_gc_cell.as<int32_t>(); r.gc_act = m.d_gc_act.as<int32_t>();
+    r.ngc = m.ngc; r.gc_cell = m.d_gc_cell.as<int32_t>(); r.gc_off = m.d_gc_off.as<int32_t>();
     r.gc_val = m.d_gc_val.as<double>(); r.goal = m.goal; r.p_stay = m.p_stay; r.p_int = m.p_int; r.p_lat = m.p_lat;
-    r.gamma = m.gamma; r.R = ql.R.as<double>(); r.P = ql.P.as<double>(); r.cnt = ql.cnt.as<uint16_t>();
+    r.gamma = m.gamma; r.acc = m.acc; r.R = ql.R.as<double>(); r.P = ql.P.as<double>(); r.cnt = ql.cnt.as<uint16_t>();
     r.umask = ql.umask.as<uint16_t>(); r.U = ql.U.as<int32_t>();
     return launch_reduce<MASK, false>(m, r, st);
 }
@@ -1614,7 +1623,7 @@ static qvts_status expand_marginals_t(Model &m, const ExpandSpec &e, QLevel &ql,
     r.beliefs = e.beliefs; r.bstride = e.bstride; r.vpath = e.vpath; r.vroot = e.vroot;
     r.root_step = e.root_step; r.root_ep = e.root_ep; r.seed = e.seed; r.level = e.level; r.n = e.n;
     r.O64 = m.d_O64.as<double>(); r.ngc = m.ngc; r.gc_cell = m.d_gc_cell.as<int32_t>();
-    r.gc_act = m.d_gc_act.as<int32_t>(); r.gc_val = m.d_gc_val.as<double>(); r.goal = m.goal;
+    r.gc_off = m.d_gc_off.as<int32_t>(); r.gc_val = m.d_gc_val.as<double>(); r.goal = m.goal;
     r.p_stay = m.p_stay; r.p_int = m.p_int; r.p_lat = m.p_lat; r.gamma = m.gamma;
     r.R = ql.R.as<double>(); r.P = ql.P.as<double>(); r.cnt = ql.cnt.as<uint16_t>();
     r.umask = ql.umask.as<uint16_t>(); r.U = ql.U.as<int32_t>(); r.Q = ql.Q.as<double>();
@@ -1681,7 +1690,7 @@ static qvts_status bf_expand_launch_t(Model &m, const BfLaunch &L, QLevel &ql, c
     r.beliefs = L.bel; r.bstride = L.stride; r.vpath = L.path; r.vroot = L.root;
     r.root_step = L.root_step; r.root_ep = L.root_ep; r.seed = L.seed; r.level = -1; r.n = L.n;
     r.O64 = m.d_O64.as<double>(); r.ngc = m.ngc; r.gc_cell = m.d_gc_cell.as<int32_t>();
-    r.gc_act = m.d_gc_act.as<int32_t>(); r.gc_val = m.d_gc_val.as<double>(); r.goal = m.goal;
+    r.gc_off = m.d_gc_off.as<int32_t>(); r.gc_val = m.d_gc_val.as<double>(); r.goal = m.goal;
     r.p_stay = m.p_stay; r.p_int = m.p_int; r.p_lat = m.p_lat; r.gamma = m.gamma;
     r.R = ql.R.as<double>(); r.P = ql.P.as<double>(); r.cnt = ql.cnt.as<uint16_t>();
     r.umask = ql.umask.as<uint16_t>(); r.U = ql.U.as<int32_t>(); r.Q = ql.Q.as<double>();
@@ -2034,103 +2043,148 @@ __global__ void __launch_bounds__(256) k_bu_marg(CorrectArgs a, double *__restri
         part[grp * a.ntiles + tile] = sm;
     }
 }
-// Batched Eq. 3 in ONE pass over b (K9 at HBM rate): one thread-block cluster per belief, CTA
-// rank r owns rows [r R, (r+1) R).  Each CTA stages its rows (+1-row halo) in shared memory with
-// one cp.async burst; every thread predicts its <= kBuGroups groups of 4 cells ONCE (action
-// geometry compile-time) and keeps bbar and the signatures in registers, adds its part of
-// P(z|b,a) = sum_y O[sig(y)][z] bbar_a(y) (fp32 per thread, fp64 across threads in fixed order),
-// the cluster sums the NC parts in rank order through DSMEM (every CTA gets the same bits), and
-// the thread writes b' = (O[s][z] / P) bbar from its registers with streaming float4 stores --
-// b is read once and b' written once.  Same fp32 prediction and weights as k_correct.
-
-// One kernel for every action: the three source taps of the selected action (the intended move
-// and its two ring laterals, reading R3) are runtime offsets into the staged rows and runtime bits
-// of the occupancy byte, so every CTA runs the same small code path (one launch per batch).
+// Batched Eq. 3 in ONE pass over b (K9 at HBM rate): one thread-block cluster of NC CTAs per
+// belief, CTA rank r owns rows [r R, (r+1) R).  Each CTA stages its rows (+1-row halo) in shared
+// memory with one cp.async burst; every thread predicts its <= G groups of 4 cells ONCE, keeps
+// O[sig(y)][z] bbar_a(y) in registers and adds its part of P(z|b,a) = sum_y O[sig(y)][z] bbar_a(y)
+// (fp32 per thread, fp64 across threads in fixed order); the cluster sums the NC parts in rank
+// order through DSMEM (every CTA gets the same bits) and the thread writes
+// b' = (O[sig][z] bbar) (1/P) from its registers with streaming float4 stores: b is read once and
+// b' written once.
+//
+// Per cell the prediction is bbar = p_int b(y - d_a) + p_lat (b(y - d_l1) + b(y - d_l2)) +
+// c(m8(y)) b(y), c = p_stay + p_int [y + d_a blocked] + p_lat ([y + d_l1 blocked] +
+// [y + d_l2 blocked]) (the blocked moves' mass stays, Eq. 2), with c tabulated over the 256
+// occupancy bytes and O[sig][z] over the 32 (occupied, sig) codes (0 for an occupied cell) once
+// per CTA: three tap loads, two table loads and five FP operations per cell.  One code path for
+// every action: the three source taps (the intended move and its two ring laterals, reading R3)
+// are runtime offsets into the staged rows; stay has coefficients (1, 0, 0).  The fp32 rounding
+// differs from k_correct's by O(1 ulp) (the two-pass path, compared in the tests).
 struct BuActs { int act[9]; };
-constexpr int kBuGroups = 11;        // 4-cell groups per thread (rows_cta * W / 4 <= 11 * 256)
-__global__ void __launch_bounds__(256, 3) k_bu_cluster(CorrectArgs a, double *__restrict__ pout, int NA, BuActs acts) {
+struct BuArgs {
+    const float *beliefs;
+    long long bstride;
+    const uint8_t *m8, *cell;
+    const double *O64;
+    const int32_t *sel_q, *sel_z, *sel_out;
+    float *out;
+    long long ostride;
+    double *pout;
+    int n, NA, H, W, rows, TPc;
+    float p_int, p_stay, p_lat;
+    BuActs acts;
+};
+constexpr int kBuThreads = 256;
+constexpr int kBuGroups = 8;         // 4-cell groups per thread: rows * W / 4 <= 8 * 256
+
+__global__ void __launch_bounds__(kBuThreads, 4) k_bu_cluster(BuArgs a) {
     namespace cg = cooperative_groups;
+    constexpr int G = kBuGroups;
     cg::cluster_group cl = cg::this_cluster();
     const int NC = (int)cl.num_blocks();
     const int rank = (int)cl.block_rank();
-    const long long grp = blockIdx.x / NC;
-    const long long q = a.sel_q[grp];
-    const int zsel = a.sel_z[grp];
-    const int k = acts.act[q % NA];
-    const float *__restrict__ b = a.beliefs + (q / NA) * a.bstride;
-    const int W = a.W, TPc = a.stage_tp;
-    const int r0 = rank * a.rows_cta, r1 = min(a.H, r0 + a.rows_cta);
-    // tap geometry: source y - d of each tap as a row-major offset, its blocked bit in m8
-    const bool stay = k == 4;
-    const int k1 = stay ? 4 : lat1(k), k2 = stay ? 4 : lat2(k);
-    const int offa = -st_dr(k) * TPc - st_dc(k), off1 = -st_dr(k1) * TPc - st_dc(k1), off2 = -st_dr(k2) * TPc - st_dc(k2);
-    const uint32_t bita = stay ? 0u : (uint32_t)nbit(k), bit1 = stay ? 0u : (uint32_t)nbit(k1), bit2 = stay ? 0u : (uint32_t)nbit(k2);
+    const long long g = blockIdx.x / NC;
+    const long long q = a.sel_q[g];
+    const int zsel = a.sel_z[g];
+    const int k = a.acts.act[q % a.NA];
+    const float *__restrict__ b = a.beliefs + (q / a.NA) * a.bstride;
+    const int W = a.W, TPc = a.TPc, W4 = W >> 2;
+    const int r0 = rank * a.rows, r1 = min(a.H, r0 + a.rows), nrows = r1 - r0;
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     extern __shared__ float4 bu_smem4[];
     float *stile = reinterpret_cast<float *>(bu_smem4);
-    __shared__ float s_o[16], s_w[16];
-    __shared__ double wsum[8], s_part;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x < 16) s_o[threadIdx.x] = (float)a.O64[threadIdx.x * 16 + zsel];
-    // stage rows [r0 - 1, r1 + 1): off-map rows and the halo columns are zero
-    const int nr = r1 - r0 + 2, W4 = W >> 2;
-    for (int tr = warp; tr < nr; tr += 8) {
-        const int rr = r0 - 1 + tr;
-        const bool ok = rr >= 0 && rr < a.H;
-        const float *src = ok ? b + (long long)rr * W : b;
-        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(stile + tr * TPc + 4);
-        for (int c4 = lane; c4 < W4; c4 += 32)
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst + 16u * c4),
-                         "l"(ok ? src + 4 * c4 : src), "r"(ok ? 16 : 0));
-        if (lane == 0) {
+    __shared__ float s_c[256], s_t[32];
+    __shared__ double wsum[8], s_parts[8];        // s_parts[r]: rank r's part, pushed by rank r
+    // stage rows [r0 - 1, r1 + 1) by bulk (TMA) copies, one row per lane of warp 0, completion on
+    // an mbarrier; off-map rows and the halo columns are zeroed by the other threads meanwhile
+    const int nr = nrows + 2;
+    __shared__ alignas(8) unsigned long long s_bar;
+    __shared__ alignas(8) unsigned long long s_rbar;   // NC arrivals: every rank's part is here
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_bar);
+    const uint32_t rbar = (uint32_t)__cvta_generic_to_shared(&s_rbar);
+    const int lo = r0 == 0 ? 1 : 0, hi = r1 == a.H ? nr - 1 : nr;     // on-map staged rows
+    if (t == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(rbar), "r"(NC));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar),
+                     "r"((uint32_t)((hi - lo) * W * 4)) : "memory");
+    }
+    // every CTA's barriers are initialised before any rank pushes into them: arrive now, wait
+    // just before the push (the staging and the prediction run in between)
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+    if (warp == 0) {
+        __syncwarp();
+        for (int tr = lo + lane; tr < hi; tr += 32)
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                             (uint32_t)__cvta_generic_to_shared(stile + tr * TPc + 4)),
+                         "l"(b + (long long)(r0 - 1 + tr) * W), "r"((uint32_t)(W * 4)), "r"(bar)
+                         : "memory");
+    } else {
+        for (int tr = t - 32; tr < nr; tr += kBuThreads - 32) {
             stile[tr * TPc + 3] = 0.f;
             stile[tr * TPc + 4 + W] = 0.f;
         }
+        for (int c = t - 32; c < W; c += kBuThreads - 32) {
+            if (lo) stile[4 + c] = 0.f;
+            if (hi < nr) stile[(nr - 1) * TPc + 4 + c] = 0.f;
+        }
     }
-    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
-    __syncthreads();
+    // meanwhile: this action's staying-mass coefficient over the occupancy bytes, the O weights
+    const bool stay = k == 4;
+    const int k1 = stay ? 4 : lat1_rt(k), k2 = stay ? 4 : lat2_rt(k);
+    {
+        float c = stay ? 1.f : a.p_stay;
+        if (!stay) {
+            if ((t >> nbit(k)) & 1) c += a.p_int;
+            if ((t >> nbit(k1)) & 1) c += a.p_lat;
+            if ((t >> nbit(k2)) & 1) c += a.p_lat;
+        }
+        s_c[t] = c;
+        if (t < 32) s_t[t] = t < 16 ? (float)a.O64[t * 16 + zsel] : 0.f;
+    }
+    const int offa = -st_dr(k) * TPc - st_dc(k), off1 = -st_dr(k1) * TPc - st_dc(k1), off2 = -st_dr(k2) * TPc - st_dc(k2);
+    const float c_int = stay ? 0.f : a.p_int, c_lat = stay ? 0.f : a.p_lat;
     // a thread owns one 4-cell column group and every RPP-th row of the CTA (W / 4 divides 256,
-    // checked on the host), so all addresses advance by constants; bbar and the signatures of its
-    // <= kBuGroups groups stay in registers from the normaliser pass to the write pass
-    const int RPP = 256 / W4, c0 = 4 * (threadIdx.x % W4), rl0 = threadIdx.x / W4;
-    const int nrows = r1 - r0;
-    const uint32_t mka = 1u << bita, mk1 = 1u << bit1, mk2 = 1u << bit2;   // the taps' blocked bits
-    const unsigned int *cellp = reinterpret_cast<const unsigned int *>(a.cell + (r0 + rl0) * W + c0);
-    const unsigned int *m8p = reinterpret_cast<const unsigned int *>(a.m8 + (r0 + rl0) * W + c0);
+    // checked on the host), so all addresses advance by constants
+    const int RPP = kBuThreads / W4, c0 = 4 * (t % W4), rl0 = t / W4;
+    const unsigned int *cellp = reinterpret_cast<const unsigned int *>(a.cell + (long long)(r0 + rl0) * W + c0);
+    const unsigned int *m8p = reinterpret_cast<const unsigned int *>(a.m8 + (long long)(r0 + rl0) * W + c0);
+    uint32_t info4[G], m84[G];
+#pragma unroll
+    for (int gg = 0; gg < G; ++gg) {
+        info4[gg] = 0u;
+        m84[gg] = 0u;
+        if (rl0 + RPP * gg < nrows) {
+            info4[gg] = __ldg(cellp + gg * (RPP * W4));
+            m84[gg] = __ldg(m8p + gg * (RPP * W4));
+        }
+    }
+    __syncthreads();                             // tables and zeros visible
+    asm volatile(
+        "{\n .reg .pred P1;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
+        " @!P1 bra WAIT_%=;\n}\n" ::"r"(bar) : "memory");
     const float *rowp = stile + (rl0 + 1) * TPc + 4 + c0;
-    const int cstep = RPP * W / 4, rstep = RPP * TPc;
-    float bb[kBuGroups][4];
-    uint32_t sg4[kBuGroups];
+    float ob[G][4];                              // O[sig][z] bbar of the thread's cells
     float accf = 0.f;
 #pragma unroll
-    for (int g = 0; g < kBuGroups; ++g) {
-        sg4[g] = 0u;
+    for (int gg = 0; gg < G; ++gg) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) bb[g][i] = 0.f;
-        if (rl0 + RPP * g < nrows) {
-            const uint32_t info4 = __ldg(cellp), m84 = __ldg(m8p);
+        for (int i = 0; i < 4; ++i) ob[gg][i] = 0.f;
+        if (rl0 + RPP * gg < nrows) {
             const float4 b4 = *reinterpret_cast<const float4 *>(rowp);
             const float b0v[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                const float b0 = b0v[i];
-                float v = b0;
-                if (!stay) {   // k_correct's arithmetic (correct_predict): same fp32 operations
-                    const uint32_t m8 = m84 >> (8 * i);
-                    const float sa = rowp[offa + i], s1 = rowp[off1 + i], s2 = rowp[off2 + i];
-                    const float ha = (m8 & mka) ? sa + b0 : sa;
-                    const float h1 = (m8 & mk1) ? s1 + b0 : s1;
-                    const float h2 = (m8 & mk2) ? s2 + b0 : s2;
-                    v = fmaf(a.p_lat, h1 + h2, fmaf(a.p_int, ha, a.p_stay * b0));
-                }
-                bb[g][i] = ((info4 >> (8 * i)) & 16u) ? 0.f : v;          // occupied: no mass
+                const float sa = rowp[offa + i], s1 = rowp[off1 + i], s2 = rowp[off2 + i];
+                const float cs = s_c[(m84[gg] >> (8 * i)) & 255u];
+                const float v = fmaf(c_lat, s1 + s2, fmaf(c_int, sa, cs * b0v[i]));
+                ob[gg][i] = s_t[(info4[gg] >> (8 * i)) & 31u] * v;        // occupied: 0
+                accf += ob[gg][i];
             }
-            sg4[g] = info4 & 0x0F0F0F0Fu;                                  // the 4 signatures
-#pragma unroll
-            for (int i = 0; i < 4; ++i) accf = fmaf(s_o[(sg4[g] >> (8 * i)) & 15u], bb[g][i], accf);
         }
-        cellp += cstep;
-        m8p += cstep;
-        rowp += rstep;
+        rowp += RPP * TPc;
     }
     // fixed-order reduction: fp64 butterfly within each warp, then the 8 warp sums in order
     double acc = (double)accf;
@@ -2138,30 +2192,36 @@ __global__ void __launch_bounds__(256, 3) k_bu_cluster(CorrectArgs a, double *__
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) wsum[warp] = acc;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        double sm = 0.0;
+    // push this rank's part into slot [rank] of every CTA of the cluster (thread rr -> rank rr) and
+    // arrive on that CTA's barrier (release: the store is visible with the arrival); then wait for
+    // the NC parts here and sum them in rank order -- the same bits on every CTA.  A CTA leaves only
+    // after all NC arrivals on its own barrier, so no rank writes into an exited CTA.
+    asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
+    if (t < NC) {
+        double part = 0.0;
 #pragma unroll
-        for (int w2 = 0; w2 < 8; ++w2) sm += wsum[w2];
-        s_part = sm;
+        for (int w2 = 0; w2 < 8; ++w2) part += wsum[w2];
+        uint32_t rp, rb;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rp) : "r"((uint32_t)__cvta_generic_to_shared(&s_parts[rank])), "r"(t));
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rb) : "r"(rbar), "r"(t));
+        asm volatile("st.shared::cluster.f64 [%0], %1;\n" ::"r"(rp), "d"(part) : "memory");
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(rb) : "memory");
     }
-    cl.sync();                                   // every rank's part is in its shared memory
-    if (threadIdx.x < 16) {
-        double P = 0.0;
-        for (int rr = 0; rr < NC; ++rr) P += *cl.map_shared_rank(&s_part, rr);   // rank order
-        // a zero-likelihood z writes zeros (the host reports QVTS_ERR_ZERO_LIKELIHOOD)
-        s_w[threadIdx.x] = P > 1e-30 ? (float)(a.O64[threadIdx.x * 16 + zsel] / P) : 0.f;
-        if (threadIdx.x == 0 && rank == 0) pout[grp] = P;
-    }
-    cl.sync();                                   // no CTA leaves while another reads its part
-    float *outp = a.child + (long long)a.sel_out[grp] * a.cstride + (r0 + rl0) * W + c0;
+    asm volatile(
+        "{\n .reg .pred P1;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], 0;\n"
+        " @!P1 bra WAIT_%=;\n}\n" ::"r"(rbar) : "memory");
+    double P = 0.0;
+    for (int rr = 0; rr < NC; ++rr) P += s_parts[rr];
+    // a zero-likelihood z writes zeros (the host reports QVTS_ERR_ZERO_LIKELIHOOD)
+    const float inv = P > 1e-30 ? (float)(1.0 / P) : 0.f;
+    if (t == 0 && rank == 0) a.pout[g] = P;
+    float *outp = a.out + (long long)a.sel_out[g] * a.ostride + (long long)(r0 + rl0) * W + c0;
 #pragma unroll
-    for (int g = 0; g < kBuGroups; ++g) {
-        if (rl0 + RPP * g < nrows) {
-            float o[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) o[i] = s_w[(sg4[g] >> (8 * i)) & 15u] * bb[g][i];
-            __stcs(reinterpret_cast<float4 *>(outp), make_float4(o[0], o[1], o[2], o[3]));
-        }
+    for (int gg = 0; gg < G; ++gg) {
+        if (rl0 + RPP * gg < nrows)
+            __stcs(reinterpret_cast<float4 *>(outp),
+                   make_float4(ob[gg][0] * inv, ob[gg][1] * inv, ob[gg][2] * inv, ob[gg][3] * inv));
         outp += RPP * W;
     }
 }
@@ -2188,7 +2248,11 @@ extern "C" qvts_status qvts_belief_update_batch(qvts_model *m, const float *b_de
     QVTS_CUDA(cudaSetDevice(m->device));
     cudaStream_t st = (cudaStream_t)stream;
     const int NA = m->NA;
-    std::vector<int32_t> sel(3 * (size_t)n);
+    // the selection (Q-node, z, output slot) of every pair through page-locked staging: a true
+    // async upload, and P's readback below the same way
+    QVTS_TRY(m->bu_host.ensure(sizeof(int32_t) * 3 * (size_t)n + sizeof(double) * (size_t)n + 16));
+    int32_t *sel = m->bu_host.as<int32_t>();
+    double *p_host = reinterpret_cast<double *>(m->bu_host.as<char>() + ((sizeof(int32_t) * 3 * (size_t)n + 15) & ~(size_t)15));
     for (int g = 0; g < n; ++g) {
         int j = -1;
         for (int i = 0; i < NA; ++i) if (m->action_id[i] == actions[g]) j = i;
@@ -2197,12 +2261,62 @@ extern "C" qvts_status qvts_belief_update_batch(qvts_model *m, const float *b_de
         sel[n + g] = zs[g];
         sel[2 * n + g] = g;
     }
-    QVTS_TRY(m->bu_key.ensure(sizeof(uint32_t) * 2 * (size_t)n));
     QVTS_TRY(m->bu_off.ensure(sizeof(int32_t) * 3 * (size_t)n));
     QVTS_TRY(m->bu_P.ensure(sizeof(double) * (size_t)n));
-    QVTS_CUDA(cudaMemsetAsync(m->bu_key.p, 0, sizeof(uint32_t) * 2 * (size_t)n, st));
-    QVTS_CUDA(cudaMemcpyAsync(m->bu_off.p, sel.data(), sizeof(int32_t) * sel.size(), cudaMemcpyHostToDevice, st));
+    QVTS_CUDA(cudaMemcpyAsync(m->bu_off.p, sel, sizeof(int32_t) * 3 * (size_t)n, cudaMemcpyHostToDevice, st));
     const int32_t *d_sel = m->bu_off.as<int32_t>();
+    auto finish = [&]() -> qvts_status {
+        QVTS_CUDA(cudaMemcpyAsync(p_host, m->bu_P.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+        QVTS_CUDA(cudaStreamSynchronize(st));
+        bool zero = false;
+        for (int g = 0; g < n; ++g) {
+            if (p_obs_out) p_obs_out[g] = p_host[g];
+            if (!(p_host[g] > 1e-30)) zero = true;
+        }
+        if (zero) { set_error("zero-likelihood observation in the batch"); return QVTS_ERR_ZERO_LIKELIHOOD; }
+        return QVTS_OK;
+    };
+    // one pass per belief on a thread-block cluster when the rows fit: 16-byte rows, W / 4 dividing
+    // 256 (the column-group mapping), a cluster of NC <= 8 CTAs whose rows take <= kBuGroups
+    // groups of 4 cells per thread; otherwise the two-pass path (normaliser, then k_correct)
+    {
+        const bool vec = (m->W & 3) == 0 && (b_stride & 3) == 0 && (out_stride & 3) == 0 &&
+                         (reinterpret_cast<uintptr_t>(b_dev) & 15) == 0 && (reinterpret_cast<uintptr_t>(out_dev) & 15) == 0;
+        const int W4 = m->W / 4, tp = m->W + 8;
+        const bool groups_ok = W4 >= 1 && 256 % W4 == 0;
+        int NC = 0, rows = 0;
+        for (int nc = 1; nc <= 8 && groups_ok && !NC; ++nc) {
+            const int r = (m->H + nc - 1) / nc;
+            if ((long long)r * W4 <= (long long)kBuGroups * kBuThreads) { NC = nc; rows = r; }
+        }
+        const char *ev_bu = std::getenv("QVTS_BU_CLUSTER");          // read per call (0: two-pass path)
+        if (vec && NC > 0 && (!ev_bu || std::atoi(ev_bu) != 0) && (long long)n * NC <= 0x7FFFFFFFLL) {
+            BuArgs ba;
+            ba.beliefs = b_dev; ba.bstride = b_stride; ba.m8 = m->d_m8.as<uint8_t>(); ba.cell = m->d_cell.as<uint8_t>();
+            ba.O64 = m->d_O64.as<double>(); ba.sel_q = d_sel; ba.sel_z = d_sel + n; ba.sel_out = d_sel + 2 * n;
+            ba.out = out_dev; ba.ostride = out_stride; ba.pout = m->bu_P.as<double>();
+            ba.n = n; ba.NA = NA; ba.H = m->H; ba.W = m->W; ba.rows = rows; ba.TPc = tp;
+            ba.p_int = (float)m->p_int; ba.p_stay = (float)m->p_stay; ba.p_lat = (float)m->p_lat;
+            for (int j = 0; j < 9; ++j) ba.acts.act[j] = j < NA ? m->action_id[j] : 4;
+            const size_t smem = sizeof(float) * (size_t)(rows + 2) * tp;
+            QVTS_CUDA(cudaFuncSetAttribute(k_bu_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            cudaLaunchConfig_t lc = {};
+            lc.gridDim = dim3((unsigned)(n * NC));
+            lc.blockDim = dim3(kBuThreads);
+            lc.dynamicSmemBytes = smem;
+            lc.stream = st;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = NC;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            lc.attrs = attr;
+            lc.numAttrs = 1;
+            QVTS_CUDA(cudaLaunchKernelEx(&lc, k_bu_cluster, ba));
+            QVTS_CUDA(cudaGetLastError());
+            return finish();
+        }
+    }
     CorrectArgs c;
     std::memset(&c, 0, sizeof(c));
     c.beliefs = b_dev; c.bstride = b_stride; c.m8 = m->d_m8.as<uint8_t>(); c.cell = m->d_cell.as<uint8_t>();
@@ -2220,51 +2334,6 @@ extern "C" qvts_status qvts_belief_update_batch(qvts_model *m, const float *b_de
     c.P = m->bu_R.as<double>();
     const long long nblocks = (long long)n * c.ntiles;
     if (nblocks > 0x7FFFFFFFLL) { set_error("batch too large"); return QVTS_ERR_INVALID_ARG; }
-    // one pass per belief on a thread-block cluster when the rows fit (16-byte rows, <= 8 CTAs of
-    // <= ~56 KB staged rows each); otherwise the two-pass path (normaliser, then k_correct)
-    {
-        const bool vec = (m->W & 3) == 0 && (b_stride & 3) == 0 && (out_stride & 3) == 0 &&
-                         (reinterpret_cast<uintptr_t>(b_dev) & 15) == 0 && (reinterpret_cast<uintptr_t>(out_dev) & 15) == 0;
-        const int tp = m->W + 8;
-        // rows per CTA: the staged rows fit ~56 KB and each thread holds <= kBuGroups 4-cell groups
-        const int max_rows = std::max(1, std::min((56 * 1024) / (4 * tp) - 2, kBuGroups * 256 / std::max(1, m->W / 4)));
-        const int NC = (m->H + max_rows - 1) / max_rows;
-        const char *ev_bu = std::getenv("QVTS_BU_CLUSTER");          // read per call (0: two-pass path)
-        const bool groups_ok = m->W / 4 >= 1 && 256 % (m->W / 4) == 0;   // the kernel's column-group mapping
-        if (vec && groups_ok && NC <= 8 && (!ev_bu || std::atoi(ev_bu) != 0) && (long long)n * NC <= 0x7FFFFFFFLL) {
-            CorrectArgs cc = c;
-            cc.rows_cta = (m->H + NC - 1) / NC;
-            cc.stage_tp = tp;
-            const size_t smem = sizeof(float) * (size_t)(cc.rows_cta + 2) * tp;
-            cudaLaunchConfig_t lc = {};
-            lc.gridDim = dim3((unsigned)(n * NC));
-            lc.blockDim = dim3(256);
-            lc.dynamicSmemBytes = smem;
-            lc.stream = st;
-            cudaLaunchAttribute attr[1];
-            attr[0].id = cudaLaunchAttributeClusterDimension;
-            attr[0].val.clusterDim.x = NC;
-            attr[0].val.clusterDim.y = 1;
-            attr[0].val.clusterDim.z = 1;
-            lc.attrs = attr;
-            lc.numAttrs = 1;
-            BuActs acts_id;
-            for (int j = 0; j < 9; ++j) acts_id.act[j] = j < NA ? m->action_id[j] : 4;
-            QVTS_CUDA(cudaFuncSetAttribute(k_bu_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            QVTS_CUDA(cudaLaunchKernelEx(&lc, k_bu_cluster, cc, m->bu_P.as<double>(), NA, acts_id));
-            QVTS_CUDA(cudaGetLastError());
-            std::vector<double> p(n);
-            QVTS_CUDA(cudaMemcpyAsync(p.data(), m->bu_P.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
-            QVTS_CUDA(cudaStreamSynchronize(st));
-            bool zero = false;
-            for (int g = 0; g < n; ++g) {
-                if (p_obs_out) p_obs_out[g] = p[g];
-                if (!(p[g] > 1e-30)) zero = true;
-            }
-            if (zero) { set_error("zero-likelihood observation in the batch"); return QVTS_ERR_ZERO_LIKELIHOOD; }
-            return QVTS_OK;
-        }
-    }
 #define QVTS_BUB(MASK)                                                                                          \
     {                                                                                                           \
         correct_stage(c);                                                                                       \
@@ -2277,16 +2346,7 @@ extern "C" qvts_status qvts_belief_update_batch(qvts_model *m, const float *b_de
     QVTS_DISPATCH_MASK(m->mask, QVTS_BUB);
 #undef QVTS_BUB
     QVTS_CUDA(cudaGetLastError());
-    std::vector<double> p(n);
-    QVTS_CUDA(cudaMemcpyAsync(p.data(), m->bu_P.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
-    QVTS_CUDA(cudaStreamSynchronize(st));
-    bool zero = false;
-    for (int g = 0; g < n; ++g) {
-        if (p_obs_out) p_obs_out[g] = p[g];
-        if (!(p[g] > 1e-30)) zero = true;
-    }
-    if (zero) { set_error("zero-likelihood observation in the batch"); return QVTS_ERR_ZERO_LIKELIHOOD; }
-    return QVTS_OK;
+    return finish();
 }
 
 // ---- trace accessors ----------------------------------------------------------------------------

@@ -51,6 +51,16 @@ struct DevBuf {
     template <class T> T *as() const { return static_cast<T *>(p); }
 };
 
+// Page-locked host staging (cudaHostAlloc): small per-call uploads and readbacks run as true
+// asynchronous copies instead of staged pageable ones
+struct HostBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+    qvts_status ensure(size_t bytes);
+    void release();
+    template <class T> T *as() const { return static_cast<T *>(p); }
+};
+
 // One row band of the grid processed by one hist CTA: rows [row0, row0+nrows), with a
 // class-partitioned slot list (SURVEY §7 "signature binning": every thread owns a stream of
 // cells that share one wall signature, so its bin index is fixed in registers).
@@ -125,7 +135,7 @@ struct Model {
     std::vector<uint8_t> occ, m8, sig;
     std::vector<double> R64;          // [NA][HW]
     // device tables
-    DevBuf d_m8, d_sig, d_cell /* sig | occ<<4 */, d_ctab, d_R64, d_O64, d_O32, d_gc_cell, d_gc_act, d_gc_val, d_free;
+    DevBuf d_m8, d_sig, d_cell /* sig | occ<<4 */, d_ctab, d_R64, d_O64, d_O32, d_gc_cell, d_gc_off /* [NA+1] per-action ranges */, d_gc_val, d_free;
     int ngc = 0;
     BandSet band_big, band_small;
     LeafBands leafb;
@@ -163,7 +173,8 @@ struct Model {
     size_t evnext = 0;
     long long n_free = 0;
     // belief_update scratch
-    DevBuf bu_R, bu_P, bu_cnt, bu_umask, bu_U, bu_off, bu_path, bu_root, bu_key;
+    DevBuf bu_R, bu_P, bu_cnt, bu_umask, bu_U, bu_off, bu_path, bu_root;
+    HostBuf bu_host;                            // qvts_belief_update_batch's selection upload / P readback
     // episodes
     DevBuf ep_b[2], ep_state, ep_root_step, ep_root_ep;
     // PBVI lower bound (NEXT-2, pbvi.cu)
