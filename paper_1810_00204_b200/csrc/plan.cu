@@ -148,36 +148,40 @@ __device__ __forceinline__ int ancestral_tail(const ReduceArgs &a, int x, int k,
     return 15;
 }
 
-// One CTA per parent V-node, one warp per action (Q-node).  The CTA first brings the parent's
-// record into shared memory (one bulk copy when there is one band, as at every leaf level; else
-// the band records summed in fixed band order, fp64); then each warp: per-action recombination of
-// the linear fields -> M[s], P(z|b,a) (Eq. 3 normaliser), R(b,a), n Philox draws
-// (lane j = sample j), counts; for the leaf level also the Q_MDP value of every sampled child,
-// V(z) = qbar + max_a' [sum_s O[s][z] S[s][a']] / P(z), and the Q-node's backup
-// Q = R + gamma sum_z (f_z/n) V(z) (Alg. 6 with gamma, R13).
+// One CTA per parent V-node, one half-warp per action (Q-node): |A|/2 warps, rounded up.  The CTA
+// first brings the parent's record into shared memory (one bulk copy when there is one band, as at
+// every leaf level; else the band records summed in fixed band order, fp64); then each half-warp:
+// per-action recombination of the linear fields -> M[s], P(z|b,a) (Eq. 3 normaliser), R(b,a)
+// (PAPER.md:58), n Philox draws (lane j = sample j), counts; for the leaf level also the Q_MDP value
+// of every sampled child, V(z) = qbar + max_a' [sum_s O[s][z] S[s][a']] / P(z), and the Q-node's
+// backup Q = R + gamma sum_z (f_z/n) V(z) (Alg. 6 with gamma, R13).
 //
 // Both sums over signatures, P(z) = sum_s O[s][z] M[s] and the numerators, use that O is the
 // Kronecker product of the four sensors' 2x2 matrices K = [[acc, 1-acc], [1-acc, acc]] (PAPER.md:336,
-// reading R7): lane s holds the vector, four butterfly stages x <- acc x + (1-acc) x(lane ^ 2^b)
-// leave sum_s O[s][z] x[s] on lane z (both half-warps hold it), 4 x 2 shuffles + 2 FP operations
-// per vector instead of a 16 x 16 product.
+// reading R7): lane s of the half-warp holds the vector, four butterfly stages
+// x <- acc x + (1-acc) x(lane ^ 2^b) leave sum_s O[s][z] x[s] on lane z, 4 x 2 shuffles + 2 FP
+// operations per vector instead of a 16 x 16 product.
 //
-// Shared memory (doubles): the parent's record [pstride] | E[8], sum b, pad [16] | per warp
-// [kRedWarpScratch]: P(z|b,a) [16], the ascending CDF [16], 16 draw counts (ints).
-constexpr int kRedWarpScratch = 16 + 16 + 16;
+// Shared memory (doubles): the parent's record [pstride] | E[8], sum b, 1/n, pad [16] | per action
+// [kRedActScratch]: P(z|b,a) [16], the ascending CDF [16], 16 draw counts (ints).
+constexpr int kRedActScratch = 16 + 16 + 8;
+template <uint32_t MASK>
+__host__ __device__ constexpr int reduce_threads() { return (mask_count(MASK) + 1) / 2 * 32; }
 template <uint32_t MASK, bool LEAF>
 __host__ __device__ constexpr int reduce_smem_doubles(int pstride) {
-    return pstride + 16 + mask_count(MASK) * kRedWarpScratch;
+    return pstride + 16 + mask_count(MASK) * kRedActScratch;
 }
 
-// Executed by a CTA of |A| warps for parent w; warp j handles action j.
-// rsm: reduce_smem_doubles(pstride) doubles of shared memory (16-byte aligned; pstride even).
+// Executed by a CTA of reduce_threads<MASK>() threads for parent w; half-warp h of warp v handles
+// action j = 2 v + h.  rsm: reduce_smem_doubles(pstride) doubles of shared memory (16-byte aligned;
+// pstride even).
 template <uint32_t MASK, bool LEAF, bool ANC>
 __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int nthreads) {
     constexpr int NA = mask_count(MASK);
     constexpr int CB = hist_cb<MASK, LEAF>();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int sl = lane & 15, hf = lane >> 4;  // signature / z of the lane, half-warp
+    const int sl = lane & 15, hf = lane >> 4;  // signature / z / sample of the lane, half-warp
+    const unsigned hmask = 0xFFFFu << (16 * hf);   // this half-warp's lanes
     double *sp = rsm;                          // [pstride] band-summed record
     double *sE = rsm + a.pstride;              // [8] blocked-mass totals, [8] = sum b, [9] = 1/n
     const double *pp = a.part + w * a.nb * (long long)a.pstride;
@@ -223,12 +227,14 @@ __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int
     }
     // E[d] = sum_y occ(y + d) b(y); orthogonal directions come from the class masses (signature
     // bit: the 8 classes with bit kd/2 set, ascending); thread 8: the belief mass sum_s (class
-    // mass), ascending s; threads 32 + j: action j's stencil ids and field indices, packed
+    // mass), ascending s; thread 9: 1/n; threads 32 + j: action j's stencil ids, packed
     __shared__ uint32_t s_pack[9];
-    if (threadIdx.x < 9) {
+    if (threadIdx.x < 10) {
         const int d = threadIdx.x;
         double e;
-        if (d == 8) {
+        if (d == 9) {
+            e = 1.0 / (double)a.n;
+        } else if (d == 8) {
             e = 0.0;
 #pragma unroll
             for (int s2 = 0; s2 < 16; ++s2) e += sp[s2 * CB];
@@ -251,8 +257,6 @@ __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int
         const int k1 = k == 4 ? 4 : lat1_rt(k), k2 = k == 4 ? 4 : lat2_rt(k);
         const int da = k == 4 ? 0 : nbit(k), d1 = k == 4 ? 0 : nbit(k1), d2 = k == 4 ? 0 : nbit(k2);
         s_pack[threadIdx.x - 32] = (uint32_t)(k | k1 << 4 | k2 << 8 | da << 12 | d1 << 16 | d2 << 20);
-    } else if (threadIdx.x == 64) {
-        sE[9] = 1.0 / (double)a.n;
     }
     __syncthreads();
     const long long v = a.vmap ? (long long)a.vmap[w] : w;
@@ -264,8 +268,10 @@ __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int
     const double ka = a.acc, kb = 1.0 - a.acc;  // the sensor matrix K
     int nflag = 0, leaves = 0;
     {
-    const int j = warp;                        // this warp's action (the CTA has |A| warps)
-    double *sW = sE + 16 + warp * kRedWarpScratch;
+    const int jr = 2 * warp + hf;              // this half-warp's action
+    const bool act = jr < NA;                  // (odd |A|: the last half-warp only keeps step)
+    const int j = act ? jr : NA - 1;
+    double *sW = sE + 16 + j * kRedActScratch;
     double *sP = sW;                           // [16] P(z|b,a)
     double *C = sW + 16;                       // [16] ascending CDF
     int *sCnt = reinterpret_cast<int *>(sW + 32);   // [16] draw counts per z
@@ -276,7 +282,7 @@ __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int
     // the taps' blocked bits for class sl (class_blocked as predicates: h + [blocked] x is the add or h)
     const bool ba = class_blocked(k, sl) != 0.0, b1 = class_blocked(k1, sl) != 0.0, b2 = class_blocked(k2, sl) != 0.0;
     const double *c = sp + sl * CB;            // class sl's record
-    // M[s]: bbar_a summed over signature class s (lane s and s + 16); the counts are cleared
+    // M[s]: bbar_a summed over signature class s (lane s); the counts are cleared
     double Pz;
     {
         const double c0 = c[0];
@@ -286,22 +292,22 @@ __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int
         if (b2) hm2 += c0;
         Pz = (k == 4) ? c0 : a.p_stay * c0 + a.p_int * hma + a.p_lat * (hm1 + hm2);
     }
-    if (lane < 16) sCnt[lane] = 0;
+    if (act) sCnt[sl] = 0;
     // P(z|b,a) = sum_s O[s][z] M[s]: the four sensor butterflies, lane z
 #pragma unroll
     for (int bt = 1; bt < 16; bt <<= 1) Pz = fma(ka, Pz, kb * __shfl_xor_sync(0xffffffffu, Pz, bt));
     // R(b,a) = (p_stay - 1) sum b - sum c_a b + goal terms, sum c_a b = p_stay mass + p_int E_a + p_lat (E_l1 + E_l2);
     // goal terms G(x, a) b(x): this action's <= 9 entries (model.cu groups them by action), one
-    // per lane, tree sum
+    // per lane, tree sum within the half-warp
     double gsum = 0.0;
     if (k != 4) {
         const int g0 = a.gc_off[j], ng = a.gc_off[j + 1] - g0;
-        if (lane < ng) gsum = a.gc_val[g0 + lane] * (double)bp[a.gc_cell[g0 + lane]];
-#pragma unroll
-        for (int o = 8; o > 0; o >>= 1) gsum += __shfl_xor_sync(0xffffffffu, gsum, o);
+        if (sl < ng) gsum = a.gc_val[g0 + sl] * (double)bp[a.gc_cell[g0 + sl]];
     }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) gsum += __shfl_xor_sync(0xffffffffu, gsum, o);
     double R = 0.0;
-    if (lane == 0) {
+    if (sl == 0) {
         if (k == 4) {
             R = -2.0 * mass + 2.0 * (double)bp[a.goal];
         } else {
@@ -309,10 +315,10 @@ __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int
             R = (a.p_stay - 1.0) * mass - Rp + gsum;
         }
     }
-    if (lane < 16) sP[lane] = Pz;
+    if (act) sP[sl] = Pz;
     __syncwarp();
-    // ascending-z CDF in fp64, summed sequentially (A.5)
-    if (lane == 0) {
+    // ascending-z CDF in fp64, summed sequentially (A.5), on the half-warp's first lane
+    if (sl == 0 && act) {
         const double2 *p2 = reinterpret_cast<const double2 *>(sP);
         double2 *c2 = reinterpret_cast<double2 *>(C);
         double acc = 0.0;
@@ -328,94 +334,90 @@ __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int
         }
     }
     __syncwarp();
-    // S3: n draws keyed by the tree path (Appendix A.2-A.5)
+    // S3: n draws keyed by the tree path (Appendix A.2-A.5), lane sl = sample j0 + sl
     const int level = a.level >= 0 ? a.level : path_level(vpath);   // level < 0: from the path
     const uint64_t qpath = vpath | ((uint64_t)(k + 1) << (8 * level));
-    for (int j0 = 0; j0 < a.n; j0 += 32) {
-        const int jj = j0 + lane;
-        if (jj < a.n) {
-            int z;
-            const uint4 r = philox4x32_10(make_uint4((uint32_t)jj, (uint32_t)qpath, (uint32_t)(qpath >> 32), step),
-                                          make_uint2(a.seed, ep));
-            if constexpr (ANC) {   // Alg. 4 literal: x drawn by k_ancestral_x, then x' and z
-                z = ancestral_tail(a, a.xs[q * a.n + jj], k, philox_uniform(r.z), philox_uniform(r.w));
-            } else {
-                const double u = philox_uniform(r.x);
-                const double tt = u * C[15];
-                // z = #{k : C_k <= tt} (A.5) by binary search over the non-decreasing CDF; the gap
-                // min_{k<15} |tt - C_k| is attained at the boundaries around tt, C_{z-1} and C_z
-                int lo = 0;
+    if (act) {
+        for (int j0 = 0; j0 < a.n; j0 += 16) {
+            const int jj = j0 + sl;
+            if (jj < a.n) {
+                int z;
+                const uint4 r = philox4x32_10(make_uint4((uint32_t)jj, (uint32_t)qpath, (uint32_t)(qpath >> 32), step),
+                                              make_uint2(a.seed, ep));
+                if constexpr (ANC) {   // Alg. 4 literal: x drawn by k_ancestral_x, then x' and z
+                    z = ancestral_tail(a, a.xs[q * a.n + jj], k, philox_uniform(r.z), philox_uniform(r.w));
+                } else {
+                    const double u = philox_uniform(r.x);
+                    const double tt = u * C[15];
+                    // z = #{k : C_k <= tt} (A.5) by binary search over the non-decreasing CDF; the
+                    // gap min_{k<15} |tt - C_k| is attained at the boundaries around tt, C_{z-1} and C_z
+                    int lo = 0;
 #pragma unroll
-                for (int st = 8; st > 0; st >>= 1)
-                    if (C[lo + st - 1] <= tt) lo += st;
-                z = lo + (C[lo] <= tt ? 1 : 0);          // in 0..16
-                double gap = INFINITY;
-                if (z >= 1 && z - 1 < 15) gap = tt - C[z - 1];
-                if (z < 15) gap = fmin(gap, C[z] - tt);
-                z = min(z, 15);
-                nflag += gap < 1e-6 ? 1 : 0;
+                    for (int st = 8; st > 0; st >>= 1)
+                        if (C[lo + st - 1] <= tt) lo += st;
+                    z = lo + (C[lo] <= tt ? 1 : 0);          // in 0..16
+                    double gap = INFINITY;
+                    if (z >= 1 && z - 1 < 15) gap = tt - C[z - 1];
+                    if (z < 15) gap = fmin(gap, C[z] - tt);
+                    z = min(z, 15);
+                    nflag += gap < 1e-6 ? 1 : 0;
+                }
+                if (a.zdraw) a.zdraw[q * a.n + jj] = (uint8_t)z;
+                atomicAdd(&sCnt[z], 1);            // integer counts: exact in any order
             }
-            if (a.zdraw) a.zdraw[q * a.n + jj] = (uint8_t)z;
-            atomicAdd(&sCnt[z], 1);            // integer counts: exact in any order
         }
     }
     __syncwarp();
-    const int cntk = sCnt[sl];                 // lane z and z + 16
-    const unsigned um = __ballot_sync(0xffffffffu, cntk > 0) & 0xFFFFu;
+    const int cntk = act ? sCnt[sl] : 0;       // lane z
+    const unsigned um = (__ballot_sync(0xffffffffu, cntk > 0) & hmask) >> (16 * hf);
     const int U = __popc(um);
-    leaves += U;
-    if (lane < 16) {
-        a.P[q * 16 + lane] = Pz;
-        a.cnt[q * 16 + lane] = (uint16_t)cntk;
-    }
-    if (lane == 0) {
-        a.R[q] = R;
-        a.umask[q] = (uint16_t)um;
-        a.U[q] = U;
+    if (act) {
+        leaves += sl == 0 ? U : 0;
+        a.P[q * 16 + sl] = Pz;
+        a.cnt[q * 16 + sl] = (uint16_t)cntk;
+        if (sl == 0) {
+            a.R[q] = R;
+            a.umask[q] = (uint16_t)um;
+            a.U[q] = U;
+        }
     }
     if (LEAF) {
-        // S[s][a'] of this action from the linear fields, lane -> (s, this half's a'), then the same
-        // butterflies: lane z holds the numerators sum_s O[s][z] S[s][a'] of its half's a'
-        constexpr int NH = (NA + 1) / 2;
-        const double c0 = c[0];
-        double Sv[NH];
+        // S[s][a'] of this action from the linear fields (lane s, every a'), then the same
+        // butterflies: lane z holds the numerators sum_s O[s][z] S[s][a']
+        double Sv[NA];
 #pragma unroll
-        for (int t2 = 0; t2 < NH; ++t2) {
-            const int j2 = hf * NH + t2;
-            Sv[t2] = 0.0;
-            if (NA % 2 == 0 || j2 < NA) {
-                const double zb = c[9 + j2];
-                double ha = c[9 + NA + da * NA + j2], h1 = c[9 + NA + d1 * NA + j2], h2 = c[9 + NA + d2 * NA + j2];
-                if (ba) ha += zb;
-                if (b1) h1 += zb;
-                if (b2) h2 += zb;
-                Sv[t2] = (k == 4) ? zb : a.p_stay * zb + a.p_int * ha + a.p_lat * (h1 + h2);
-            }
+        for (int j2 = 0; j2 < NA; ++j2) {
+            const double zb = c[9 + j2];
+            double ha = c[9 + NA + da * NA + j2], h1 = c[9 + NA + d1 * NA + j2], h2 = c[9 + NA + d2 * NA + j2];
+            if (ba) ha += zb;
+            if (b1) h1 += zb;
+            if (b2) h2 += zb;
+            Sv[j2] = (k == 4) ? zb : a.p_stay * zb + a.p_int * ha + a.p_lat * (h1 + h2);
         }
-        (void)c0;
 #pragma unroll
         for (int bt = 1; bt < 16; bt <<= 1)
 #pragma unroll
-            for (int t2 = 0; t2 < NH; ++t2) Sv[t2] = fma(ka, Sv[t2], kb * __shfl_xor_sync(0xffffffffu, Sv[t2], bt));
-        double best = -INFINITY;
+            for (int j2 = 0; j2 < NA; ++j2) Sv[j2] = fma(ka, Sv[j2], kb * __shfl_xor_sync(0xffffffffu, Sv[j2], bt));
+        double best = Sv[0];
 #pragma unroll
-        for (int t2 = 0; t2 < NH; ++t2)
-            if (NA % 2 == 0 || hf * NH + t2 < NA) best = fmax(best, Sv[t2]);
-        best = fmax(best, __shfl_xor_sync(0xffffffffu, best, 16));
-        // lane z < 16, z sampled: V(z) = qbar + max_a' num / P(z); the backup sums f_z V(z)
+        for (int j2 = 1; j2 < NA; ++j2) best = fmax(best, Sv[j2]);
+        // lane z, z sampled: V(z) = qbar + max_a' num / P(z); the backup sums f_z V(z)
         double fv = 0.0;
-        if (lane < 16 && cntk > 0) {
+        if (cntk > 0) {
             const double Vz = a.qbar + best / Pz;
-            if (a.leafV) a.leafV[q * 16 + lane] = Vz;
+            if (a.leafV) a.leafV[q * 16 + sl] = Vz;
             fv = (double)cntk * Vz;
         }
 #pragma unroll
         for (int o = 8; o > 0; o >>= 1) fv += __shfl_xor_sync(0xffffffffu, fv, o);
-        if (lane == 0) a.Q[q] = R + a.gamma * (fv * sE[9]);     // sE[9] = 1/n
+        if (sl == 0 && act) a.Q[q] = R + a.gamma * (fv * sE[9]);     // sE[9] = 1/n
     }
-    }   // this warp's action
+    }   // this half-warp's action
     // flagged-draw and leaf counts: per warp, one global atomic each (counts are integers)
-    for (int o = 16; o > 0; o >>= 1) nflag += __shfl_xor_sync(0xffffffffu, nflag, o);
+    for (int o = 16; o > 0; o >>= 1) {
+        nflag += __shfl_xor_sync(0xffffffffu, nflag, o);
+        leaves += __shfl_xor_sync(0xffffffffu, leaves, o);
+    }
     if (lane == 0 && a.counters) {
         if (nflag) atomicAdd(&a.counters[0], (unsigned long long)nflag);
         if (LEAF && leaves) atomicAdd(&a.counters[1], (unsigned long long)leaves);
@@ -423,21 +425,21 @@ __device__ void reduce_parent(const ReduceArgs &a, long long w, double *rsm, int
     __syncthreads();   // rsm may be reused by the caller
 }
 
-// k_reduce is latency-bound on its band-partial loads: ~1536 resident threads per SM beat the
-// registers that cost (measured at A8: 6 blocks of 256 -> leaf launch 7.4 -> 4.5 ms)
+// k_reduce: ~1536 resident threads per SM (measured at A8 in round 1: 6 blocks of 256 -> leaf
+// launch 7.4 -> 4.5 ms); one half-warp per action
 template <uint32_t MASK>
 __host__ __device__ constexpr int reduce_min_blocks() {
-    return 1536 / (mask_count(MASK) * 32) > 8 ? 8 : 1536 / (mask_count(MASK) * 32);
+    return 1536 / reduce_threads<MASK>() > 16 ? 16 : 1536 / reduce_threads<MASK>();
 }
 
 // ANC: the ancestral sampler's x' and z tail (a.xs set), compiled apart so the marginal sampler's
 // kernel carries none of its registers
 template <uint32_t MASK, bool LEAF, bool ANC>
-__global__ void __launch_bounds__(mask_count(MASK) * 32, reduce_min_blocks<MASK>()) k_reduce(ReduceArgs a) {
+__global__ void __launch_bounds__(reduce_threads<MASK>(), reduce_min_blocks<MASK>()) k_reduce(ReduceArgs a) {
     extern __shared__ double rsm[];
     if (a.skip && *a.skip) return;
     if (a.nwork_dev && (long long)blockIdx.x >= *a.nwork_dev) return;
-    reduce_parent<MASK, LEAF, ANC>(a, blockIdx.x, rsm, mask_count(MASK) * 32);
+    reduce_parent<MASK, LEAF, ANC>(a, blockIdx.x, rsm, reduce_threads<MASK>());
 }
 
 // ---- NEXT-3: the state draw x ~ b of Alg. 4 for every sample of every Q-node of a parent ------
@@ -1160,7 +1162,7 @@ static qvts_status launch_reduce(Model &m, const ReduceArgs &r, cudaStream_t st)
     QVTS_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (r.nwork > 0x7FFFFFFFLL) { set_error("too many parents"); return QVTS_ERR_INVALID_ARG; }
     if (r.pstride & 1) { set_error("record stride must be even (16-byte bulk copies)"); return QVTS_ERR_INVALID_ARG; }
-    QVTS_PROF(LEAF ? 2 : 3, kfn<<<(unsigned)r.nwork, NA * 32, smem, st>>>(r));
+    QVTS_PROF(LEAF ? 2 : 3, kfn<<<(unsigned)r.nwork, reduce_threads<MASK>(), smem, st>>>(r));
     QVTS_CUDA(cudaGetLastError());
     return QVTS_OK;
 }
@@ -2284,6 +2286,8 @@ extern "C" qvts_status qvts_belief_update_batch(qvts_model *m, const float *b_de
                          (reinterpret_cast<uintptr_t>(b_dev) & 15) == 0 && (reinterpret_cast<uintptr_t>(out_dev) & 15) == 0;
         const int W4 = m->W / 4, tp = m->W + 8;
         const bool groups_ok = W4 >= 1 && 256 % W4 == 0;
+        // the smallest cluster (<= 8 CTAs, portable) whose rows fit kBuGroups groups per thread;
+        // 16-CTA clusters of 16 rows (non-portable, 6 CTAs per SM) measured slower: 0.50 vs 0.42 ms
         int NC = 0, rows = 0;
         for (int nc = 1; nc <= 8 && groups_ok && !NC; ++nc) {
             const int r = (m->H + nc - 1) / nc;
@@ -2299,7 +2303,8 @@ extern "C" qvts_status qvts_belief_update_batch(qvts_model *m, const float *b_de
             ba.p_int = (float)m->p_int; ba.p_stay = (float)m->p_stay; ba.p_lat = (float)m->p_lat;
             for (int j = 0; j < 9; ++j) ba.acts.act[j] = j < NA ? m->action_id[j] : 4;
             const size_t smem = sizeof(float) * (size_t)(rows + 2) * tp;
-            QVTS_CUDA(cudaFuncSetAttribute(k_bu_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            auto kfn = k_bu_cluster;
+            QVTS_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             cudaLaunchConfig_t lc = {};
             lc.gridDim = dim3((unsigned)(n * NC));
             lc.blockDim = dim3(kBuThreads);
@@ -2312,7 +2317,7 @@ extern "C" qvts_status qvts_belief_update_batch(qvts_model *m, const float *b_de
             attr[0].val.clusterDim.z = 1;
             lc.attrs = attr;
             lc.numAttrs = 1;
-            QVTS_CUDA(cudaLaunchKernelEx(&lc, k_bu_cluster, ba));
+            QVTS_CUDA(cudaLaunchKernelEx(&lc, kfn, ba));
             QVTS_CUDA(cudaGetLastError());
             return finish();
         }
