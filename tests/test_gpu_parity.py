@@ -534,6 +534,37 @@ def test_plan_localised_root_skips_tiles(Q):
     assert res2.n_tiles_skipped > 0
 
 
+@pytest.mark.parametrize("H,Wd", [(200, 256), (37, 64), (256, 16), (64, 1024)])
+def test_belief_update_batch_cluster_shapes(Q, H, Wd):
+    """The one-pass cluster kernel on the map shapes that change its geometry: 7 CTAs with a short
+    last one (200 x 256), one CTA owning every row so both halo rows are off the map (37 x 64),
+    64 rows per pass of a 16-wide map (256 x 16), one row per pass and 8 CTAs of 8 rows
+    (64 x 1024); A9 (stay included), mixed actions and observations, against the oracle (Eq. 3,
+    PAPER.md:59-63) element by element."""
+    gm = W.random_map(H, Wd, 0.2, seed=H + Wd)
+    g = Q.Model(gm, action_mask=W.A9)
+    o = O.Model.grid(gm, action_mask=W.A9)
+    rng = np.random.default_rng(H)
+    nb = 11
+    B = np.stack([W.random_belief(gm, 300 + i, sparsity=0.3 if i % 2 else 0.0) for i in range(nb)]).astype(np.float32)
+    acts = np.array([g.action_ids[i % g.n_actions] for i in range(nb)], np.int32)
+    rng.shuffle(acts)
+    zs = np.zeros(nb, np.int32)
+    for i in range(nb):
+        P = o.marginal(o.predict(B[i].astype(np.float64), g.action_ids.index(acts[i])))
+        zs[i] = int(np.argsort(P)[-1 - (i % 4)])
+    out = torch.empty((nb, gm.occupancy.size), dtype=torch.float32, device="cuda")
+    p = g.belief_update_batch(dev(B), acts, zs, out)
+    res = out.cpu().numpy()
+    for i in range(nb):
+        ob, op = o.belief_update(B[i].astype(np.float64), g.action_ids.index(acts[i]), int(zs[i]))
+        assert abs(p[i] - op) <= 1e-7, (i, p[i], op)
+        assert np.max(np.abs(res[i] - ob)) <= PT.TOL
+        assert np.max(np.abs(res[i] - ob)) <= 1e-5 * max(1e-3, float(np.max(ob)))
+        assert np.all(res[i][gm.occupancy == 1] == 0.0)
+    g.close()
+
+
 @pytest.mark.parametrize("cluster", ["1", "0"])
 def test_belief_update_batch_C3_paths_and_alignment(Q, cluster, monkeypatch):
     """Batched Eq. 3 on a map with 16-byte rows (C3, 128x128): the one-pass cluster kernel
