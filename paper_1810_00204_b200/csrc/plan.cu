@@ -682,9 +682,11 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_hist(HistArgs a) {
                                  "l"(ok ? src + c : src), "r"(ok ? 4 : 0));
             }
         }
-        for (int tr = t; tr < TH; tr += kPairThreads) {      // halo columns
-            tile[tr * TP + 3] = 0.f;
-            tile[tr * TP + 4 + a.W] = 0.f;
+        // halo columns, and the row padding the copies never write: the skip scan below reads
+        // whole rows, so stale shared memory there would decide skips at random
+        for (int i = t; i < TH * (TP - a.W); i += kPairThreads) {
+            const int tr = i / (TP - a.W), j = i - tr * (TP - a.W);
+            tile[tr * TP + (j < 4 ? j : a.W + j)] = 0.f;
         }
         for (int i = t; i < 3 * TP; i += kPairThreads) tile[TH * TP + i] = 0.f;   // zero rows: pad cell
     }
