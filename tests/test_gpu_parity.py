@@ -532,6 +532,15 @@ def test_plan_localised_root_skips_tiles(Q):
         b[row[len(row) // 2]] = 0.5
     res2, _, _ = run_parity(Q, gm, W.A8, 3, 8, b, seed=4)
     assert res2.n_tiles_skipped > 0
+    # the skip decisions are a function of the beliefs alone: the graph-captured step (no trace)
+    # skips the same tiles and returns the same root values bit for bit
+    g = Q.Model(gm, action_mask=W.A8)
+    g.value_iteration(1e-9)
+    rt = g.plan_step(dev(b), 3, 8, seed=4, want_trace=True)
+    rg = g.plan_step(dev(b), 3, 8, seed=4)
+    assert rt.n_tiles_skipped == rg.n_tiles_skipped == res2.n_tiles_skipped
+    assert list(rt.q_root[:g.n_actions]) == list(rg.q_root[:g.n_actions])
+    g.close()
 
 
 @pytest.mark.parametrize("H,Wd", [(200, 256), (37, 64), (256, 16), (64, 1024)])
