@@ -446,6 +446,13 @@ __global__ void __launch_bounds__(reduce_threads<MASK>(), reduce_min_blocks<MASK
 // One CTA per parent: fp64 sums of 256-cell chunks (warp per chunk, fixed order), their exclusive
 // prefix, then per (action, sample) target t = u1 * C_total: the chunk by binary search and the
 // cell by a sequential fp64 scan inside it, min{x : t < C_x} (A.5; zero-mass cells never drawn).
+// chunk of the two-level prefix: a multiple of 32 cells, at most 2048 chunks (32 KB of shared
+// prefix for any map)
+__host__ __device__ constexpr int ancestral_chunk(int HW) {
+    return ((HW + 2047) / 2048 + 31) / 32 * 32 < 32 ? 32 : ((HW + 2047) / 2048 + 31) / 32 * 32;
+}
+__host__ __device__ constexpr int ancestral_nch(int HW) { return (HW + ancestral_chunk(HW) - 1) / ancestral_chunk(HW); }
+
 template <uint32_t MASK>
 __global__ void __launch_bounds__(256) k_ancestral_x(const float *__restrict__ beliefs, long long bstride,
                                                      const int32_t *vmap, long long nwork, int HW,
@@ -455,30 +462,86 @@ __global__ void __launch_bounds__(256) k_ancestral_x(const float *__restrict__ b
                                                      const int32_t *skip = nullptr,
                                                      const long long *nwork_dev = nullptr) {
     constexpr int NA = mask_count(MASK);
-    constexpr int CH = 256;
-    extern __shared__ double sx[];   // [nch] chunk sums, then exclusive prefix in place
+    extern __shared__ double sx[];   // [nch] chunk sums, [nch + 1] exclusive prefix
+    __shared__ double s_wtot[8];
     if (skip && *skip) return;
     if (nwork_dev && (long long)blockIdx.x >= *nwork_dev) return;   // graph path: worst-case grid
     const long long w = blockIdx.x;
     const long long v = vmap ? (long long)vmap[w] : w;
     const float *__restrict__ b = beliefs + v * bstride;
-    const int nch = (HW + CH - 1) / CH;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int CH = ancestral_chunk(HW), nch = ancestral_nch(HW);
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     double *csum = sx, *cpre = sx + nch;
-    for (int c = warp; c < nch; c += 8) {
-        double s = 0.0;
-        for (int i = lane; i < CH; i += 32) {
-            const int x = c * CH + i;
-            if (x < HW) s += (double)b[x];
+    // fp64 chunk sums: a warp reads 128 consecutive cells per pass (4 per lane), each lane sums
+    // its 4 in order, 8-lane butterflies give the 32-cell sums, and a chunk of CH cells adds its
+    // CH / 32 pieces in order (lane 0 of each 8-lane group)
+    const bool v4 = ((HW & 3) == 0) && ((reinterpret_cast<uintptr_t>(b) & 15) == 0);
+    if (CH == 32) {   // four chunks per 128-cell pass (maps up to 64K cells), 4 passes in flight
+        const int nblk = (nch + 3) / 4;
+        for (int blk0 = warp; blk0 < nblk; blk0 += 32) {
+            float4 f[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int x = 128 * (blk0 + 8 * u) + 4 * lane;
+                f[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (blk0 + 8 * u < nblk) {
+                    if (v4 && x + 3 < HW) {
+                        f[u] = __ldg(reinterpret_cast<const float4 *>(b + x));
+                    } else {
+                        if (x < HW) f[u].x = __ldg(b + x);
+                        if (x + 1 < HW) f[u].y = __ldg(b + x + 1);
+                        if (x + 2 < HW) f[u].z = __ldg(b + x + 2);
+                        if (x + 3 < HW) f[u].w = __ldg(b + x + 3);
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int blk = blk0 + 8 * u;
+                double q = (((double)f[u].x + (double)f[u].y) + (double)f[u].z) + (double)f[u].w;
+#pragma unroll
+                for (int o = 1; o < 8; o <<= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+                if (blk < nblk && (lane & 7) == 0 && 4 * blk + (lane >> 3) < nch) csum[4 * blk + (lane >> 3)] = q;
+            }
         }
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    } else for (int c = warp; c < nch; c += 8) {
+        double s = 0.0;
+        for (int p0 = c * CH; p0 < min(HW, (c + 1) * CH); p0 += 128) {
+            const int x = p0 + 4 * lane;
+            double q = 0.0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if (x + i < HW && x + i < (c + 1) * CH) q += (double)__ldg(b + x + i);
+#pragma unroll
+            for (int o = 1; o < 8; o <<= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+            // pieces of this pass: lanes 0, 8, 16, 24 hold the 32-cell sums, in cell order
+#pragma unroll
+            for (int g = 0; g < 4; ++g) s += __shfl_sync(0xffffffffu, q, 8 * g);
+        }
         if (lane == 0) csum[c] = s;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        double acc = 0.0;
-        for (int c = 0; c < nch; ++c) { cpre[c] = acc; acc += csum[c]; }
-        cpre[nch] = acc;
+    // exclusive prefix over the chunks in a fixed order: each thread a run of consecutive chunks,
+    // the run totals scanned across the CTA (warp shuffles, then the 8 warp totals in order)
+    const int per = (nch + 255) / 256, c0 = t * per, c1 = min(nch, c0 + per);
+    double run = 0.0;
+    for (int c = c0; c < c1; ++c) run += csum[c];
+    double inc = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_wtot[warp] = inc;
+    __syncthreads();
+    double base = 0.0;
+    for (int w2 = 0; w2 < warp; ++w2) base += s_wtot[w2];
+    double acc0 = base + (inc - run);         // exclusive prefix of this thread's run
+    for (int c = c0; c < c1; ++c) { cpre[c] = acc0; acc0 += csum[c]; }
+    if (t == 255) {
+        double tot = 0.0;
+        for (int w2 = 0; w2 < 8; ++w2) tot += s_wtot[w2];
+        cpre[nch] = tot;
     }
     __syncthreads();
     const double total = cpre[nch];
@@ -486,7 +549,7 @@ __global__ void __launch_bounds__(256) k_ancestral_x(const float *__restrict__ b
     if (level < 0) level = path_level(vp);
     const int root = vroot[v];
     const uint32_t step = root_step[root], ep = root_ep[root];
-    for (int idx = threadIdx.x; idx < NA * n; idx += 256) {
+    for (int idx = t; idx < NA * n; idx += 256) {
         const int j = idx / n, s = idx % n;
         int kk = 0;
 #pragma unroll
@@ -494,23 +557,23 @@ __global__ void __launch_bounds__(256) k_ancestral_x(const float *__restrict__ b
         const uint64_t qpath = vp | ((uint64_t)(kk + 1) << (8 * level));
         const uint4 r = philox4x32_10(make_uint4((uint32_t)s, (uint32_t)qpath, (uint32_t)(qpath >> 32), step),
                                       make_uint2(seed, ep));
-        const double t = philox_uniform(r.y) * total;
-        int lo = 0, hi = nch - 1;                   // first chunk whose end exceeds t
+        const double tt = philox_uniform(r.y) * total;
+        int lo = 0, hi = nch - 1;                   // first chunk whose end exceeds tt
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
-            if (t < cpre[mid + 1]) hi = mid; else lo = mid + 1;
+            if (tt < cpre[mid + 1]) hi = mid; else lo = mid + 1;
         }
         double acc = cpre[lo];
         int xsel = -1, last = -1;
-        for (int i = 0; i < CH; ++i) {
-            const int x = lo * CH + i;
-            if (x >= HW) break;
-            const double bv = (double)b[x];
+        const int x1 = min(HW, (lo + 1) * CH);
+        for (int x = lo * CH; x < x1; ++x) {
+            const double bv = (double)__ldg(b + x);
             acc += bv;
             if (bv > 0.0) last = x;
-            if (t < acc) { xsel = x; break; }
+            if (tt < acc) { xsel = x; break; }
         }
-        if (xsel < 0) xsel = last >= 0 ? last : lo * CH;   // rounding at the very end of a chunk
+        // rounding at the very end of a chunk (the prefix and this scan sum in different orders)
+        if (xsel < 0) xsel = last >= 0 ? last : lo * CH;
         xs[((long long)w * NA + j) * n + s] = xsel;
     }
 }
@@ -1267,7 +1330,7 @@ static qvts_status plan_levels_t(Model &m, const RootBatch &roots, const qvts_pl
                 // with a trace, every level keeps its state draws (qvts_trace_state_draws)
                 DevBuf &xb = trace ? ql.xdraw : m.xs;
                 QVTS_TRY(xb.ensure(sizeof(int32_t) * (size_t)nq * n));
-                const int nch = (m.HW + 255) / 256;
+                const int nch = ancestral_nch(m.HW);
                 QVTS_PROF(7, k_ancestral_x<MASK><<<(unsigned)nwork, 256, sizeof(double) * (2 * nch + 1), st>>>(
                                  bel, bstride, vmap, nwork, m.HW, vl.path.as<uint64_t>(), vl.root.as<int32_t>(),
                                  roots.step_dev, roots.episode_dev, cfg.seed, d, n, xb.as<int32_t>()));
@@ -1436,7 +1499,7 @@ static qvts_status plan_levels_dev_t(Model &m, const float *root, const qvts_pla
         r.xs = nullptr; r.m8 = m.d_m8.as<uint8_t>(); r.sig = m.d_sig.as<uint8_t>(); r.W = m.W; r.acc = m.acc;
         r.nwork_dev = cnt + d;
         if (cfg.sampler == QVTS_SAMPLER_ANCESTRAL) {
-            const int nch = (m.HW + 255) / 256;
+            const int nch = ancestral_nch(m.HW);
             QVTS_PROF(7, k_ancestral_x<MASK><<<(unsigned)nwork, 256, sizeof(double) * (2 * nch + 1), st>>>(
                              bel, bstride, nullptr, nwork, m.HW, vl.path.as<uint64_t>(), vl.root.as<int32_t>(),
                              r.root_step, r.root_ep, cfg.seed, d, n, m.xs.as<int32_t>(), nullptr, cnt + d));
@@ -1635,7 +1698,7 @@ static qvts_status expand_marginals_t(Model &m, const ExpandSpec &e, QLevel &ql,
     r.m8 = m.d_m8.as<uint8_t>(); r.sig = m.d_sig.as<uint8_t>(); r.W = m.W; r.acc = m.acc;
     if (e.sampler == QVTS_SAMPLER_ANCESTRAL) {
         QVTS_TRY(m.xs.ensure(sizeof(int32_t) * (size_t)nq * e.n));
-        const int nch = (m.HW + 255) / 256;
+        const int nch = ancestral_nch(m.HW);
         QVTS_PROF(7, k_ancestral_x<MASK><<<(unsigned)nwork, 256, sizeof(double) * (2 * nch + 1), st>>>(
                          e.beliefs, e.bstride, nullptr, nwork, m.HW, e.vpath, e.vroot, e.root_step, e.root_ep,
                          e.seed, e.level, e.n, m.xs.as<int32_t>()));
@@ -1702,7 +1765,7 @@ static qvts_status bf_expand_launch_t(Model &m, const BfLaunch &L, QLevel &ql, c
     r.m8 = m.d_m8.as<uint8_t>(); r.sig = m.d_sig.as<uint8_t>(); r.W = m.W; r.acc = m.acc;
     r.skip = L.skip;
     if (L.sampler == QVTS_SAMPLER_ANCESTRAL) {
-        const int nch = (m.HW + 255) / 256;
+        const int nch = ancestral_nch(m.HW);
         QVTS_PROF(7, k_ancestral_x<MASK><<<1, 256, sizeof(double) * (2 * nch + 1), st>>>(
                          L.bel, L.stride, L.sel, 1, m.HW, L.path, L.root, L.root_step, L.root_ep, L.seed, -1, L.n,
                          m.xs.as<int32_t>(), L.skip));
