@@ -16,7 +16,8 @@ from paper_1810_00204_b200 import qvts as Q  # noqa: E402
 
 E = int(os.environ.get("EPISODES", "1024"))
 MS = int(os.environ.get("MAX_STEPS", "1000"))
-gm = W.CONFIGS["C5"]["map"]()
+MAP_SEED = int(os.environ.get("MAP_SEED", "5"))          # SURVEY d.1: C5 x 3 map seeds as separate runs
+gm = W.random_map(256, 256, 0.2, seed=MAP_SEED)
 m = Q.Model(gm, action_mask=W.A9)
 m.value_iteration(1e-9)
 m.run_episodes(8, max_steps=5, planner=Q.QVTS_PLANNER_QVTS, depth=3, n_samples=8, seed=99)   # warm
@@ -27,7 +28,7 @@ torch.cuda.synchronize()
 dt = time.perf_counter() - t0
 steps = int(rec["steps"].sum())
 oc = {str(k): int((rec["outcome"] == k).sum()) for k in range(4)}
-print(json.dumps({"config": "C5: random(256,256,0.2,seed=5), A9, D=3, n=8, 1024 episodes, max_steps 1000, stop_patience 3, uniform b0",
+print(json.dumps({"config": f"C5: random(256,256,0.2,seed={MAP_SEED}), A9, D=3, n=8, {E} episodes, max_steps {MS}, stop_patience 3, uniform b0",
                   "episodes": E, "wall_s": dt, "episodes_per_s": E / dt, "episode_steps": steps,
                   "episode_steps_per_s": steps / dt, "mean_steps": steps / E, "outcomes": oc,
                   "success_rate": oc["0"] / E, "mean_collisions": float(rec["collisions"].mean()),
