@@ -19,7 +19,8 @@
  *    ascending stencil id.  Observations z are 4-bit words 0..15, bit k = sensor N_{2k+1}
  *    (bit0 up, bit1 left, bit2 right, bit3 down, reading R6).
  *  - Beliefs passed in must be non-negative, zero on occupied cells and sum to 1 (± 1e-4).
- *    Kernels never read belief mass on occupied cells (such states are absorbing, R5).
+ *    Occupied cells are absorbing with no mass (R5); the kernels rely on those zeros (e.g. the
+ *    batched update multiplies them by a zero weight instead of testing the occupancy).
  */
 #ifndef QVTS_H
 #define QVTS_H
