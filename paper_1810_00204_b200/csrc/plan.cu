@@ -2320,9 +2320,11 @@ extern "C" qvts_status qvts_belief_update_batch(qvts_model *m, const float *b_de
     QVTS_TRY(m->bu_host.ensure(sizeof(int32_t) * 3 * (size_t)n + sizeof(double) * (size_t)n + 16));
     int32_t *sel = m->bu_host.as<int32_t>();
     double *p_host = reinterpret_cast<double *>(m->bu_host.as<char>() + ((sizeof(int32_t) * 3 * (size_t)n + 15) & ~(size_t)15));
+    int lut[9];                                  // stencil id -> action index (-1: not in the set)
+    for (int k = 0; k < 9; ++k) lut[k] = -1;
+    for (int i = 0; i < NA; ++i) lut[m->action_id[i]] = i;
     for (int g = 0; g < n; ++g) {
-        int j = -1;
-        for (int i = 0; i < NA; ++i) if (m->action_id[i] == actions[g]) j = i;
+        const int j = (actions[g] >= 0 && actions[g] < 9) ? lut[actions[g]] : -1;
         if (j < 0 || zs[g] < 0 || zs[g] > 15) { set_error("action not in the action set or z out of range"); return QVTS_ERR_INVALID_ARG; }
         sel[g] = g * NA + j;
         sel[n + g] = zs[g];
