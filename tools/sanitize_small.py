@@ -2,9 +2,10 @@
 (memcheck / racecheck / synccheck / initcheck; SURVEY §4 layer 5).  Run as
     compute-sanitizer --tool <tool> python tools/sanitize_small.py [quick]
 Covers: VI, FIB, PBVI, belief_update (single, batch), plan_step (Q_MDP and FIB leaves, marginal
-and ancestral samplers, graph-captured and level-synchronous, fused leaf level, the opt-in
-tensor-core leaf kernel, k_correct staged and unstaged), best-first planning with tree reuse and
-the three episode planners."""
+and ancestral samplers, graph-captured and level-synchronous, the k_hist leaf path, k_leaf's
+cp.async staging fallback and band split, the opt-in tensor-core leaf kernel, k_correct staged
+and unstaged), belief_update_batch on both paths, best-first planning with tree reuse and the
+three episode planners."""
 import os
 import sys
 
@@ -29,11 +30,15 @@ for gm, mask in maps:
     bb = torch.stack([b, out])
     ob = torch.empty_like(bb)
     m.belief_update_batch(bb, [m.action_ids[1], m.action_ids[0]], [2, 5], ob)
+    os.environ["QVTS_BU_CLUSTER"] = "0"                     # the two-pass path too
+    m.belief_update_batch(bb, [m.action_ids[1], m.action_ids[0]], [2, 5], ob)
+    os.environ.pop("QVTS_BU_CLUSTER")
     for leaf in (0, 1):
         for sampler in ((0, 1) if not quick else (0,)):
             m.plan_step(b, 2, 8, seed=1, want_trace=True, leaf_bound=leaf, sampler=sampler)
             m.trace(with_draws=True, n_samples=8, beliefs=True)
-    for env in ({}, {"QVTS_PLAN_GRAPH": "0"}, {"QVTS_FUSED_LEAF": "1", "QVTS_PLAN_GRAPH": "0"},
+    for env in ({}, {"QVTS_PLAN_GRAPH": "0"}, {"QVTS_LEAF_KERNEL": "0", "QVTS_PLAN_GRAPH": "0"},
+                {"QVTS_LEAF_TMA": "0", "QVTS_PLAN_GRAPH": "0"}, {"QVTS_LEAF_NSPLIT": "4", "QVTS_PLAN_GRAPH": "0"},
                 {"QVTS_LEAF_MMA": "1", "QVTS_PLAN_GRAPH": "0"}, {"QVTS_LEAF_MMA": "1"},
                 {"QVTS_CORRECT_STAGE": "0", "QVTS_PLAN_GRAPH": "0"}):
         old = {k: os.environ.get(k) for k in env}
