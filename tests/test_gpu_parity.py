@@ -667,3 +667,19 @@ def test_leaf_mma_matches_scalar_leaf_and_oracle(Q, name, depth, n, monkeypatch)
     # the tensor-core leaf tree against the oracle element by element (1e-5, flagged-draw replay)
     monkeypatch.setenv("QVTS_LEAF_MMA", "1")
     run_parity(Q, gm, mask, depth, n, b32, seed=4, step=1, beliefs=False)
+
+
+@pytest.mark.parametrize("env", [{"QVTS_LEAF_KERNEL": "0"}, {"QVTS_LEAF_NSPLIT": "2"}, {"QVTS_LEAF_TMA": "0"},
+                                 {"QVTS_CORRECT_STAGE": "0"}, {"QVTS_BAND_ROWS": "8"}],
+                         ids=["hist_leaf", "leaf_split", "leaf_cp_async", "correct_unstaged", "band_rows_8"])
+def test_alternative_kernel_paths_match_oracle(Q, env, monkeypatch):
+    """Every run-time kernel option the library keeps (read per call; model-level for the band
+    height) is a different code path to the same numbers: the k_hist<leaf> leaf level instead of
+    k_leaf, k_leaf with its bands split over CTAs (band records summed by k_reduce), k_leaf's
+    4-byte cp.async staging instead of TMA, k_correct without row staging, and 8-row hist bands.
+    On a 160 x 96 map (two k_leaf bands, several hist bands, 16-byte rows) each runs the whole
+    depth-3 tree against the oracle element by element with flagged-draw replay (c.5)."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    gm = W.random_map(160, 96, 0.2, seed=21)
+    run_parity(Q, gm, W.A8, 3, 8, W.random_belief(gm, 13), seed=5, step=1)
