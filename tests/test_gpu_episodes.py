@@ -107,3 +107,23 @@ def test_episode_sharding_is_rank_invariant(Q):
     rec = total.reshape(5, 6)
     assert np.array_equal(rec[:, 1], ref["steps"]) and np.array_equal(rec[:, 0], ref["outcome"])
     assert np.allclose(rec[:, 5], ref["disc_return"], rtol=0, atol=0)
+
+
+def test_episode_waves_do_not_change_records(Q, monkeypatch):
+    """Live episodes are planned in waves sized to the free memory (QVTS_EPISODE_WAVE, read per
+    call, forces the size); randomness is keyed by (seed, episode, step, path), so one episode per
+    wave, three per wave and all at once give the same records bit for bit."""
+    gm = W.random_map(12, 13, 0.2, seed=6)
+    g = Q.Model(gm, action_mask=W.A9)
+    g.value_iteration()
+    recs = []
+    for wave in (None, "1", "3"):
+        if wave is None:
+            monkeypatch.delenv("QVTS_EPISODE_WAVE", raising=False)
+        else:
+            monkeypatch.setenv("QVTS_EPISODE_WAVE", wave)
+        rec, _ = g.run_episodes(7, max_steps=25, planner=0, depth=2, n_samples=4, seed=11)
+        recs.append(rec)
+    for r in recs[1:]:
+        for k in ("outcome", "steps", "collisions", "disc_return", "x0"):
+            assert np.array_equal(r[k], recs[0][k]), k

@@ -683,3 +683,24 @@ def test_alternative_kernel_paths_match_oracle(Q, env, monkeypatch):
         monkeypatch.setenv(k, v)
     gm = W.random_map(160, 96, 0.2, seed=21)
     run_parity(Q, gm, W.A8, 3, 8, W.random_belief(gm, 13), seed=5, step=1)
+
+
+def test_belief_update_batch_two_pass_tile_size(Q, monkeypatch):
+    """The two-pass batched update with 256-group tiles (QVTS_BU_GROUPS, read per call; default
+    2048) gives the cluster kernel's results on the C3 map: P to 1e-8, b' to 1e-7 (different
+    fp32 prediction forms, Eq. 3)."""
+    gm = W.CONFIGS["C3"]["map"]()
+    g = Q.Model(gm, action_mask=W.A8)
+    nb = 9
+    B = np.stack([W.random_belief(gm, 700 + i) for i in range(nb)]).astype(np.float32)
+    acts = np.array([g.action_ids[i % g.n_actions] for i in range(nb)], np.int32)
+    zs = np.array([(3 * i) % 16 for i in range(nb)], np.int32)
+    out1 = torch.empty((nb, gm.occupancy.size), dtype=torch.float32, device="cuda")
+    out2 = torch.empty_like(out1)
+    p1 = g.belief_update_batch(dev(B), acts, zs, out1)
+    monkeypatch.setenv("QVTS_BU_CLUSTER", "0")
+    monkeypatch.setenv("QVTS_BU_GROUPS", "256")
+    p2 = g.belief_update_batch(dev(B), acts, zs, out2)
+    assert np.max(np.abs(np.asarray(p1) - np.asarray(p2))) <= 1e-8
+    assert float((out1 - out2).abs().max()) <= 1e-7
+    g.close()
